@@ -1,0 +1,333 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the passage it follows.  None of them re-calls the oracle's own
+routine to produce an expected value: expected values are closed forms, hand
+numbers (tests/golden/), brute-force enumeration (tests/refcheck.py), an
+independent definitional Elmore, or invariants.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import refcheck as rc
+from gen import synth
+from helpers import fixture_design, golden, randomize_state, rebuild_demand, single_net, tiny_pool
+from oracle import oracle
+
+REL = 1e-12
+
+
+def rel_close(a, b, tol):
+    return abs(a - b) <= tol * max(1.0, abs(a), abs(b))
+
+
+# ------------------------------------------------------------------ O4 tables
+def test_eq3_marginal_tables_closed_form():
+    """Eq. (3): marginal at d = c is e^s - 1; sums telescope to the state."""
+    g = golden("closed_forms.json")["eq3"]
+    d = synth.empty_design(4, 4, 4)
+    VR, Mp, Mz, ravg = oracle.tables(d)
+    z = -d.delta_lo                     # index of delta = 0
+    assert Mp[z] == pytest.approx(g["marginal_at_d_eq_c_cpos"], rel=1e-15)
+    assert Mz[z] == pytest.approx(g["marginal_at_d_eq_c_czero"], rel=1e-15)
+    # state e^{1.5*2} - e^0 = sum of marginals for delta = 0, 1 (c = 0, d: 0 -> 2)
+    assert Mz[z] + Mz[z + 1] + 1.0 == pytest.approx(g["state_c0_d2"], rel=1e-14)
+    # c > 0, d = c - 4: e^{-2} = 1 - sum_{delta=-4}^{-1} M(delta)
+    assert 1.0 - Mp[z - 4:z].sum() == pytest.approx(g["state_d_eq_c_minus_4_cpos"], rel=1e-12)
+    assert np.all(Mp > 0) and np.all(np.diff(Mp) > 0) and np.all(Mz[z:] > Mp[z:])   # c = 0 implies d - c >= 0
+
+
+def test_via_resistance_table():
+    """VR[a][b] = sum of vr over the crossed cuts (Alg. 2 input vr)."""
+    d = synth.empty_design(4, 4, 4)
+    d.vr = np.array([0.010, 0.008, 0.006])
+    VR, _, _, ravg = oracle.tables(d)
+    assert VR[0][0] == 0.0 and VR[2][2] == 0.0
+    assert VR[0][3] == pytest.approx(0.024, rel=1e-15) and VR[3][0] == VR[0][3]
+    assert VR[1][2] == pytest.approx(0.008, rel=1e-15)
+    assert ravg == pytest.approx(np.mean(d.r), rel=1e-15)
+
+
+# ------------------------------------------------------------------ O2 Eq. (4)
+def test_eq4_pin_weight_values():
+    """Eq. (4) logistic, k = 10, b = 0.3 (reading R1) and Fig. 7 (l.305-308)."""
+    g = golden("closed_forms.json")["eq4"]
+    d = synth.empty_design(4, 4, 4)
+    assert oracle.pin_weight(d, -500.0, -500.0) == pytest.approx(g["ratio_1"], rel=1e-15)
+    assert oracle.pin_weight(d, -150.0, -500.0) == pytest.approx(g["ratio_b"], rel=1e-15)
+    assert oracle.pin_weight(d, 0.0, -500.0) == pytest.approx(g["ratio_0"], rel=1e-15)
+    assert oracle.pin_weight(d, -1.0, g["fig7_wns"]) == pytest.approx(g["fig7_sink_minus1"], rel=1e-14)
+    assert oracle.pin_weight(d, -100.0, g["fig7_wns"]) == pytest.approx(g["fig7_sink_minus100"], rel=1e-15)
+    # WNS >= 0: floor weight (reading R2)
+    assert oracle.pin_weight(d, 5.0, 0.0) == d.w_floor
+
+
+# ------------------------------------------------------------------ O1 tree
+def test_fig6_node_counts():
+    """Fig. 6: net 1 (straight 2-pin) -> 2 nodes; net 2 -> 4 route nodes + 1 bend = 5,
+    with the Fig. 8 topology 3->4, 4->5, 4->6, 6->7 (l.452-453; reading R34)."""
+    g = golden("closed_forms.json")["fig6"]
+    d = synth.empty_design(8, 8, 4)
+    n1 = dict(pins=[(0, 5, 0, 1.0, -1.0), (4, 5, 0, 1.0, -1.0)], segs=[(0, 5, 4, 5)])
+    # node3 = (0,0) driver, node4 = (2,0) Steiner, node5 = (4,0) sink, node6 = (2,2) bend, node7 = (4,2) sink
+    n2 = dict(pins=[(0, 0, 0, 1.0, -1.0), (4, 0, 0, 1.0, -1.0), (4, 2, 0, 1.0, -1.0)],
+              segs=[(0, 0, 4, 0), (2, 0, 2, 2), (2, 2, 4, 2)])
+    d = synth.with_nets(d, [n1, n2])
+    t1, t2 = oracle.tree(d, 0), oracle.tree(d, 1)
+    assert len(t1) == g["net1_nodes"] and len(t2) == g["net2_nodes"]
+    pos = {(int(r[0]), int(r[1])): i for i, r in enumerate(t2)}
+    par = {k: (int(t2[v][2])) for k, v in pos.items()}
+    at = {i: k for k, i in pos.items()}
+    assert par[(0, 0)] == -1
+    assert at[par[(2, 0)]] == (0, 0)          # 3 -> 4
+    assert at[par[(4, 0)]] == (2, 0)          # 4 -> 5
+    assert at[par[(2, 2)]] == (2, 0)          # 4 -> 6 (the added bend)
+    assert at[par[(4, 2)]] == (2, 2)          # 6 -> 7
+    heights = {k: int(t2[v][5]) for k, v in pos.items()}
+    assert heights == {(0, 0): 3, (2, 0): 2, (4, 0): 0, (2, 2): 1, (4, 2): 0}
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_tree_matches_independent_builder(seed):
+    """O1 vs an independent graph-walk implementation (tests/refcheck.py) on generated nets:
+    same node set, parent links, run lengths; every edge straight; sum len = unit edges."""
+    d = synth.generate(n_nets=300, X=24, Y=24, L=6, seed=seed, pin_max=16)
+    for net in range(d.n_nets):
+        t = oracle.tree(d, net)
+        ref = rc.build_tree(rc.net_pins(d, net), rc.net_segs(d, net))
+        assert len(t) == len(ref)
+        mine = {(int(r[0]), int(r[1])): (int(r[3]), int(r[4])) for r in t}
+        theirs = {(n["x"], n["y"]): (n["len"], n["edir"]) for n in ref}
+        assert mine == theirs
+        assert sum(int(r[3]) for r in t) == len(rc.unit_edges(rc.net_segs(d, net)))
+
+
+def test_route_errors():
+    """Route validation (SURVEY §8(b) errors): cycle, pin off-route, diagonal segment."""
+    d = synth.empty_design(8, 8, 4)
+    bad = [dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2)]),
+           dict(pins=[(0, 0, 0, 1, 0), (3, 3, 0, 1, 0)], segs=[(0, 0, 2, 0)]),
+           dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 2)])]
+    msgs = ["not a tree", "not on the route", "axis-aligned"]
+    for n, m in zip(bad, msgs):
+        e = synth.with_nets(synth.empty_design(8, 8, 4), [n])
+        with pytest.raises(oracle.OracleError, match=m):
+            oracle.run(e)
+
+
+# ------------------------------------------------------------------ O9 Elmore
+@pytest.mark.parametrize("name", ["A", "B"])
+def test_elmore_hand_fixtures(name):
+    """Hand-computed Elmore on 2-3 segment nets (tests/golden/elmore_fixtures.json)."""
+    G = golden("elmore_fixtures.json")
+    fx = G[name]
+    d = fixture_design(fx, G["tech"])
+    r = oracle.run(d)
+    assert r["net_cap"][0] == pytest.approx(fx["net_cap"], rel=1e-12)
+    assert r["net_rc"][0] == pytest.approx(fx["net_rc"], rel=1e-12)
+    if name == "A":
+        assert r["sink_delay"][1] == pytest.approx(fx["delay_sink"], rel=1e-12)
+        assert r["sink_delay"][1] == pytest.approx(sum(fx["terms"].values()), rel=1e-12)
+    else:
+        assert r["sink_delay"][1] == pytest.approx(fx["delay_A"], rel=1e-12)
+        assert r["sink_delay"][2] == pytest.approx(fx["delay_B"], rel=1e-12)
+    assert r["sink_delay"][0] == 0.0
+    assert int((r["vias"][:, 3] - r["vias"][:, 2]).sum()) == fx["via_cuts"]
+    assert int(r["wire_dem"].sum()) == fx["wirelength"]
+
+
+@pytest.mark.parametrize("seed,L", [(21, 4), (22, 6)])
+def test_elmore_vs_definitional(seed, L):
+    """Canonical fast form vs the O(n^2) explicit-RC-graph Elmore within 1e-9 relative."""
+    d = tiny_pool(seed, L, n=150, X=10, Y=10, pin_max=8)
+    r = oracle.run(d)
+    for net in range(d.n_nets):
+        pins, nodes = rc.net_pins(d, net), rc.build_tree(rc.net_pins(d, net), rc.net_segs(d, net))
+        w = r["wires"][r["wire_ptr"][net]:r["wire_ptr"][net + 1]]
+        v = r["vias"][r["via_ptr"][net]:r["via_ptr"][net + 1]]
+        lay = rc.solution_layers(nodes, w)
+        spans = []
+        vmap = {(int(a[0]), int(a[1])): (int(a[2]), int(a[3])) for a in v}
+        for i, nd in enumerate(nodes):
+            l = pins[0][2] if i == 0 else lay[i]
+            spans.append(vmap.get((nd["x"], nd["y"]), (l, l)))
+        delays, ncap, nrc = rc.elmore_definitional(d, pins, nodes, lay, spans)
+        p0 = d.pin_ptr[net]
+        for q in range(len(pins)):
+            assert rel_close(r["sink_delay"][p0 + q], delays[q], 1e-9)
+        assert rel_close(r["net_cap"][net], ncap, 1e-9)
+        assert rel_close(r["net_rc"][net], nrc, 1e-9)
+
+
+# ------------------------------------------------------------------ O6 DP
+def _dp_cases(seed, L, rdrv_mode=0, max_nodes=6, want=60):
+    pool = tiny_pool(seed, L, n=500, rdrv_mode=rdrv_mode)
+    rng = np.random.default_rng(seed)
+    out = []
+    for net in range(pool.n_nets):
+        nodes = rc.build_tree(rc.net_pins(pool, net), rc.net_segs(pool, net))
+        if 2 <= len(nodes) <= max_nodes:
+            out.append((randomize_state(single_net(pool, net), rng), nodes))
+        if len(out) >= want:
+            break
+    return out
+
+
+@pytest.mark.parametrize("seed,L", [(31, 4), (32, 4), (33, 6)])
+def test_dp_exact_when_wd_zero(seed, L):
+    """W_D = 0: the objective is separable, so Alg. 3/4 is an exact tree DP.
+    Cost equals the brute-force minimum; layers equal wherever that minimum is unique."""
+    for d, nodes in _dp_cases(seed, L):
+        d.W_D = 0.0
+        r = oracle.run(d)
+        best, arg, second = rc.brute_force(d, 0, nodes)
+        assert rel_close(r["net_cost"][0], best, REL), (r["net_cost"][0], best)
+        if second > best * (1 + 1e-9) + 1e-12:
+            assert rc.solution_layers(nodes, r["wires"])[1:] == list(arg[1:])
+
+
+def test_dp_exact_on_depth1_trees():
+    """Depth-1 trees (root + leaf sons), any weights, r_drv = 0: no after-effect, DP = optimum (SURVEY c.5)."""
+    n_checked = 0
+    for seed in (41, 42, 43):
+        for d, nodes in _dp_cases(seed, 6, max_nodes=5, want=200):
+            if any(nd["kids"] for nd in nodes[1:]):
+                continue
+            d.W_D = 100.0
+            r = oracle.run(d)
+            best, arg, second = rc.brute_force(d, 0, nodes)
+            assert rel_close(r["net_cost"][0], best, REL)
+            if second > best * (1 + 1e-9) + 1e-12:
+                assert rc.solution_layers(nodes, r["wires"])[1:] == list(arg[1:])
+            n_checked += 1
+    assert n_checked > 50
+
+
+@pytest.mark.parametrize("seed,L,rdrv", [(51, 4, 0), (52, 6, 1), (53, 4, 1)])
+def test_dp_cost_reconstruction_and_lower_bound(seed, L, rdrv):
+    """W_D > 0 (heuristic look-ahead): (i) re-evaluating the emitted solution from
+    scratch reproduces f[root]; (ii) f[root] >= the brute-force optimum."""
+    for d, nodes in _dp_cases(seed, L, rdrv_mode=rdrv):
+        d.W_D = 100.0
+        r = oracle.run(d)
+        lay = rc.solution_layers(nodes, r["wires"])
+        recon = rc.assignment_cost(d, 0, nodes, lay)
+        assert rel_close(r["net_cost"][0], recon, REL), (r["net_cost"][0], recon)
+        best, _, _ = rc.brute_force(d, 0, nodes)
+        assert r["net_cost"][0] >= best * (1 - 1e-12)
+
+
+def test_straight_two_pin_choice_by_hand():
+    """Straight 2-pin net, W_D = W_CAP = 0 (SURVEY c.5 'O6 special case'): the chosen layer minimises
+    V_root + W_CONG*ofw[j]*S_j + V_sink over legal j, lowest j on ties.  Hand-built case: L = 6,
+    H layers 0, 2, 4; layer 0 congested, so the cheapest total is decided by via cuts vs ofw."""
+    d = synth.empty_design(8, 8, 6, cap_wire=2, cap_via=16)
+    d.W_D, d.W_CAP = 0.0, 0.0
+    d = synth.with_nets(d, [dict(pins=[(1, 3, 0, 1.0, -5.0), (5, 3, 0, 1.0, -5.0)], segs=[(1, 3, 5, 3)])])
+    d.wire_dem0 = np.zeros(d.wire_cap.shape[0], np.int32)
+    # hand values: M_pos(d-c) = e^{0.5(d-c+1)} - e^{0.5(d-c)}; via kappa = 0.05 + ofw[k] * M_pos(-16)
+    Mpos = lambda dl: math.exp(0.5 * (dl + 1)) - math.exp(0.5 * dl)
+    kap = [0.05 + (2.0 if k < 2 else 1.0) * Mpos(-16) for k in range(5)]
+    cands = {}
+    for j, ofw in ((0, 2.0), (2, 1.0), (4, 1.0)):
+        S = 4 * Mpos(0 - 2)
+        cands[j] = 2 * sum(kap[:j]) + ofw * S
+    want = min(cands, key=lambda j: (cands[j], j))
+    r = oracle.run(d)
+    assert int(r["wires"][0][4]) == want
+    assert r["net_cost"][0] == pytest.approx(cands[want], rel=1e-12)
+    # now congest layer 0 heavily: the via stack becomes worth paying
+    e = synth.with_nets(synth.empty_design(8, 8, 6, cap_wire=2, cap_via=16),
+                        [dict(pins=[(1, 3, 0, 1.0, -5.0), (5, 3, 0, 1.0, -5.0)], segs=[(1, 3, 5, 3)])])
+    e.W_D, e.W_CAP = 0.0, 0.0
+    e.wire_dem0 = np.zeros(e.wire_cap.shape[0], np.int32)
+    e.wire_dem0[: (e.X - 1) * e.Y] = 12          # layer 0: d - c = 10
+    r2 = oracle.run(e)
+    S0 = 4 * Mpos(10)
+    cands[0] = 2.0 * S0
+    want2 = min(cands, key=lambda j: (cands[j], j))
+    assert want2 != 0 and int(r2["wires"][0][4]) == want2
+
+
+def test_unit_weight_identity_cost_equals_net_rc():
+    """W_CAP = W_CONG = W_VIA = 0, W_D = 1, WNS >= 0 with w_floor = 1: f[root] == net_rc bitwise
+    (SURVEY c.5 'O6 vs O9'), and for single-sink nets without spurs it is the sink's Elmore delay."""
+    d = tiny_pool(61, 6, n=300, X=12, Y=12, pin_max=6)
+    d.W_CAP = d.W_CONG = d.W_VIA = 0.0
+    d.W_D = 1.0
+    d.wns, d.w_floor = 0.0, 1.0
+    r = oracle.run(d)
+    assert np.array_equal(r["net_cost"], r["net_rc"])
+    two = np.where(np.diff(d.pin_ptr) == 2)[0]
+    for net in two:
+        assert r["net_cost"][net] == pytest.approx(r["sink_delay"][d.pin_ptr[net] + 1], rel=1e-9, abs=1e-15)
+
+
+# ------------------------------------------------------------------ O8 commit + projection
+def test_commit_invariants_and_projection():
+    """Commit: final grid == rebuild from the emitted solution; wire
+    demand added == wirelength; via demand added == layer changes; projection == the 2D input."""
+    d = synth.make_config(1)
+    r = oracle.run(d)
+    wd, vd = rebuild_demand(d, r["wires"], r["vias"])
+    assert np.array_equal(wd, r["wire_dem"]) and np.array_equal(vd, r["via_dem"])
+    assert int(r["wire_dem"].sum()) == d.unit_edges_total()
+    assert int(r["via_dem"].sum()) == int((r["vias"][:, 3] - r["vias"][:, 2]).sum())
+    for net in range(d.n_nets):
+        w = r["wires"][r["wire_ptr"][net]:r["wire_ptr"][net + 1]]
+        proj = rc.unit_edges([tuple(int(t) for t in x[:4]) for x in w])
+        assert proj == rc.unit_edges(rc.net_segs(d, net))
+        for x in w:      # wires respect layer direction
+            assert d.dir[x[4]] == (0 if x[1] == x[3] else 1)
+    v = r["vias"]
+    assert np.all(v[:, 3] > v[:, 2])
+
+
+# ------------------------------------------------------------------ batching recurrence
+def test_batch_recurrence_vs_bruteforce():
+    """Conflict-free layering: batch(j) = 1 + max batch over earlier-priority nets
+    whose footprints (unit edges U LA-node GCells) intersect j's, 0 if none -- by brute force."""
+    d = synth.make_config(1)
+    r = oracle.run(d, solution=False, grids=False, timing=False)
+    order = sorted(range(d.n_nets), key=lambda i: (int(d.order_key[i]), i))
+    fps = {}
+    for net in range(d.n_nets):
+        nodes = rc.build_tree(rc.net_pins(d, net), rc.net_segs(d, net))
+        fps[net] = {("e",) + e for e in rc.unit_edges(rc.net_segs(d, net))} | {("g", n["x"], n["y"]) for n in nodes}
+    want = {}
+    for k, j in enumerate(order):
+        b = 0
+        for i in order[:k]:
+            if fps[i] & fps[j]:
+                b = max(b, want[i] + 1)
+        want[j] = b
+    assert [int(r["batch_of"][j]) for j in range(d.n_nets)] == [want[j] for j in range(d.n_nets)]
+
+
+def _tie_design(pins, segs, L=6):
+    """Tie-heavy setting (SURVEY c.5 'Test inputs that provoke ties'): identical r, c, ofw on all
+    layers, W_VIA = W_CONG = W_D = 0, so many layer choices and spans cost exactly the same."""
+    d = synth.empty_design(8, 8, L)
+    d.r = np.full(L, 0.005)
+    d.c = np.full(L, 0.2)
+    d.ofw = np.ones(L)
+    d.W_VIA = d.W_CONG = d.W_D = 0.0
+    return synth.with_nets(d, [dict(pins=pins, segs=segs)])
+
+
+def test_tie_break_son_lowest_layer():
+    """Son argmin ties go to the lowest layer j (R21; Alg. 3 l.395 'argmin' with ties unspecified).
+    Root pins on layers 0 and 2 force the root span to cover [0, 2], where H layers 0 and 2 tie."""
+    d = _tie_design([(0, 0, 0, 1.0, -5.0), (0, 0, 2, 1.0, -5.0), (4, 0, 0, 1.0, -5.0)], [(0, 0, 4, 0)])
+    r = oracle.run(d)
+    assert int(r["wires"][0][4]) == 0
+
+
+def test_tie_break_span_key():
+    """Span ties on G' go to the smaller t - b, then the lower b (R21).  Pins on the V layer 1 at both
+    ends of an H wire: spans (0,1) and (1,2) tie on cost and size; the lower b wins -> wire on layer 0."""
+    d = _tie_design([(0, 0, 1, 1.0, -5.0), (4, 0, 1, 1.0, -5.0)], [(0, 0, 4, 0)])
+    r = oracle.run(d)
+    assert int(r["wires"][0][4]) == 0
+    assert [tuple(int(t) for t in v) for v in r["vias"]] == [(0, 0, 0, 1), (4, 0, 0, 1)]
