@@ -1,0 +1,199 @@
+/*
+ * la.h -- C ABI of the B200-native GAP-LA layer-assignment hot path.
+ *
+ * Paper: "GAP-LA: GPU-Accelerated Performance-Driven Layer Assignment",
+ * arXiv 2507.13375 (cited below as PAPER l.<line of PAPER.md>).
+ *
+ * The calls follow the paper's problem statement: layer assignment "takes a
+ * GCell grid graph with GCell edge capacity, a netlist and an optimized 2D
+ * global routing solution as input and assigns each 2D routing segment to a
+ * certain layer to generate a 3D global routing solution" whose projection is
+ * the input (PAPER §II-B l.132-133, §II-D l.150-152).  The per-batch loop is
+ * Alg. 2 (l.335-354): for every batch, bottom-up getSubtreeCandidate (Alg. 3,
+ * l.355-411) then top-down traceBackSolution (Alg. 4, l.418-435); demand is the
+ * Alg. 2 input "demand map D and capacity map C" (l.343), committed between
+ * batches (§III-A l.224-226).  Net delay is Elmore on the pi-model RC tree
+ * (§II-C l.146, §III-D l.443-444).  Exact operand-level definitions: DESIGN.md
+ * §3 (= SURVEY.md §8(c) c.3, O1-O9), readings of garbled / silent passages:
+ * DESIGN.md §4.
+ *
+ * Conventions (all calls):
+ *  - Return la_status: LA_OK (0) or a negative error; no exception crosses the
+ *    ABI.  la_last_error() returns a thread-local message (net id / segment
+ *    index for route errors).
+ *  - Every input pointer is caller-owned HOST memory, read only during the call
+ *    (the library copies what it needs).  The library owns all device memory
+ *    and the context.  Output pointers are caller-allocated HOST buffers.
+ *  - Results are in input net / pin order, never in batch order.
+ *  - Units: kOhm, fF, ps (kOhm x fF = ps); GCell pitch = 1.
+ *  - Call order: la_init_grid -> la_load_nets -> for k = 0..n_batches-1:
+ *    la_assign_batch(k), la_commit_demand(k) -> la_eval_timing / la_get_*.
+ *    Violations return LA_ESTATE.  LA_ECUDA / LA_ENCCL poison the context:
+ *    every later call except la_destroy returns LA_ESTATE.
+ *  - la_assign_batch / la_commit_demand / la_assign_all only ENQUEUE work on
+ *    the context's stream (no host synchronisation); la_sync, la_eval_timing,
+ *    la_get_* synchronise.  Asynchronous CUDA faults surface at the next
+ *    synchronising call.
+ *  - Multi-GPU (world > 1): one process and one context per GPU.
+ *    la_load_nets, la_commit_demand, la_eval_timing and la_get_solution are
+ *    collective (every rank calls them with the same arguments).
+ *  - Nothing on the compute path runs on the host: if the CUDA device or the
+ *    kernels are unavailable the calls fail (LA_ECUDA); there is no CPU
+ *    fallback.
+ */
+#ifndef GAPLA_LA_H
+#define GAPLA_LA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct la_ctx la_ctx;
+
+typedef enum {
+    LA_OK = 0,
+    LA_EINVAL = -1,  /* bad descriptor field or invalid route (see la_init_grid / la_load_nets) */
+    LA_ESTATE = -2,  /* call-order violation, or context poisoned by an earlier CUDA/NCCL error */
+    LA_ENOMEM = -3,  /* device or host allocation failed                                        */
+    LA_ECUDA = -4,   /* CUDA runtime error (context poisoned)                                    */
+    LA_ENCCL = -5,   /* NCCL error (context poisoned)                                            */
+    LA_ERANGE = -6   /* batch index out of range, or an output buffer too small                  */
+} la_status;
+
+/* Grid, technology and weights.  Alg. 2 inputs. */
+typedef struct {
+    int32_t X, Y, L;            /* GCells along x and y; metal layers, 2 <= L <= 16; X, Y <= 65535   */
+    const uint8_t *dir;         /* [L] 0 = H (wires along x), 1 = V                                   */
+    const uint8_t *routable;    /* [L] 0/1; each direction needs >= 1 routable layer                  */
+    const double *r, *c;        /* [L] wire R (kOhm) and C (fF) per GCell pitch        */
+    const double *vr;           /* [L-1] via R (kOhm) of the cut between layer k and k+1 (l.340)     */
+    const double *ofw;          /* [L] Eq. (3) overflow weight ofw(l) (l.182)                          */
+    double s_pos, s_zero;       /* Eq. (3) exponent: 0.5 if c > 0, 1.5 if c = 0 (l.182)               */
+    const int32_t *wire_cap;    /* wire-edge capacity, API layout: layers l = 0..L-1 concatenated;   */
+                                /* within layer l the edges keyed by their lower endpoint (x, y),    */
+                                /* row-major [y][x]: (X-1)*Y entries if H, X*(Y-1) if V               */
+    const int32_t *via_cap;     /* via-cut capacity [(L-1)][Y][X], cut k between layers k and k+1    */
+    const int32_t *wire_dem0;   /* initial wire demand, same layout; NULL = all 0                     */
+    const int32_t *via_dem0;    /* initial via-cut demand, same layout; NULL = all 0                  */
+    double W_D, W_CAP, W_CONG;  /* Alg. 2 weights w^d, w^cap, w^cong (l.338)                           */
+    double W_VIA;               /* per-via-cut cost inside ViaCong (Alg. 3 l.377; reading R11)         */
+    double r_avg;               /* look-ahead unit R (l.452); NaN = mean of routable r                 */
+    double logit_k, logit_b;    /* Eq. (4): k = 10, b = 0.3 (l.314)                                    */
+    double w_floor;             /* pin weight used when WNS >= 0 (reading R2)                          */
+    int32_t delta_lo, delta_hi; /* Eq. (3) marginal-table domain for d - c (reading R20)               */
+    int32_t device;             /* CUDA device ordinal of this process                                 */
+    int32_t rank, world;        /* this process's rank, number of ranks (1..8)                          */
+    const void *nccl_id;        /* 128-byte ncclUniqueId created by rank 0; NULL when world == 1       */
+    void *stream;               /* cudaStream_t to enqueue on; NULL = library-owned stream             */
+} la_grid_desc;
+
+/* Netlist pins and the 2D routing solution. */
+typedef struct {
+    int64_t n_nets;
+    const int64_t *pin_ptr;     /* [n_nets+1] CSR over pins; pin 0 of each net is its driver          */
+    const int32_t *pin_x, *pin_y;   /* GCell of each pin                                              */
+    const uint8_t *pin_layer;   /* < L                                                                  */
+    const double *pin_cap;      /* fF (driver entry ignored)                                            */
+    const double *pin_slack;    /* ps (driver entry ignored), Eq. (4) input                             */
+    const int64_t *seg_ptr;     /* [n_nets+1] CSR into seg_xy                                            */
+    const int32_t *seg_xy;      /* [n_segs][4] x1 y1 x2 y2, axis-aligned 2D segments (may overlap)       */
+    const double *r_drv;        /* [n_nets] kOhm, ur(root) seed (reading R6); NULL = 0                   */
+    const int64_t *order_key;   /* [n_nets] priority, smaller = earlier, ties by net index; NULL = index */
+    double wns;                 /* design WNS (ps), Eq. (4)                                              */
+} la_net_desc;
+
+/* Counters of the loaded instance (exact, from the built forest). */
+typedef struct {
+    int64_t n_nets, n_pins, n_nodes, n_sinks;
+    int64_t wirelength;         /* unit 2D edges over all nets                                          */
+    int64_t footprint;          /* (element, net) pairs sorted by the batching pass                      */
+    int32_t n_batches, max_height;
+    int64_t max_batch_nets, max_net_nodes;
+    int64_t via_cuts;           /* after assignment (valid once la_get_solution / la_eval_timing ran)  */
+    int64_t launches;           /* kernels launched by la_assign_* / la_commit_demand / la_eval_timing */
+    double load_ms;             /* host tree build + upload inside la_load_nets                         */
+    double batch_ms;            /* GPU batching pass (sort + Kahn layering) inside la_load_nets         */
+} la_stats;
+
+/* Create a context: validate the grid, allocate the packed device demand
+ * planes, build the Eq. (3) marginal tables and the via-R table, set up NCCL
+ * when world > 1.
+ * Errors: LA_EINVAL when L < 2 or L > 16, X or Y <= 1 or > 65535, any r, c,
+ * vr, ofw, W_*, s_pos, s_zero or capacity negative, delta_lo > delta_hi, a
+ * direction without a routable layer, bad rank/world; LA_ECUDA / LA_ENCCL on
+ * device errors; LA_ENOMEM. */
+la_status la_init_grid(const la_grid_desc *g, la_ctx **out);
+
+/* Build the LA directed trees (PAPER §III-B; DESIGN §3 O1), weights Eq.(4)/(5)
+ * (O2) and upstream-R estimates (O3) on the host, upload the batch-major
+ * forest, and run the GPU conflict-free batching pass (DESIGN §5 K1/K2).
+ * Writes the number of batches.  Collective when world > 1.
+ * Errors: LA_EINVAL for a pin layer >= L, a pin or segment outside the grid,
+ * a non-axis-aligned segment, a route that is not a tree, a pin GCell not on
+ * the route, a net without pins (message names the net); LA_ESTATE if nets
+ * were already loaded. */
+la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches);
+
+/* Alg. 3 + Alg. 4 for batch k on this rank's shard of the batch: bottom-up
+ * candidate DP with look-ahead, then backtrack.  Enqueue only.
+ * Errors: LA_ERANGE (k out of range), LA_ESTATE (k is not the next batch). */
+la_status la_assign_batch(la_ctx *ctx, int32_t batch);
+
+/* Commit batch k's chosen wires and via cuts into the demand grid (integer
+ * atomics); with world > 1 first reconcile every rank's decisions for batch k
+ * (NCCL all-reduce over the batch's packed decisions), so every replica applies
+ * every commit.  Collective.  Enqueue only.
+ * Errors: LA_ESTATE unless batch k was just assigned. */
+la_status la_commit_demand(la_ctx *ctx, int32_t batch);
+
+/* Convenience: la_assign_batch + la_commit_demand for every remaining batch
+ * (the whole Alg. 2 loop), enqueued back to back.  Collective. */
+la_status la_assign_all(la_ctx *ctx);
+
+/* Elmore delay / downstream capacitance over the 3D RC trees of every net
+ * (DESIGN §3 O9).  Outputs (any may be NULL): sink_delay[n_pins] in input pin
+ * order (driver slots 0), net_cap[n_nets] (wire + sink C, fF), net_rc[n_nets]
+ * (sum over resistors of R x downstream C, ps).  Requires every batch
+ * committed.  Synchronises.  Collective. */
+la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, double *net_rc);
+
+/* The 3D solution in input net order (Alg. 2 output GRS-3D, l.344).  Pass
+ * NULL arrays to query the counts.  Per net, wires [x1 y1 x2 y2 layer] with
+ * x1 <= x2, y1 <= y2 sorted lexicographically, one per LA-tree edge; vias
+ * [x y b t] (t > b) sorted, one per via stack; net_cost[i] = f[root][p_drv]
+ * (Alg. 4 l.426).  wire_ptr / via_ptr are CSR offsets [n_nets+1].
+ * Synchronises.  Collective. */
+la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias,
+                          int64_t *wire_ptr, int32_t *wires,
+                          int64_t *via_ptr, int32_t *vias, double *net_cost);
+
+/* Current demand in the API layout of la_grid_desc (either may be NULL). */
+la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem);
+
+/* Conflict-free batch id of every net, input order. */
+la_status la_get_batches(la_ctx *ctx, int32_t *batch_of);
+
+/* Restore the initial demand and rewind to batch 0 (keeps the loaded forest),
+ * so the hot path can be re-run on the same input. */
+la_status la_reset(la_ctx *ctx);
+
+la_status la_get_stats(la_ctx *ctx, la_stats *out);
+
+/* Wait for all enqueued work; surfaces asynchronous CUDA errors. */
+la_status la_sync(la_ctx *ctx);
+
+void la_destroy(la_ctx *ctx);
+
+/* Thread-local message of the last error (never NULL). */
+const char *la_last_error(void);
+
+/* Contiguous shard [*beg, *end) of n items for `rank` of `world` (host-only
+ * helper; the split used for every batch). */
+void la_shard_range(int64_t n, int32_t world, int32_t rank, int64_t *beg, int64_t *end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAPLA_LA_H */

@@ -1,0 +1,1071 @@
+// Host side of the GAP-LA B200 library: the C ABI of include/la.h.
+//
+// Responsibilities: validate inputs, build the Eq. (3) marginal and
+// via-R tables (host libm, reading R20), build every net's layer-assignment
+// directed tree (PAPER §III-B l.264-281), its Eq. (4)/(5) weights (§III-C
+// l.307-320) and upstream-R estimates (§III-D l.452) with a thread pool, lay the
+// forest out batch-major after the GPU conflict-free batching pass, upload, and
+// drive the kernels batch by batch (Alg. 2, l.345-352).  No step of the hot path
+// (DP, backtrack, commit, reconcile, Elmore) runs here.
+//
+// Compiled with -ffp-contract=off: the host-computed fp64 inputs of the DP
+// (weights, ur, tables) follow DESIGN §3 O2-O4 operand by operand.
+#include <algorithm>
+#include <array>
+#include <limits>
+#include <type_traits>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <nccl.h>
+
+#include "la_internal.h"
+
+using namespace gapla;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+la_status set_err(la_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+const double INF = std::numeric_limits<double>::infinity();
+enum { DIR_E = 0, DIR_W = 1, DIR_N = 2, DIR_S = 3 };
+const int DX[4] = {1, -1, 0, 0}, DY[4] = {0, 0, 1, -1};
+const int OPP[4] = {DIR_W, DIR_E, DIR_S, DIR_N};
+
+}  // namespace
+
+struct la_ctx {
+    int device = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool poisoned = false;
+    bool loaded = false;
+    int32_t next_batch = 0;
+    bool pending_commit = false;
+
+    int X = 0, Y = 0, L = 0, LH = 0, LV = 0;
+    std::vector<uint8_t> dir, routable;
+    std::vector<double> r, c, vr, ofw;
+    double s_pos = 0, s_zero = 0, W_D = 0, W_CAP = 0, W_CONG = 0, W_VIA = 0, r_avg = 0;
+    double logit_k = 0, logit_b = 0, w_floor = 0;
+    int32_t delta_lo = 0, delta_hi = 0;
+    std::vector<int64_t> wire_off;            // [L+1] API layout offsets
+    int64_t n_wire_api = 0, n_via_api = 0, n_wire_packed = 0;
+    TechTab tab;
+
+    // device grid
+    int32_t *d_wH = nullptr, *d_wV = nullptr, *d_via = nullptr;
+    int32_t *d_wH0 = nullptr, *d_wV0 = nullptr, *d_via0 = nullptr;
+    int32_t *d_wcap = nullptr, *d_vcap = nullptr;
+    int64_t *d_wire_off = nullptr;
+    double *d_Mpos = nullptr, *d_Mzero = nullptr;
+    TechTab *d_tab = nullptr;
+    DevGrid G{};
+
+    // forest (host copies needed for outputs)
+    int64_t n_nets = 0, n_pins = 0, n_nodes = 0, n_sinks = 0;
+    std::vector<uint32_t> h_xy;
+    std::vector<int32_t> h_len;
+    std::vector<uint8_t> h_edir;
+    std::vector<int64_t> h_net_node0, h_net_id;
+    std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
+    std::vector<int32_t> batch_of_net;        // input order
+    DevForest F{};
+    DevScratch S{};
+    std::vector<void *> dev_allocs;           // forest + scratch
+
+    la_stats stats{};
+    ncclComm_t comm = nullptr;
+
+    ~la_ctx() {
+        for (void *p : dev_allocs) cudaFree(p);
+        void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab};
+        for (void *p : gp) if (p) cudaFree(p);
+        if (comm) ncclCommDestroy(comm);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+la_status cuda_fail(la_ctx *ctx, cudaError_t e, const char *where) {
+    if (ctx) ctx->poisoned = true;
+    return set_err(LA_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                    \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);    \
+    } while (0)
+
+#define NK(call)                                                                          \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess) {                                                          \
+            ctx->poisoned = true;                                                         \
+            return set_err(LA_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+        }                                                                                 \
+    } while (0)
+
+template <class T>
+la_status dev_upload(la_ctx *ctx, T **dst, const T *src, size_t n) {
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16));
+    if (e != cudaSuccess) {
+        ctx->poisoned = true;
+        return set_err(e == cudaErrorMemoryAllocation ? LA_ENOMEM : LA_ECUDA,
+                       std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    ctx->dev_allocs.push_back(p);
+    *dst = static_cast<T *>(p);
+    if (src && n) CK(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return LA_OK;
+}
+
+template <class T>
+la_status dev_alloc(la_ctx *ctx, T **dst, size_t n) {
+    return dev_upload<T>(ctx, dst, nullptr, n);
+}
+
+#define TRY(x)                          \
+    do {                                \
+        la_status s_ = (x);             \
+        if (s_ != LA_OK) return s_;     \
+    } while (0)
+
+bool ok_nonneg(const double *a, int n) {
+    for (int i = 0; i < n; i++)
+        if (!(a[i] >= 0.0)) return false;
+    return true;
+}
+
+// ------------------------------------------------------------ tree builder ---
+// One net's layer-assignment directed tree (DESIGN §3 O1).  Nodes: pin GCells,
+// GCells of degree != 2, and bends; edges are maximal straight runs; root = the
+// driver GCell; children ordered E, W, N, S; sinks keep input order.
+struct BuiltNet {
+    // per node, final order (height ascending, then preorder)
+    std::vector<uint32_t> xy;
+    std::vector<int32_t> kid;      // 4 per node, local final ids, -1
+    std::vector<int32_t> len;
+    std::vector<uint8_t> edir, nkid, nl, nh;
+    std::vector<int32_t> sink0;    // local sink offset
+    std::vector<uint16_t> nsink;
+    std::vector<double> wd, ur;
+    std::vector<uint8_t> height;
+    // sinks grouped by node in final node order
+    std::vector<uint8_t> p_layer;
+    std::vector<double> p_cap, p_w;
+    std::vector<int64_t> p_orig;
+    std::vector<uint64_t> fp;      // footprint elements
+    int64_t wl = 0;
+};
+
+struct Builder {
+    const la_ctx *ctx;
+    const la_net_desc *nd;
+    // scratch
+    std::vector<uint64_t> ek;      // edge keys: gcell * 2 + t  (t = 0 H (x,y)-(x+1,y), 1 V (x,y)-(x,y+1))
+    std::vector<uint64_t> vs;      // vertex gcells
+    std::vector<uint8_t> mask;     // neighbour bits per vertex (1 << dir)
+    std::vector<int32_t> vnode;    // vertex -> preorder node id, -1
+    std::vector<int32_t> stack, bfs;
+    std::vector<uint64_t> pcells;
+    // preorder tree
+    std::vector<int32_t> px, py, ppar, plen, pedir, pheight, pnl, pnh;
+    std::vector<std::vector<int32_t>> pkids;
+    std::vector<std::vector<int64_t>> psinks;
+    std::vector<double> w, ur;
+    std::vector<int32_t> order, finalid;
+
+    int64_t vfind(uint64_t g) const {
+        auto it = std::lower_bound(vs.begin(), vs.end(), g);
+        return (it != vs.end() && *it == g) ? (int64_t)(it - vs.begin()) : -1;
+    }
+    bool has_edge(uint64_t k) const { return std::binary_search(ek.begin(), ek.end(), k); }
+
+    double pin_weight(double slack) const {      // Eq. (4), reading R1/R2
+        if (!(nd->wns < 0.0)) return ctx->w_floor;
+        double x = slack / nd->wns;
+        return 1.0 / (1.0 + std::exp(-ctx->logit_k * (x - ctx->logit_b)));
+    }
+
+    // returns empty string on success, else the error message
+    std::string build(int64_t net, BuiltNet &out) {
+        const int X = ctx->X, Y = ctx->Y, L = ctx->L;
+        const int64_t p0 = nd->pin_ptr[net], p1 = nd->pin_ptr[net + 1];
+        const int64_t s0 = nd->seg_ptr[net], s1 = nd->seg_ptr[net + 1];
+        char buf[200];
+        if (p1 <= p0) return "net " + std::to_string(net) + ": no pins";
+        for (int64_t p = p0; p < p1; p++) {
+            if (nd->pin_x[p] < 0 || nd->pin_y[p] < 0 || nd->pin_x[p] >= X || nd->pin_y[p] >= Y) {
+                std::snprintf(buf, sizeof buf, "net %lld: pin %lld outside the grid", (long long)net, (long long)p);
+                return buf;
+            }
+            if (nd->pin_layer[p] >= L) {
+                std::snprintf(buf, sizeof buf, "net %lld: pin %lld layer >= L", (long long)net, (long long)p);
+                return buf;
+            }
+        }
+        ek.clear();
+        for (int64_t s = s0; s < s1; s++) {
+            const int32_t *q = nd->seg_xy + 4 * s;
+            int x1 = q[0], y1 = q[1], x2 = q[2], y2 = q[3];
+            if (x1 < 0 || y1 < 0 || x2 < 0 || y2 < 0 || x1 >= X || x2 >= X || y1 >= Y || y2 >= Y) {
+                std::snprintf(buf, sizeof buf, "net %lld: segment %lld outside the grid", (long long)net,
+                              (long long)(s - s0));
+                return buf;
+            }
+            if (x1 != x2 && y1 != y2) {
+                std::snprintf(buf, sizeof buf, "net %lld: segment %lld not axis-aligned", (long long)net,
+                              (long long)(s - s0));
+                return buf;
+            }
+            if (y1 == y2) {
+                for (int x = std::min(x1, x2); x < std::max(x1, x2); x++) ek.push_back(((uint64_t)y1 * X + x) * 2);
+            } else {
+                for (int y = std::min(y1, y2); y < std::max(y1, y2); y++) ek.push_back(((uint64_t)y * X + x1) * 2 + 1);
+            }
+        }
+        std::sort(ek.begin(), ek.end());
+        ek.erase(std::unique(ek.begin(), ek.end()), ek.end());
+        const uint64_t g_drv = (uint64_t)nd->pin_y[p0] * X + nd->pin_x[p0];
+        vs.clear();
+        for (uint64_t k : ek) {
+            uint64_t g = k >> 1;
+            vs.push_back(g);
+            vs.push_back((k & 1) ? g + X : g + 1);
+        }
+        if (ek.empty()) vs.push_back(g_drv);
+        std::sort(vs.begin(), vs.end());
+        vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+        for (int64_t p = p0; p < p1; p++) {
+            if (vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]) < 0) {
+                std::snprintf(buf, sizeof buf, "net %lld: pin %lld GCell not on the route", (long long)net, (long long)p);
+                return buf;
+            }
+        }
+        const size_t nv = vs.size();
+        if (nv != ek.size() + 1) {
+            std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
+            return buf;
+        }
+        mask.assign(nv, 0);
+        for (size_t i = 0; i < nv; i++) {
+            uint64_t g = vs[i];
+            int x = (int)(g % X), y = (int)(g / X);
+            uint8_t m = 0;
+            if (x + 1 < X && has_edge(g * 2)) m |= 1 << DIR_E;
+            if (x > 0 && has_edge((g - 1) * 2)) m |= 1 << DIR_W;
+            if (y + 1 < Y && has_edge(g * 2 + 1)) m |= 1 << DIR_N;
+            if (y > 0 && has_edge((g - X) * 2 + 1)) m |= 1 << DIR_S;
+            mask[i] = m;
+        }
+        // connectivity from the driver
+        {
+            std::vector<uint8_t> seen(nv, 0);
+            bfs.clear();
+            int64_t r0 = vfind(g_drv);
+            bfs.push_back((int32_t)r0);
+            seen[r0] = 1;
+            for (size_t h = 0; h < bfs.size(); h++) {
+                uint64_t g = vs[bfs[h]];
+                int x = (int)(g % X), y = (int)(g / X);
+                for (int d = 0; d < 4; d++) {
+                    if (!(mask[bfs[h]] >> d & 1)) continue;
+                    int64_t j = vfind((uint64_t)(y + DY[d]) * X + (x + DX[d]));
+                    if (!seen[j]) { seen[j] = 1; bfs.push_back((int32_t)j); }
+                }
+            }
+            if (bfs.size() != nv) {
+                std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
+                return buf;
+            }
+        }
+        pcells.clear();
+        for (int64_t p = p0; p < p1; p++) pcells.push_back((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]);
+        std::sort(pcells.begin(), pcells.end());
+        auto is_node = [&](size_t vi) {
+            if (std::binary_search(pcells.begin(), pcells.end(), vs[vi])) return true;
+            uint8_t m = mask[vi];
+            if (__builtin_popcount(m) != 2) return true;
+            return !(m == ((1 << DIR_E) | (1 << DIR_W)) || m == ((1 << DIR_N) | (1 << DIR_S)));
+        };
+        // preorder DFS from the root, children E, W, N, S
+        px.clear(); py.clear(); ppar.clear(); plen.clear(); pedir.clear(); pkids.clear(); psinks.clear();
+        vnode.assign(nv, -1);
+        auto add = [&](int x, int y, int par, int ln, int ed, int64_t vi) {
+            px.push_back(x); py.push_back(y); ppar.push_back(par); plen.push_back(ln); pedir.push_back(ed);
+            pkids.emplace_back(); psinks.emplace_back();
+            vnode[vi] = (int32_t)px.size() - 1;
+            return (int32_t)px.size() - 1;
+        };
+        std::vector<int32_t> pre;
+        {
+            int64_t rv = vfind(g_drv);
+            add((int)(g_drv % X), (int)(g_drv / X), -1, 0, -1, rv);
+            stack.assign(1, 0);
+            std::vector<int32_t> vof(1, (int32_t)rv);
+            while (!stack.empty()) {
+                int32_t n = stack.back();
+                stack.pop_back();
+                pre.push_back(n);
+                int32_t kids[4];
+                int nk = 0;
+                for (int d = 0; d < 4; d++) {
+                    if (ppar[n] >= 0 && d == OPP[pedir[n]]) continue;
+                    if (!(mask[vof[n]] >> d & 1)) continue;
+                    int cx = px[n] + DX[d], cy = py[n] + DY[d], ln = 1;
+                    int64_t vi = vfind((uint64_t)cy * X + cx);
+                    while (!is_node(vi)) {
+                        cx += DX[d]; cy += DY[d]; ln++;
+                        vi = vfind((uint64_t)cy * X + cx);
+                    }
+                    int32_t k = add(cx, cy, n, ln, d, vi);
+                    vof.push_back((int32_t)vi);
+                    pkids[n].push_back(k);
+                    kids[nk++] = k;
+                }
+                for (int i = nk - 1; i >= 0; i--) stack.push_back(kids[i]);
+            }
+        }
+        const size_t nn = px.size();
+        // pins: nl/nh over all pins (driver included); sinks in input order
+        pnl.assign(nn, 255);
+        pnh.assign(nn, -1);
+        for (int64_t p = p0; p < p1; p++) {
+            int32_t n = vnode[vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p])];
+            pnl[n] = std::min<int32_t>(pnl[n], nd->pin_layer[p]);
+            pnh[n] = std::max<int32_t>(pnh[n], nd->pin_layer[p]);
+            if (p != p0) psinks[n].push_back(p);
+        }
+        // heights; subtree max sink weight (Eq. 5, reading R3); 0 without sinks (R39)
+        pheight.assign(nn, 0);
+        w.assign(nn, 0.0);
+        for (auto it = pre.rbegin(); it != pre.rend(); ++it) {
+            int32_t n = *it;
+            int h = 0;
+            double m = 0.0;
+            for (int64_t q : psinks[n]) m = std::max(m, pin_weight(nd->pin_slack[q]));
+            for (int32_t k : pkids[n]) { h = std::max(h, pheight[k] + 1); m = std::max(m, w[k]); }
+            pheight[n] = h;
+            w[n] = m;
+        }
+        // ur (reading R6): ur(root) = r_drv, ur(n) = ur(parent) + r_avg * len
+        ur.assign(nn, 0.0);
+        for (int32_t n : pre)
+            ur[n] = (ppar[n] < 0) ? (nd->r_drv ? nd->r_drv[net] : 0.0) : ur[ppar[n]] + ctx->r_avg * plen[n];
+        // final order: height ascending, then preorder
+        order.assign(pre.begin(), pre.end());
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return pheight[a] < pheight[b]; });
+        finalid.assign(nn, -1);
+        for (size_t i = 0; i < nn; i++) finalid[order[i]] = (int32_t)i;
+        out.xy.resize(nn); out.kid.assign(nn * 4, -1); out.len.resize(nn); out.edir.resize(nn);
+        out.nkid.resize(nn); out.nl.resize(nn); out.nh.resize(nn); out.sink0.resize(nn); out.nsink.resize(nn);
+        out.wd.resize(nn); out.ur.resize(nn); out.height.resize(nn);
+        out.p_layer.clear(); out.p_cap.clear(); out.p_w.clear(); out.p_orig.clear();
+        for (size_t i = 0; i < nn; i++) {
+            int32_t n = order[i];
+            out.xy[i] = (uint32_t)px[n] | ((uint32_t)py[n] << 16);
+            for (size_t k = 0; k < pkids[n].size(); k++) out.kid[i * 4 + k] = finalid[pkids[n][k]];
+            out.len[i] = plen[n];
+            out.edir[i] = ppar[n] < 0 ? NO_DIR : (uint8_t)pedir[n];
+            out.nkid[i] = (uint8_t)pkids[n].size();
+            out.nl[i] = (uint8_t)pnl[n];
+            out.nh[i] = (uint8_t)(pnh[n] < 0 ? 255 : pnh[n]);
+            out.wd[i] = ctx->W_D * w[n];
+            out.ur[i] = ur[n];
+            out.height[i] = (uint8_t)std::min(pheight[n], 255);
+            out.sink0[i] = (int32_t)out.p_layer.size();
+            out.nsink[i] = (uint16_t)psinks[n].size();
+            for (int64_t q : psinks[n]) {
+                out.p_layer.push_back(nd->pin_layer[q]);
+                out.p_cap.push_back(nd->pin_cap[q]);
+                // pin-via delay weight: w^d_{n->par} for a non-root node (Alg. 3 l.6), W_D * w_q at the root (R13)
+                out.p_w.push_back(ppar[n] < 0 ? ctx->W_D * pin_weight(nd->pin_slack[q]) : ctx->W_D * w[n]);
+                out.p_orig.push_back(q);
+            }
+        }
+        // footprint = unit edges U node GCells (disjoint element spaces)
+        out.fp.clear();
+        for (uint64_t k : ek) out.fp.push_back(k);
+        const uint64_t gbase = (uint64_t)2 * X * Y;
+        for (size_t n = 0; n < nn; n++) out.fp.push_back(gbase + (uint64_t)py[n] * X + px[n]);
+        out.wl = (int64_t)ek.size();
+        return "";
+    }
+};
+
+// Flat per-thread storage of built nets (input-order chunk).
+struct Chunk {
+    int64_t beg = 0, end = 0;
+    std::vector<int64_t> node_off, sink_off, fp_off;   // per net, size n+1
+    BuiltNet acc;                                      // concatenated arrays
+    std::string err;
+    int64_t err_net = -1;
+    int64_t wl = 0;
+    int max_height = 0;
+};
+
+template <class T>
+void append(std::vector<T> &a, const std::vector<T> &b) { a.insert(a.end(), b.begin(), b.end()); }
+
+}  // namespace
+
+// =============================================================== C ABI ======
+extern "C" {
+
+const char *la_last_error(void) { return g_err.c_str(); }
+
+void la_shard_range(int64_t n, int32_t world, int32_t rank, int64_t *beg, int64_t *end) {
+    if (world <= 0) world = 1;
+    int64_t q = n / world, r = n % world;
+    *beg = rank * q + std::min<int64_t>(rank, r);
+    *end = *beg + q + (rank < r ? 1 : 0);
+}
+
+la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
+    if (!g || !out) return set_err(LA_EINVAL, "null argument");
+    *out = nullptr;
+    if (g->L < 2 || g->L > MAXL) return set_err(LA_EINVAL, "L must be in [2, 16]");
+    if (g->X <= 1 || g->Y <= 1 || g->X > 65535 || g->Y > 65535) return set_err(LA_EINVAL, "X, Y must be in [2, 65535]");
+    if (!g->dir || !g->routable || !g->r || !g->c || !g->vr || !g->ofw || !g->wire_cap || !g->via_cap)
+        return set_err(LA_EINVAL, "null grid array");
+    const int L = g->L;
+    if (!ok_nonneg(g->r, L) || !ok_nonneg(g->c, L) || !ok_nonneg(g->vr, L - 1) || !ok_nonneg(g->ofw, L))
+        return set_err(LA_EINVAL, "negative (or NaN) r, c, vr or ofw");
+    double ws[] = {g->W_D, g->W_CAP, g->W_CONG, g->W_VIA, g->s_pos, g->s_zero, g->w_floor};
+    if (!ok_nonneg(ws, 7)) return set_err(LA_EINVAL, "negative (or NaN) weight or exponent");
+    if (g->delta_lo > g->delta_hi) return set_err(LA_EINVAL, "delta_lo > delta_hi");
+    if (g->world < 1 || g->world > 64 || g->rank < 0 || g->rank >= g->world) return set_err(LA_EINVAL, "bad rank/world");
+    if (g->world > 1 && !g->nccl_id) return set_err(LA_EINVAL, "world > 1 needs nccl_id");
+    bool hasH = false, hasV = false;
+    for (int l = 0; l < L; l++) {
+        if (g->dir[l] > 1) return set_err(LA_EINVAL, "dir must be 0 or 1");
+        if (g->routable[l]) (g->dir[l] == 0 ? hasH : hasV) = true;
+    }
+    if (!hasH || !hasV) return set_err(LA_EINVAL, "each direction needs a routable layer");
+
+    la_ctx *ctx = new la_ctx();
+    ctx->device = g->device;
+    ctx->rank = g->rank;
+    ctx->world = g->world;
+    ctx->X = g->X; ctx->Y = g->Y; ctx->L = L;
+    ctx->dir.assign(g->dir, g->dir + L);
+    ctx->routable.assign(g->routable, g->routable + L);
+    ctx->r.assign(g->r, g->r + L);
+    ctx->c.assign(g->c, g->c + L);
+    ctx->vr.assign(g->vr, g->vr + L - 1);
+    ctx->ofw.assign(g->ofw, g->ofw + L);
+    ctx->s_pos = g->s_pos; ctx->s_zero = g->s_zero;
+    ctx->W_D = g->W_D; ctx->W_CAP = g->W_CAP; ctx->W_CONG = g->W_CONG; ctx->W_VIA = g->W_VIA;
+    ctx->logit_k = g->logit_k; ctx->logit_b = g->logit_b; ctx->w_floor = g->w_floor;
+    ctx->delta_lo = g->delta_lo; ctx->delta_hi = g->delta_hi;
+    // r_avg (reading R6): mean of routable r, summed in ascending layer order
+    if (std::isnan(g->r_avg)) {
+        double s = 0.0;
+        int cnt = 0;
+        for (int l = 0; l < L; l++)
+            if (g->routable[l]) { s = s + g->r[l]; cnt++; }
+        ctx->r_avg = s / (double)cnt;
+    } else {
+        ctx->r_avg = g->r_avg;
+    }
+    ctx->wire_off.assign(L + 1, 0);
+    for (int l = 0; l < L; l++) {
+        int64_t n = g->dir[l] == 0 ? (int64_t)(g->X - 1) * g->Y : (int64_t)g->X * (g->Y - 1);
+        ctx->wire_off[l + 1] = ctx->wire_off[l] + n;
+        if (g->dir[l] == 0) ctx->LH++; else ctx->LV++;
+    }
+    ctx->n_wire_api = ctx->wire_off[L];
+    ctx->n_via_api = (int64_t)(L - 1) * g->X * g->Y;
+    for (int64_t i = 0; i < ctx->n_wire_api; i++)
+        if (g->wire_cap[i] < 0) { delete ctx; return set_err(LA_EINVAL, "negative wire capacity"); }
+    for (int64_t i = 0; i < ctx->n_via_api; i++)
+        if (g->via_cap[i] < 0) { delete ctx; return set_err(LA_EINVAL, "negative via capacity"); }
+
+    // technology tables (O4): VR[a][b] ascending sums; Eq. (3) marginals with host libm
+    std::memset(&ctx->tab, 0, sizeof(TechTab));
+    for (int l = 0; l < L; l++) {
+        ctx->tab.r[l] = g->r[l];
+        ctx->tab.c[l] = g->c[l];
+        ctx->tab.ofw[l] = g->ofw[l];
+        if (l < L - 1) ctx->tab.vr[l] = g->vr[l];
+    }
+    for (int a = 0; a < L; a++)
+        for (int b = 0; b < L; b++) {
+            double s = 0.0;
+            for (int k = std::min(a, b); k < std::max(a, b); k++) s = s + g->vr[k];
+            ctx->tab.VR[a * MAXL + b] = s;
+        }
+    const int nd = g->delta_hi - g->delta_lo + 1;
+    std::vector<double> Mpos(nd), Mzero(nd);
+    for (int i = 0; i < nd; i++) {
+        double d = (double)(g->delta_lo + i);
+        Mpos[i] = std::exp(g->s_pos * (d + 1.0)) - std::exp(g->s_pos * d);
+        Mzero[i] = std::exp(g->s_zero * (d + 1.0)) - std::exp(g->s_zero * d);
+    }
+
+    cudaError_t e = cudaSetDevice(g->device);
+    if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "cudaSetDevice"); }
+    if (g->stream) {
+        ctx->stream = static_cast<cudaStream_t>(g->stream);
+    } else {
+        e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "cudaStreamCreate"); }
+        ctx->own_stream = true;
+    }
+    auto fail = [&](la_status st) { delete ctx; return st; };
+    auto up = [&](auto **dst, const auto *src, size_t n) -> la_status {
+        using T = std::remove_const_t<std::remove_reference_t<decltype(*src)>>;
+        void *p = nullptr;
+        cudaError_t ee = cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16));
+        if (ee != cudaSuccess) return set_err(ee == cudaErrorMemoryAllocation ? LA_ENOMEM : LA_ECUDA,
+                                              std::string("cudaMalloc: ") + cudaGetErrorString(ee));
+        *dst = static_cast<T *>(p);
+        if (src && n) {
+            ee = cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
+            if (ee != cudaSuccess) return set_err(LA_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(ee));
+        }
+        return LA_OK;
+    };
+    la_status st;
+    ctx->n_wire_packed = (int64_t)(g->X - 1) * g->Y * ctx->LH + (int64_t)g->X * (g->Y - 1) * ctx->LV;
+    if ((st = up(&ctx->d_wH, (const int32_t *)nullptr, (size_t)(g->X - 1) * g->Y * ctx->LH)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_wV, (const int32_t *)nullptr, (size_t)g->X * (g->Y - 1) * ctx->LV)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_via, (const int32_t *)nullptr, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_wcap, g->wire_cap, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_vcap, g->via_cap, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_wire_off, ctx->wire_off.data(), (size_t)L + 1)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_Mpos, Mpos.data(), (size_t)nd)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_Mzero, Mzero.data(), (size_t)nd)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_tab, &ctx->tab, 1)) != LA_OK) return fail(st);
+    int32_t *d_wdem0 = nullptr, *d_vdem0 = nullptr;
+    if (g->wire_dem0 && (st = up(&d_wdem0, g->wire_dem0, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
+    if (g->via_dem0 && (st = up(&d_vdem0, g->via_dem0, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+
+    DevGrid &G = ctx->G;
+    G.X = g->X; G.Y = g->Y; G.L = L; G.LH = ctx->LH; G.LV = ctx->LV;
+    int ih = 0, iv = 0;
+    for (int l = 0; l < MAXL; l++) {
+        G.dir[l] = l < L ? g->dir[l] : 0;
+        G.routable[l] = l < L ? g->routable[l] : 0;
+        G.lidx[l] = l < L ? (int8_t)(g->dir[l] == 0 ? ih++ : iv++) : 0;
+    }
+    G.delta_lo = g->delta_lo; G.delta_hi = g->delta_hi;
+    G.W_D = g->W_D; G.W_CAP = g->W_CAP; G.W_CONG = g->W_CONG; G.W_VIA = g->W_VIA;
+    G.wH = ctx->d_wH; G.wV = ctx->d_wV; G.via = ctx->d_via;
+    G.Mpos = ctx->d_Mpos; G.Mzero = ctx->d_Mzero; G.tab = ctx->d_tab;
+    e = launch_pack_state(G, ctx->d_wcap, d_wdem0, ctx->d_vcap, d_vdem0, ctx->d_wire_off, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (d_wdem0) cudaFree(d_wdem0);
+    if (d_vdem0) cudaFree(d_vdem0);
+    if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "pack initial state"); }
+    // pristine copy of the initial packed state for la_reset
+    size_t bH = sizeof(int32_t) * (size_t)(g->X - 1) * g->Y * ctx->LH;
+    size_t bV = sizeof(int32_t) * (size_t)g->X * (g->Y - 1) * ctx->LV;
+    size_t bVia = sizeof(int32_t) * (size_t)ctx->n_via_api;
+    if ((st = up(&ctx->d_wH0, (const int32_t *)nullptr, bH / 4)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_wV0, (const int32_t *)nullptr, bV / 4)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_via0, (const int32_t *)nullptr, bVia / 4)) != LA_OK) return fail(st);
+    e = cudaMemcpyAsync(ctx->d_wH0, ctx->d_wH, bH, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->d_wV0, ctx->d_wV, bV, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->d_via0, ctx->d_via, bVia, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "snapshot initial state"); }
+
+    if (g->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, g->nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, g->world, id, g->rank);
+        if (r != ncclSuccess) {
+            delete ctx;
+            return set_err(LA_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+    *out = ctx;
+    return LA_OK;
+}
+
+la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
+    if (!ctx || !n) return set_err(LA_EINVAL, "null argument");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    if (ctx->loaded) return set_err(LA_ESTATE, "nets already loaded");
+    if (n->n_nets < 0) return set_err(LA_EINVAL, "bad net descriptor");
+    if (n->n_nets > 0) {
+        if (!n->pin_ptr || !n->seg_ptr || !n->pin_x || !n->pin_y || !n->pin_layer || !n->pin_cap || !n->pin_slack)
+            return set_err(LA_EINVAL, "bad net descriptor: null array");
+        if (!n->seg_xy && n->seg_ptr[n->n_nets] > 0) return set_err(LA_EINVAL, "bad net descriptor: null seg_xy");
+    }
+    if (n->n_nets >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "too many nets");
+    CK(cudaSetDevice(ctx->device));
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t N = n->n_nets;
+    ctx->n_nets = N;
+    ctx->n_pins = N > 0 ? n->pin_ptr[N] : 0;
+
+    // ---- build every net's tree in parallel (input-order chunks)
+    unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    if (N < 4096) nthr = 1;
+    const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t)nthr * 8));
+    std::vector<Chunk> chunks(nchunks);
+    for (int64_t c = 0; c < nchunks; c++) {
+        chunks[c].beg = N * c / nchunks;
+        chunks[c].end = N * (c + 1) / nchunks;
+    }
+    std::atomic<int64_t> next{0};
+    auto worker = [&]() {
+        Builder B{ctx, n};
+        BuiltNet bn;
+        for (;;) {
+            int64_t c = next.fetch_add(1);
+            if (c >= nchunks) break;
+            Chunk &ch = chunks[c];
+            ch.node_off.assign(1, 0);
+            ch.sink_off.assign(1, 0);
+            ch.fp_off.assign(1, 0);
+            for (int64_t net = ch.beg; net < ch.end; net++) {
+                std::string err = B.build(net, bn);
+                if (!err.empty()) { ch.err = err; ch.err_net = net; break; }
+                BuiltNet &a = ch.acc;
+                append(a.xy, bn.xy); append(a.kid, bn.kid); append(a.len, bn.len); append(a.edir, bn.edir);
+                append(a.nkid, bn.nkid); append(a.nl, bn.nl); append(a.nh, bn.nh); append(a.sink0, bn.sink0);
+                append(a.nsink, bn.nsink); append(a.wd, bn.wd); append(a.ur, bn.ur); append(a.height, bn.height);
+                append(a.p_layer, bn.p_layer); append(a.p_cap, bn.p_cap); append(a.p_w, bn.p_w);
+                append(a.p_orig, bn.p_orig); append(a.fp, bn.fp);
+                ch.node_off.push_back((int64_t)a.xy.size());
+                ch.sink_off.push_back((int64_t)a.p_layer.size());
+                ch.fp_off.push_back((int64_t)a.fp.size());
+                ch.wl += bn.wl;
+                if (!bn.height.empty()) ch.max_height = std::max<int>(ch.max_height, bn.height.back());
+            }
+        }
+    };
+    {
+        std::vector<std::thread> th;
+        for (unsigned i = 1; i < nthr; i++) th.emplace_back(worker);
+        worker();
+        for (auto &t : th) t.join();
+    }
+    for (auto &ch : chunks)
+        if (ch.err_net >= 0) return set_err(LA_EINVAL, ch.err);
+
+    // per-net index: chunk and local position
+    std::vector<int32_t> chunk_of(N);
+    for (int64_t c = 0; c < nchunks; c++)
+        for (int64_t i = chunks[c].beg; i < chunks[c].end; i++) chunk_of[i] = (int32_t)c;
+    auto nnodes_of = [&](int64_t net) {
+        const Chunk &ch = chunks[chunk_of[net]];
+        int64_t i = net - ch.beg;
+        return ch.node_off[i + 1] - ch.node_off[i];
+    };
+
+    // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
+    std::vector<int64_t> by_rank(N);
+    for (int64_t i = 0; i < N; i++) by_rank[i] = i;
+    if (n->order_key)
+        std::stable_sort(by_rank.begin(), by_rank.end(),
+                         [&](int64_t a, int64_t b) { return n->order_key[a] < n->order_key[b]; });
+    std::vector<int64_t> fp_pos(N + 1, 0);
+    for (int64_t r = 0; r < N; r++) {
+        int64_t net = by_rank[r];
+        const Chunk &ch = chunks[chunk_of[net]];
+        int64_t i = net - ch.beg;
+        fp_pos[r + 1] = fp_pos[r] + (ch.fp_off[i + 1] - ch.fp_off[i]);
+    }
+    const int64_t n_fp = fp_pos[N];
+    std::vector<uint64_t> keys(n_fp);
+    {
+        std::atomic<int64_t> nx{0};
+        auto fill = [&]() {
+            const int64_t step = 4096;
+            for (;;) {
+                int64_t a = nx.fetch_add(step);
+                if (a >= N) break;
+                for (int64_t r = a; r < std::min(N, a + step); r++) {
+                    int64_t net = by_rank[r];
+                    const Chunk &ch = chunks[chunk_of[net]];
+                    int64_t i = net - ch.beg;
+                    int64_t o = fp_pos[r];
+                    for (int64_t k = ch.fp_off[i]; k < ch.fp_off[i + 1]; k++) keys[o++] = (ch.acc.fp[k] << 32) | (uint64_t)r;
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (unsigned i = 1; i < nthr; i++) th.emplace_back(fill);
+        fill();
+        for (auto &t : th) t.join();
+    }
+    int elem_bits = 1;
+    while (((uint64_t)1 << elem_bits) < (uint64_t)3 * ctx->X * ctx->Y) elem_bits++;
+    auto t1 = std::chrono::steady_clock::now();
+
+    // ---- GPU conflict-free batching (K1/K2)
+    std::vector<int32_t> batch_of_rank;
+    int32_t nb = 0;
+    {
+        cudaError_t e = gpu_conflict_batches(keys.data(), n_fp, elem_bits, N, batch_of_rank, nb, ctx->stream,
+                                             &ctx->stats.launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "conflict-free batching");
+    }
+    std::vector<uint64_t>().swap(keys);
+    auto t2 = std::chrono::steady_clock::now();
+    ctx->batch_of_net.assign(N, 0);
+    for (int64_t r = 0; r < N; r++) ctx->batch_of_net[by_rank[r]] = batch_of_rank[r];
+
+    // ---- batch-major net order: by batch, then node count descending, then rank
+    std::vector<int64_t> pos_net(N);   // final position -> input net
+    {
+        std::vector<int64_t> cnt(nb + 1, 0);
+        for (int64_t i = 0; i < N; i++) cnt[ctx->batch_of_net[i] + 1]++;
+        for (int32_t b = 0; b < nb; b++) cnt[b + 1] += cnt[b];
+        ctx->batch_net0.assign(cnt.begin(), cnt.end());
+        std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
+        for (int64_t r = 0; r < N; r++) {
+            int64_t net = by_rank[r];
+            pos_net[cur[ctx->batch_of_net[net]]++] = net;
+        }
+        for (int32_t b = 0; b < nb; b++)
+            std::stable_sort(pos_net.begin() + ctx->batch_net0[b], pos_net.begin() + ctx->batch_net0[b + 1],
+                             [&](int64_t a, int64_t c) { return nnodes_of(a) > nnodes_of(c); });
+    }
+    // offsets in final order
+    std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
+    int64_t max_nodes = 0;
+    for (int64_t p = 0; p < N; p++) {
+        int64_t net = pos_net[p];
+        const Chunk &ch = chunks[chunk_of[net]];
+        int64_t i = net - ch.beg;
+        int64_t nn = ch.node_off[i + 1] - ch.node_off[i];
+        node0[p + 1] = node0[p] + nn;
+        sink0g[p + 1] = sink0g[p] + (ch.sink_off[i + 1] - ch.sink_off[i]);
+        max_nodes = std::max(max_nodes, nn);
+    }
+    const int64_t NN = node0[N], NS = sink0g[N];
+    ctx->n_nodes = NN;
+    ctx->n_sinks = NS;
+    // host staging in device layout
+    std::vector<uint32_t> xy(NN);
+    std::vector<int32_t> kid(NN * 4), len(NN), sink0(NN);
+    std::vector<uint8_t> edir(NN), nkid(NN), nl(NN), nh(NN), pdrv(N);
+    std::vector<uint16_t> nsink(NN);
+    std::vector<double> wd(NN), ur(NN);
+    std::vector<uint8_t> p_layer(NS);
+    std::vector<double> p_cap(NS), p_w(NS);
+    std::vector<int64_t> p_orig(NS), net_id(N);
+    {
+        std::atomic<int64_t> nx{0};
+        auto lay = [&]() {
+            const int64_t step = 2048;
+            for (;;) {
+                int64_t a = nx.fetch_add(step);
+                if (a >= N) break;
+                for (int64_t p = a; p < std::min(N, a + step); p++) {
+                    int64_t net = pos_net[p];
+                    const Chunk &ch = chunks[chunk_of[net]];
+                    const BuiltNet &A = ch.acc;
+                    int64_t i = net - ch.beg;
+                    int64_t s0 = ch.node_off[i], s1 = ch.node_off[i + 1];
+                    int64_t q0 = ch.sink_off[i];
+                    int64_t d0 = node0[p], e0 = sink0g[p];
+                    net_id[p] = net;
+                    pdrv[p] = n->pin_layer[n->pin_ptr[net]];
+                    for (int64_t k = s0; k < s1; k++) {
+                        int64_t d = d0 + (k - s0);
+                        xy[d] = A.xy[k];
+                        for (int j = 0; j < 4; j++) kid[d * 4 + j] = A.kid[k * 4 + j] < 0 ? -1 : (int32_t)(d0 + A.kid[k * 4 + j]);
+                        len[d] = A.len[k]; edir[d] = A.edir[k]; nkid[d] = A.nkid[k]; nl[d] = A.nl[k]; nh[d] = A.nh[k];
+                        sink0[d] = (int32_t)(e0 + A.sink0[k]);
+                        nsink[d] = A.nsink[k]; wd[d] = A.wd[k]; ur[d] = A.ur[k];
+                    }
+                    for (int64_t q = q0; q < ch.sink_off[i + 1]; q++) {
+                        int64_t d = e0 + (q - q0);
+                        p_layer[d] = A.p_layer[q]; p_cap[d] = A.p_cap[q]; p_w[d] = A.p_w[q]; p_orig[d] = A.p_orig[q];
+                    }
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (unsigned i = 1; i < nthr; i++) th.emplace_back(lay);
+        lay();
+        for (auto &t : th) t.join();
+    }
+    if (NN >= ((int64_t)1 << 31) || NS >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "forest too large");
+    int64_t wl = 0;
+    int maxh = 0;
+    for (auto &ch : chunks) { wl += ch.wl; maxh = std::max(maxh, ch.max_height); }
+    chunks.clear();
+    chunks.shrink_to_fit();
+
+    // ---- upload forest, allocate scratch
+    DevForest &F = ctx->F;
+    F.n_nets = N; F.n_nodes = NN; F.n_sinks = NS;
+    uint32_t *d_xy; int32_t *d_kid, *d_len, *d_sink0; uint8_t *d_edir, *d_nkid, *d_nl, *d_nh, *d_pl, *d_pdrv;
+    uint16_t *d_nsink; double *d_wd, *d_ur, *d_pc, *d_pw; int64_t *d_po, *d_node0, *d_netid;
+    TRY(dev_upload(ctx, &d_xy, xy.data(), NN)); TRY(dev_upload(ctx, &d_kid, kid.data(), NN * 4));
+    TRY(dev_upload(ctx, &d_len, len.data(), NN)); TRY(dev_upload(ctx, &d_sink0, sink0.data(), NN));
+    TRY(dev_upload(ctx, &d_edir, edir.data(), NN)); TRY(dev_upload(ctx, &d_nkid, nkid.data(), NN));
+    TRY(dev_upload(ctx, &d_nl, nl.data(), NN)); TRY(dev_upload(ctx, &d_nh, nh.data(), NN));
+    TRY(dev_upload(ctx, &d_nsink, nsink.data(), NN)); TRY(dev_upload(ctx, &d_wd, wd.data(), NN));
+    TRY(dev_upload(ctx, &d_ur, ur.data(), NN)); TRY(dev_upload(ctx, &d_pl, p_layer.data(), NS));
+    TRY(dev_upload(ctx, &d_pc, p_cap.data(), NS)); TRY(dev_upload(ctx, &d_pw, p_w.data(), NS));
+    TRY(dev_upload(ctx, &d_po, p_orig.data(), NS)); TRY(dev_upload(ctx, &d_node0, node0.data(), N + 1));
+    TRY(dev_upload(ctx, &d_netid, net_id.data(), N)); TRY(dev_upload(ctx, &d_pdrv, pdrv.data(), N));
+    F.xy = d_xy; F.kid = d_kid; F.len = d_len; F.edir = d_edir; F.nkid = d_nkid; F.nl = d_nl; F.nh = d_nh;
+    F.sink0 = d_sink0; F.nsink = d_nsink; F.wd = d_wd; F.ur = d_ur; F.p_layer = d_pl; F.p_cap = d_pc; F.p_w = d_pw;
+    F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv;
+    DevScratch &S = ctx->S;
+    const size_t NL = (size_t)NN * ctx->L;
+    TRY(dev_alloc(ctx, &S.A, NL)); TRY(dev_alloc(ctx, &S.B, NL)); TRY(dev_alloc(ctx, &S.Cap, NL));
+    TRY(dev_alloc(ctx, &S.choice, NL)); TRY(dev_alloc(ctx, &S.entry, NL)); TRY(dev_alloc(ctx, &S.froot, N));
+    TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
+    TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
+    TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
+    TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
+    if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
+    CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->h_xy.swap(xy);
+    ctx->h_len.swap(len);
+    ctx->h_edir.swap(edir);
+    ctx->h_net_node0.swap(node0);
+    ctx->h_net_id.swap(net_id);
+    auto t3 = std::chrono::steady_clock::now();
+
+    la_stats &stt = ctx->stats;
+    stt.n_nets = N; stt.n_pins = ctx->n_pins; stt.n_nodes = NN; stt.n_sinks = NS;
+    stt.wirelength = wl; stt.footprint = n_fp; stt.n_batches = nb; stt.max_height = maxh;
+    stt.max_net_nodes = max_nodes;
+    stt.max_batch_nets = 0;
+    for (int32_t b = 0; b < nb; b++)
+        stt.max_batch_nets = std::max(stt.max_batch_nets, ctx->batch_net0[b + 1] - ctx->batch_net0[b]);
+    stt.batch_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+    stt.load_ms = std::chrono::duration<double, std::milli>((t1 - t0) + (t3 - t2)).count();
+    ctx->loaded = true;
+    ctx->next_batch = 0;
+    ctx->pending_commit = false;
+    if (n_batches) *n_batches = nb;
+    return LA_OK;
+}
+
+static la_status check_ready(la_ctx *ctx) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    if (!ctx->loaded) return set_err(LA_ESTATE, "nets not loaded");
+    return LA_OK;
+}
+
+la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
+    TRY(check_ready(ctx));
+    const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    if (batch < 0 || batch >= nb) return set_err(LA_ERANGE, "batch index out of range");
+    if (ctx->pending_commit || batch != ctx->next_batch)
+        return set_err(LA_ESTATE, "batches must be assigned in order, each committed before the next");
+    int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1], s0, s1;
+    la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
+    if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
+        CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
+    CK(launch_assign(ctx->G, ctx->F, ctx->S, b0 + s0, b0 + s1, ctx->stream));
+    ctx->stats.launches += 1;
+    ctx->pending_commit = true;
+    return LA_OK;
+}
+
+la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
+    TRY(check_ready(ctx));
+    if (!ctx->pending_commit || batch != ctx->next_batch)
+        return set_err(LA_ESTATE, "commit must follow the assignment of the same batch");
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
+    const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
+    if (ctx->world > 1) {
+        // reconcile: every rank contributes its shard's packed decisions (others 0) -> sum
+        int64_t s0, s1;
+        la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
+        const int64_t m0 = ctx->h_net_node0[b0 + s0], m1 = ctx->h_net_node0[b0 + s1];
+        CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
+        CK(launch_pack_decisions(ctx->S, m0, m1, ctx->stream));
+        NK(ncclAllReduce(ctx->S.dec + n0, ctx->S.dec + n0, (size_t)(n1 - n0), ncclUint32, ncclSum, ctx->comm,
+                         ctx->stream));
+        NK(ncclAllReduce(ctx->S.froot + b0, ctx->S.froot + b0, (size_t)(b1 - b0), ncclFloat64, ncclSum, ctx->comm,
+                         ctx->stream));
+        CK(launch_unpack_decisions(ctx->S, n0, n1, ctx->stream));
+        ctx->stats.launches += 2;
+    }
+    CK(launch_commit(ctx->G, ctx->F, ctx->S, n0, n1, ctx->stream));
+    ctx->stats.launches += 1;
+    ctx->pending_commit = false;
+    ctx->next_batch = batch + 1;
+    return LA_OK;
+}
+
+la_status la_assign_all(la_ctx *ctx) {
+    TRY(check_ready(ctx));
+    const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    for (int32_t b = ctx->next_batch; b < nb; b++) {
+        if (!ctx->pending_commit) TRY(la_assign_batch(ctx, b));
+        TRY(la_commit_demand(ctx, b));
+    }
+    return LA_OK;
+}
+
+static la_status require_done(la_ctx *ctx) {
+    TRY(check_ready(ctx));
+    const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    if (ctx->next_batch != nb || ctx->pending_commit) return set_err(LA_ESTATE, "not every batch is committed");
+    return LA_OK;
+}
+
+la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, double *net_rc) {
+    TRY(require_done(ctx));
+    if (ctx->n_pins) CK(cudaMemsetAsync(ctx->S.sink_delay, 0, sizeof(double) * ctx->n_pins, ctx->stream));
+    CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_nets, ctx->stream));
+    ctx->stats.launches += 1;
+    if (sink_delay && ctx->n_pins)
+        CK(cudaMemcpyAsync(sink_delay, ctx->S.sink_delay, sizeof(double) * ctx->n_pins, cudaMemcpyDeviceToHost, ctx->stream));
+    if (net_cap && ctx->n_nets)
+        CK(cudaMemcpyAsync(net_cap, ctx->S.net_cap, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
+    if (net_rc && ctx->n_nets)
+        CK(cudaMemcpyAsync(net_rc, ctx->S.net_rc, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LA_OK;
+}
+
+la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_t *wire_ptr, int32_t *wires,
+                          int64_t *via_ptr, int32_t *vias, double *net_cost) {
+    TRY(require_done(ctx));
+    const int64_t N = ctx->n_nets, NN = ctx->n_nodes;
+    std::vector<uint8_t> lay(NN), sb(NN), st(NN);
+    std::vector<double> froot(N);
+    if (NN) {
+        CK(cudaMemcpyAsync(lay.data(), ctx->S.lay, NN, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(sb.data(), ctx->S.sb, NN, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(st.data(), ctx->S.st, NN, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (N) CK(cudaMemcpyAsync(froot.data(), ctx->S.froot, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    // per input net: counts
+    std::vector<int64_t> nw(N + 1, 0), nv(N + 1, 0);
+    std::vector<int64_t> pos_of(N);
+    int64_t vcuts = 0;
+    for (int64_t p = 0; p < N; p++) {
+        int64_t net = ctx->h_net_id[p];
+        pos_of[net] = p;
+        int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
+        nw[net + 1] = (b - a) - 1;
+        int64_t v = 0;
+        for (int64_t k = a; k < b; k++) {
+            if (st[k] > sb[k]) v++;
+            vcuts += st[k] - sb[k];
+        }
+        nv[net + 1] = v;
+    }
+    ctx->stats.via_cuts = vcuts;
+    for (int64_t i = 0; i < N; i++) { nw[i + 1] += nw[i]; nv[i + 1] += nv[i]; }
+    if (n_wires) *n_wires = nw[N];
+    if (n_vias) *n_vias = nv[N];
+    if (wire_ptr) std::memcpy(wire_ptr, nw.data(), sizeof(int64_t) * (N + 1));
+    if (via_ptr) std::memcpy(via_ptr, nv.data(), sizeof(int64_t) * (N + 1));
+    if (net_cost)
+        for (int64_t i = 0; i < N; i++) net_cost[i] = froot[pos_of[i]];
+    if (wires || vias) {
+        std::vector<std::array<int32_t, 5>> W;
+        std::vector<std::array<int32_t, 4>> V;
+        for (int64_t net = 0; net < N; net++) {
+            int64_t p = pos_of[net];
+            int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
+            W.clear();
+            V.clear();
+            for (int64_t k = a; k < b; k++) {
+                int x = ctx->h_xy[k] & 0xffff, y = ctx->h_xy[k] >> 16;
+                if (ctx->h_edir[k] != NO_DIR) {
+                    int ln = ctx->h_len[k];
+                    int qx = x, qy = y;   // parent GCell
+                    switch (ctx->h_edir[k]) {
+                        case DIR_E: qx = x - ln; break;
+                        case DIR_W: qx = x + ln; break;
+                        case DIR_N: qy = y - ln; break;
+                        default: qy = y + ln; break;
+                    }
+                    W.push_back({std::min(x, qx), std::min(y, qy), std::max(x, qx), std::max(y, qy), (int32_t)lay[k]});
+                }
+                if (st[k] > sb[k]) V.push_back({x, y, (int32_t)sb[k], (int32_t)st[k]});
+            }
+            std::sort(W.begin(), W.end());
+            std::sort(V.begin(), V.end());
+            if (wires) std::memcpy(wires + 5 * nw[net], W.data(), 20 * W.size());
+            if (vias) std::memcpy(vias + 4 * nv[net], V.data(), 16 * V.size());
+        }
+    }
+    return LA_OK;
+}
+
+la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    int32_t *dw = nullptr, *dv = nullptr;
+    CK(cudaMalloc(&dw, sizeof(int32_t) * std::max<int64_t>(ctx->n_wire_api, 1)));
+    cudaError_t e = cudaMalloc(&dv, sizeof(int32_t) * std::max<int64_t>(ctx->n_via_api, 1));
+    if (e == cudaSuccess) e = launch_unpack_demand(ctx->G, ctx->d_wcap, ctx->d_vcap, dw, dv, ctx->d_wire_off, ctx->stream);
+    if (e == cudaSuccess && wire_dem)
+        e = cudaMemcpyAsync(wire_dem, dw, sizeof(int32_t) * ctx->n_wire_api, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && via_dem)
+        e = cudaMemcpyAsync(via_dem, dv, sizeof(int32_t) * ctx->n_via_api, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(dw);
+    if (dv) cudaFree(dv);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_demand");
+    return LA_OK;
+}
+
+la_status la_get_batches(la_ctx *ctx, int32_t *batch_of) {
+    TRY(check_ready(ctx));
+    if (batch_of) std::memcpy(batch_of, ctx->batch_of_net.data(), sizeof(int32_t) * ctx->n_nets);
+    return LA_OK;
+}
+
+la_status la_reset(la_ctx *ctx) {
+    TRY(check_ready(ctx));
+    size_t bH = sizeof(int32_t) * (size_t)(ctx->X - 1) * ctx->Y * ctx->LH;
+    size_t bV = sizeof(int32_t) * (size_t)ctx->X * (ctx->Y - 1) * ctx->LV;
+    size_t bVia = sizeof(int32_t) * (size_t)ctx->n_via_api;
+    CK(cudaMemcpyAsync(ctx->d_wH, ctx->d_wH0, bH, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_wV, ctx->d_wV0, bV, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_via, ctx->d_via0, bVia, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->next_batch = 0;
+    ctx->pending_commit = false;
+    return LA_OK;
+}
+
+la_status la_get_stats(la_ctx *ctx, la_stats *out) {
+    if (!ctx || !out) return set_err(LA_EINVAL, "null argument");
+    *out = ctx->stats;
+    return LA_OK;
+}
+
+la_status la_sync(la_ctx *ctx) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LA_OK;
+}
+
+void la_destroy(la_ctx *ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+}
+
+}  // extern "C"

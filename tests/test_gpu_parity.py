@@ -1,0 +1,248 @@
+"""GPU (CUDA, sm_100a) vs CPU oracle parity, through the C ABI.
+
+Bar (BASELINE.json north_star): layer choices, via spans, demand grids
+and batch ids bit-exact; net cost f[root], sink delays, net caps and net RC sums
+within 1e-9 relative (and, by the shared expression-order contract, expected
+bitwise -- checked separately so a rounding-order drift is visible on its own).
+"""
+import copy
+
+import numpy as np
+import pytest
+
+import refcheck as rc
+from gen import synth
+from helpers import randomize_state
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def la():
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2507_13375_b200 import la as mod
+    return mod
+
+
+def run_gpu(la, d, per_batch=False):
+    A = la.LayerAssigner(d, device=0)
+    nb = A.load()
+    if per_batch:
+        for k in range(nb):
+            A.assign_batch(k)
+            A.commit_demand(k)
+        out = A.eval_timing()
+        out.update(A.solution())
+        wd, vd = A.demand()
+        out.update(wire_dem=wd, via_dem=vd, batch_of=A.batches())
+    else:
+        out = A.run()
+    out["stats"] = A.stats()
+    out["n_batches"] = nb
+    A.close()
+    return out
+
+
+def assert_parity(got, ref, bitwise_fp=False):
+    for k in ("wire_ptr", "wires", "via_ptr", "vias", "wire_dem", "via_dem", "batch_of"):
+        a, b = np.asarray(got[k]), np.asarray(ref[k])
+        assert a.shape == b.shape, (k, a.shape, b.shape)
+        if not np.array_equal(a, b):
+            bad = np.argwhere(a != b)[:5]
+            raise AssertionError(f"{k}: {int((a != b).sum())} mismatches, first at {bad.tolist()}")
+    for k in ("net_cost", "sink_delay", "net_cap", "net_rc"):
+        a, b = got[k], ref[k]
+        np.testing.assert_allclose(a, b, rtol=RTOL, atol=0.0, err_msg=k)
+        if bitwise_fp:
+            assert np.array_equal(a, b), f"{k}: not bitwise equal ({int((a != b).sum())} values)"
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_config_parity(la, cfg):
+    d = synth.make_config(cfg)
+    got = run_gpu(la, d)
+    ref = oracle.run(d)
+    assert_parity(got, ref)
+    assert got["n_batches"] == int(ref["batch_of"].max()) + 1
+
+
+def test_config3_parity_full(la):
+    """Config 3 (1M nets, 1024^2, L = 10, criticality-weighted, r_drv > 0) at full size."""
+    d = synth.make_config(3)
+    got = run_gpu(la, d)
+    ref = oracle.run(d)
+    assert_parity(got, ref)
+
+
+def test_config4_parity_sample(la):
+    """Config 4's grid / 13 layers / high-fanout mix (64-256 pins) at 400K nets."""
+    d = synth.make_config(4, n_nets=400_000)
+    got = run_gpu(la, d)
+    ref = oracle.run(d)
+    assert got["stats"]["max_net_nodes"] > 64
+    assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_bitwise_fp(la, cfg):
+    """Shared expression-order contract: costs, delays, caps bitwise equal."""
+    d = synth.make_config(cfg)
+    assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
+
+
+def test_per_batch_api_equals_assign_all(la):
+    d = synth.make_config(1)
+    a = run_gpu(la, d, per_batch=True)
+    b = run_gpu(la, d, per_batch=False)
+    for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost", "sink_delay"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_reset_and_rerun_identical(la):
+    d = synth.make_config(1)
+    A = la.LayerAssigner(d)
+    A.load()
+    first = A.run()
+    A.reset()
+    second = A.run()
+    A.close()
+    for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost", "sink_delay", "net_rc"):
+        assert np.array_equal(first[k], second[k]), k
+
+
+# --------------------------------------------------------------- edge cases
+def _hand(L=6, X=12, Y=12, **kw):
+    d = synth.empty_design(X, Y, L)
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+def test_empty_design(la):
+    d = synth.with_nets(_hand(), [])
+    got = run_gpu(la, d)
+    assert got["n_batches"] == 0 and len(got["wires"]) == 0 and got["wire_dem"].sum() == 0
+
+
+def test_degenerate_nets(la):
+    """Single-GCell nets (R38), pins on high layers, several pins per GCell (R29), a dangling spur (R39),
+    overlapping input segments (R30), same-direction continuation at a pin node (R40), a ring-free plus."""
+    nets = [
+        dict(pins=[(3, 3, 0, 1.0, -50.0), (3, 3, 4, 0.7, -400.0), (3, 3, 2, 1.1, 10.0)], segs=[]),
+        dict(pins=[(0, 0, 5, 1.0, -1.0), (5, 0, 3, 1.0, -450.0)], segs=[(0, 0, 5, 0)]),
+        dict(pins=[(1, 5, 1, 1.0, -30.0), (4, 5, 0, 2.0, -300.0)], segs=[(1, 5, 6, 5)]),              # spur to (6,5)
+        dict(pins=[(2, 8, 0, 1.0, -5.0), (7, 8, 1, 1.0, -5.0)], segs=[(2, 8, 5, 8), (4, 8, 7, 8)]),    # overlap
+        dict(pins=[(1, 10, 0, 1.0, -5.0), (4, 10, 0, 1.0, -490.0), (8, 10, 2, 1.0, -100.0)], segs=[(1, 10, 8, 10)]),
+        dict(pins=[(9, 3, 0, 1.0, 0.0), (9, 5, 0, 1.0, -10.0), (9, 1, 0, 1.0, -20.0), (11, 3, 0, 1.0, -30.0),
+                   (7, 3, 0, 1.0, -40.0)], segs=[(9, 1, 9, 5), (7, 3, 11, 3)], r_drv=1.5),
+    ]
+    d = synth.with_nets(_hand(), nets)
+    assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
+
+
+@pytest.mark.parametrize("L", [2, 3, 4, 16])
+def test_layer_counts(la, L):
+    d = synth.generate(n_nets=3000, X=40, Y=40, L=L, seed=70 + L, pin_max=16, rdrv_mode=1)
+    assert_parity(run_gpu(la, d), oracle.run(d))
+
+
+def test_random_state_ties_and_zero_caps(la):
+    """Random initial demand, many zero capacities (s_zero), tie-heavy tech (identical layers)."""
+    rng = np.random.default_rng(5)
+    d = synth.generate(n_nets=4000, X=48, Y=48, L=8, seed=81, pin_max=32, rdrv_mode=1)
+    d = randomize_state(d, rng, wire_caps=(0, 0, 1, 2, 5), via_caps=(0, 1, 8), wire_dem=3, via_dem=3)
+    e = copy.copy(d)
+    e.r, e.c, e.ofw = np.full(8, 0.004), np.full(8, 0.18), np.ones(8)
+    e.W_VIA = 0.0
+    for dd in (d, e):
+        assert_parity(run_gpu(la, dd), oracle.run(dd), bitwise_fp=True)
+
+
+@pytest.mark.parametrize("wd,wns", [(0.0, -500.0), (1e4, -500.0), (100.0, 25.0)])
+def test_weight_regimes(la, wd, wns):
+    d = synth.generate(n_nets=5000, X=64, Y=64, L=10, seed=91, pin_max=63, rdrv_mode=1)
+    d.W_D, d.wns = wd, wns
+    assert_parity(run_gpu(la, d), oracle.run(d))
+
+
+def test_unrouteable_direction_layers(la):
+    """Some layers not routable (R15): they never carry wires, still carry vias."""
+    d = synth.generate(n_nets=3000, X=40, Y=40, L=8, seed=95, pin_max=16)
+    d.routable = np.array([0, 1, 1, 0, 1, 1, 0, 1], np.uint8)
+    got, ref = run_gpu(la, d), oracle.run(d)
+    assert_parity(got, ref)
+    assert set(np.unique(got["wires"][:, 4])).isdisjoint({0, 3, 6})
+
+
+# --------------------------------------------------------------- ABI errors on the device path
+def test_call_order_errors(la):
+    d = synth.make_config(1, n_nets=200)
+    A = la.LayerAssigner(d)
+    nb = A.load()
+    assert nb >= 2
+    with pytest.raises(la.LaError) as e:
+        la.la_assign_batch(A.ctx, 1)
+    assert e.value.status == la.LA_ESTATE
+    with pytest.raises(la.LaError) as e:
+        la.la_assign_batch(A.ctx, nb)
+    assert e.value.status == la.LA_ERANGE
+    with pytest.raises(la.LaError) as e:
+        la.la_commit_demand(A.ctx, 0)
+    assert e.value.status == la.LA_ESTATE
+    with pytest.raises(la.LaError) as e:
+        A.eval_timing()
+    assert e.value.status == la.LA_ESTATE
+    with pytest.raises(la.LaError) as e:
+        A.load()
+    assert e.value.status == la.LA_ESTATE
+    A.assign_all()
+    A.eval_timing()
+    A.close()
+
+
+@pytest.mark.parametrize("net,msg", [
+    (dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2)]),
+     "not a tree"),
+    (dict(pins=[(0, 0, 0, 1, 0), (3, 3, 0, 1, 0)], segs=[(0, 0, 2, 0)]), "not on the route"),
+    (dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 2)]), "axis-aligned"),
+    (dict(pins=[(0, 0, 0, 1, 0), (2, 0, 9, 1, 0)], segs=[(0, 0, 2, 0)]), "layer"),
+    (dict(pins=[(0, 0, 0, 1, 0), (2, 0, 0, 1, 0)], segs=[(0, 0, 40, 0)]), "outside"),
+])
+def test_route_errors(la, net, msg):
+    d = synth.with_nets(_hand(), [dict(pins=[(5, 5, 0, 1, 0), (6, 5, 0, 1, 0)], segs=[(5, 5, 6, 5)]), net])
+    A = la.LayerAssigner(d)
+    with pytest.raises(la.LaError, match=msg) as e:
+        A.load()
+    assert e.value.status == la.LA_EINVAL and "net 1" in str(e.value)
+    A.close()
+
+
+# --------------------------------------------------------------- properties at full scale
+@pytest.mark.slow
+def test_config5_full_scale_properties(la):
+    """Config 5 (12M nets, 4096^2, L = 13) in the bench's launch configuration: projection, demand ==
+    rebuild from the solution, wirelength and via-count invariants, conflict-free batches, and the
+    definitional O(n^2) Elmore on a sample of nets recomputed one by one from the GPU solution."""
+    d = synth.make_config(5)
+    got = run_gpu(la, d)
+    st = got["stats"]
+    assert int(got["wire_dem"].sum()) == st["wirelength"] == d.unit_edges_total()
+    assert int(got["via_dem"].sum()) == int((got["vias"][:, 3] - got["vias"][:, 2]).sum())
+    rng = np.random.default_rng(0)
+    for net in rng.choice(d.n_nets, 300, replace=False):
+        pins, segs = rc.net_pins(d, net), rc.net_segs(d, net)
+        nodes = rc.build_tree(pins, segs)
+        w = got["wires"][got["wire_ptr"][net]:got["wire_ptr"][net + 1]]
+        v = got["vias"][got["via_ptr"][net]:got["via_ptr"][net + 1]]
+        assert rc.unit_edges([tuple(int(t) for t in x[:4]) for x in w]) == rc.unit_edges(segs)
+        lay = rc.solution_layers(nodes, w)
+        vmap = {(int(a[0]), int(a[1])): (int(a[2]), int(a[3])) for a in v}
+        spans = [vmap.get((nd["x"], nd["y"]), (pins[0][2] if i == 0 else lay[i],) * 2) for i, nd in enumerate(nodes)]
+        delays, ncap, nrc = rc.elmore_definitional(d, pins, nodes, lay, spans)
+        p0 = int(d.pin_ptr[net])
+        np.testing.assert_allclose(got["sink_delay"][p0:p0 + len(pins)], delays, rtol=1e-9, atol=1e-15)
+        np.testing.assert_allclose([got["net_cap"][net], got["net_rc"][net]], [ncap, nrc], rtol=1e-9)
