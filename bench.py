@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the GAP-LA layer-assignment hot path (DP + backtrack + commit + Elmore) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+One step = one pass of the whole hot path over the whole synthetic design:
+la_reset (restore the initial demand, a device copy) + every conflict-free batch (la_assign_batch =
+K4/K5 DP + backtrack, la_commit_demand = K8 commit [+ NCCL reconcile when N > 1]) + la_eval_timing
+(K6/K7 Elmore).  Inputs (forest, grid state) are resident in HBM and far larger than L2.  Forest
+build and batching (la_load_nets) are setup, reported separately; the e2e number includes them.
+
+Rank 0 prints ONE JSON line (see DESIGN.md §8 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "nets layer-assigned/sec (DP+Elmore+commit) at 1/2/4/8 B200; % HBM roofline"
+DEFAULT_CONFIG = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, help="BASELINE.json config (1-based)")
+    ap.add_argument("--n-nets", type=int, default=None, help="override the config's net count")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    ap.add_argument("--ncu-pass", action="store_true",
+                    help="setup + 1 warm step, then ONE step between cudaProfilerStart/Stop (for ncu)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM-style copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc, self.th = device, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def host_info():
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = "unknown"
+    return model, os.cpu_count()
+
+
+def algorithmic_bytes(st, L, n_nets, via_cuts=None):
+    """SURVEY §8(d) d.4 per-unit algorithmic bytes, with the instance's exact counts:
+    K4/K5 (k_assign): tree 32/node + sinks 9/pin + wire state 4/(unit edge, legal layer)
+                      + via state 4/(node, cut) + decisions 3/node + f_root 8/net
+    K8 (k_commit):   8 per unit edge + 8 per via cut (int32 read-modify-write)
+    K6/K7 (k_elmore): 19/node + 17/sink + 16/net"""
+    N, P = st["n_nodes"], st["n_sinks"]
+    assign = 32 * N + 9 * P + 4 * st["wire_state_words"] + 4 * st["via_state_words"] + 3 * N + 8 * n_nets
+    commit = 8 * st["wirelength"] + 8 * (via_cuts or 0)
+    elmore = 19 * N + 17 * P + 16 * n_nets
+    return assign, commit, elmore
+
+
+def ncu_traffic(workload):
+    """dram bytes per k_assign launch from the committed ncu summary (profiles/), if it matches."""
+    p = os.path.join(ROOT, "profiles", "ncu_k_assign_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        if j.get("workload") == workload:
+            return j.get("dram_bytes_per_launch"), j.get("file")
+    except Exception:
+        pass
+    return None, None
+
+
+# ------------------------------------------------------------------ reference arm (the CPU oracle)
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from gen import synth
+    from oracle import oracle
+    d = synth.make_config(args.config, n_nets=args.n_nets)
+    # size each step as a bounded prefix (priority order) of the workload: ~args.cpu_seconds / (W+K) s each
+    probe = oracle.run(d, solution=False, grids=False, timing=False, batches=False, max_nets=min(20000, d.n_nets))
+    rate = probe["nets_run"] / max(probe["elapsed_s"], 1e-9)
+    per_step_s = max(2.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    sample = int(min(d.n_nets, max(1000, rate * per_step_s)))
+    for _ in range(args.warmup):
+        oracle.run(d, solution=False, grids=False, timing=False, batches=False, max_nets=sample)
+    vals = []
+    for _ in range(args.steps):
+        r = oracle.run(d, solution=False, grids=False, timing=False, batches=False, max_nets=sample)
+        vals.append(r["nets_run"] / r["elapsed_s"])
+    v = statistics.median(vals)
+    model, ncpu = host_info()
+    desc = (f"first {sample} nets (priority order) of {d.name}, sequential fp64 oracle, 1 thread on {model} "
+            f"({ncpu} host cores); timed region = DP+backtrack+commit+Elmore, tree build excluded")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "nets/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sample / v,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": d.name, "sample_nets": sample},
+        "cpu_baseline": {"value": v, "unit": "nets/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": "nets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def cpu_baseline(d, seconds):
+    from oracle import oracle
+    probe = oracle.run(d, solution=False, grids=False, timing=False, batches=False, max_nets=min(20000, d.n_nets))
+    rate = probe["nets_run"] / max(probe["elapsed_s"], 1e-9)
+    sample = int(min(d.n_nets, max(1000, rate * seconds)))
+    r = oracle.run(d, solution=False, grids=False, timing=False, batches=False, max_nets=sample)
+    model, ncpu = host_info()
+    return {"value": r["nets_run"] / r["elapsed_s"], "unit": "nets/s", "cores": 1, "kind": "oracle",
+            "sample": (f"first {sample} nets (priority order) of {d.name}: sequential fp64 oracle, 1 thread of "
+                       f"{ncpu} ({model}); {r['elapsed_s']:.1f} s of DP+backtrack+commit+Elmore, tree build excluded")}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from gen import synth
+    from paper_2507_13375_b200 import la
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    d = synth.make_config(args.config, n_nets=args.n_nets)
+    nid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(la.la_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nid = bytes(buf.cpu().numpy().tobytes())
+    stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    t_setup = time.perf_counter()
+    A = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=nid, stream=stream.cuda_stream)
+    nb = A.load()
+    setup_s = time.perf_counter() - t_setup
+    st0 = A.stats()
+
+    def step():
+        A.reset()
+        A.assign_all()
+        la.la_eval_timing(A.ctx)   # device outputs only; synchronises
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    if args.ncu_pass:
+        barrier()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.profiler.stop()
+        if rank == 0:
+            print(json.dumps({"ncu_pass": True, "workload": d.name, "batches": nb}), flush=True)
+        return
+
+    A.profiling(True)
+    A.profile(reset=True)
+    launches0 = A.stats()["launches"]
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    prof = A.profile(reset=True)
+    A.profiling(False)
+    launches = (A.stats()["launches"] - launches0) // args.steps
+    sol = A.solution()
+    via_cuts = int((sol["vias"][:, 3] - sol["vias"][:, 2]).sum()) if len(sol["vias"]) else 0
+    st = A.stats()
+    value = d.n_nets / (ms / 1000.0)
+
+    # roofline of the dominant kernel (k_assign) from live CUDA-event times over the timed region
+    hbm, peak_src = peaks()
+    a_bytes, c_bytes, e_bytes = algorithmic_bytes(st, d.L, d.n_nets, via_cuts)
+    a_launch = prof["assign_launches"] / args.steps
+    a_ms = prof["assign_ms"] / args.steps           # k_assign device time per step (this rank's shard)
+    a_bytes_rank = a_bytes / world
+    achieved = a_bytes_rank / (a_ms / 1000.0) / 1e9 if a_ms > 0 else None
+    traffic_step, traffic_file = ncu_traffic(d.name)
+    roof = {"kernel": "k_assign (K4+K5: Alg. 3 DP + Alg. 4 backtrack)", "bound": "hbm",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None,
+            "traffic": traffic_step, "traffic_source": traffic_file,
+            "alg_bytes_per_launch": a_bytes_rank / max(a_launch, 1), "launches_per_step": a_launch,
+            "kernel_ms_per_step": a_ms, "kernel_share_of_step": a_ms / ms,
+            "peak_source": peak_src}
+    step_bytes = a_bytes + c_bytes + e_bytes
+    roof_step = {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / 1000.0) / 1e9,
+                 "frac": step_bytes / (ms / 1000.0) / 1e9 / hbm,
+                 "kernel_ms_per_step": {"k_assign": a_ms, "k_commit": prof["commit_ms"] / args.steps,
+                                        "k_elmore": prof["elmore_ms"] / args.steps,
+                                        "reconcile": prof["reconcile_ms"] / args.steps}}
+    A.close()
+
+    # e2e: the public API from host buffers: init_grid + load_nets + all batches + Elmore + solution to host
+    e2e = None
+    if not args.no_e2e:
+        vals, h2d, d2h = [], 0, 0
+        for i in range(args.e2e_steps + 1):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            B = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=None if world == 1 else nid,
+                                 stream=stream.cuda_stream)
+            B.load()
+            B.assign_all()
+            B.eval_timing()
+            B.solution()
+            torch.cuda.synchronize()
+            barrier()
+            dt = time.perf_counter() - t0
+            s2 = B.stats()
+            B.close()
+            if world > 1:
+                t = torch.tensor([dt], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
+            if i > 0:          # first pass is a warm-up
+                vals.append(dt)
+                h2d, d2h = s2["h2d_bytes"], s2["d2h_bytes"]
+        e2e = {"value": d.n_nets / statistics.median(vals), "unit": "nets/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "seconds_per_step": statistics.median(vals),
+               "includes": "la_init_grid + la_load_nets (host tree build, GPU batching, upload) + every batch + "
+                           "la_eval_timing + la_get_solution, pageable host buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(d, args.cpu_seconds)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "nets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": d.name, "nets": d.n_nets, "grid": f"{d.X}x{d.Y}", "layers": d.L,
+                       "pins": d.n_pins, "la_nodes": st["n_nodes"], "wirelength": st["wirelength"],
+                       "via_cuts": via_cuts, "batches": nb, "max_height": st["max_height"],
+                       "max_batch_nets": st["max_batch_nets"],
+                       "parallelism": f"dp{world}: nets of every conflict-free batch sharded over {world} GPU(s)",
+                       "l2": f"inputs > L2: {(4 * (st['via_state_words'] + st['wire_state_words']) + 50 * st['n_nodes']) / 1e9:.2f} GB touched per step",
+                       "setup_s": setup_s, "load_ms": st0["load_ms"], "batching_ms": st0["batch_ms"]},
+            "roofline": roof, "roofline_step": roof_step,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

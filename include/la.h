@@ -115,7 +115,17 @@ typedef struct {
     int64_t launches;           /* kernels launched by la_assign_* / la_commit_demand / la_eval_timing */
     double load_ms;             /* host tree build + upload inside la_load_nets                         */
     double batch_ms;            /* GPU batching pass (sort + Kahn layering) inside la_load_nets         */
+    int64_t wire_state_words;   /* sum over LA-tree edges of len x (#legal layers of the edge direction) */
+    int64_t via_state_words;    /* n_nodes x (L - 1)                                                      */
+    int64_t h2d_bytes, d2h_bytes;   /* host<->device bytes copied by the library since init             */
 } la_stats;
+
+/* Per-kernel device time, from CUDA events recorded on the context stream
+ * around every launch while profiling is enabled (la_set_profiling). */
+typedef struct {
+    int64_t assign_launches, commit_launches, elmore_launches, reconcile_calls;
+    double assign_ms, commit_ms, elmore_ms, reconcile_ms;
+} la_profile;
 
 /* Create a context: validate the grid, allocate the packed device demand
  * planes, build the Eq. (3) marginal tables and the via-R table, set up NCCL
@@ -180,6 +190,17 @@ la_status la_get_batches(la_ctx *ctx, int32_t *batch_of);
 la_status la_reset(la_ctx *ctx);
 
 la_status la_get_stats(la_ctx *ctx, la_stats *out);
+
+/* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
+la_status la_set_profiling(la_ctx *ctx, int32_t enable);
+
+/* Accumulated per-kernel device times since the last reset (synchronises).
+ * reset != 0 clears the accumulators after reading. */
+la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset);
+
+/* Create an ncclUniqueId (128 bytes) on rank 0, to be broadcast to every rank
+ * and passed as la_grid_desc.nccl_id. */
+la_status la_nccl_unique_id(void *out128);
 
 /* Wait for all enqueued work; surfaces asynchronous CUDA errors. */
 la_status la_sync(la_ctx *ctx);

@@ -588,6 +588,7 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     if (out->sink_delay) for (int64_t p = 0; p < nets->pin_ptr[NN]; p++) out->sink_delay[p] = 0.0;
 
     double elapsed = 0.0;
+    std::vector<double> dummy;   // sink-delay sink when the caller passes none
     Tree T;
     NetState st;
     for (int64_t oi = 0; oi < nrun; oi++) {
@@ -656,9 +657,8 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
         }
         // O9 Elmore
         double ncap = 0, nrc = 0;
-        std::vector<double> dummy;
         double *sd = out->sink_delay;
-        if (!sd) { dummy.assign(nets->pin_ptr[NN], 0.0); sd = dummy.data(); }
+        if (!sd) { if (dummy.empty()) dummy.assign(nets->pin_ptr[NN], 0.0); sd = dummy.data(); }
         elmore(C, nets, drv, T, st, sd, &ncap, &nrc);
         auto t1 = std::chrono::steady_clock::now();
         elapsed += std::chrono::duration<double>(t1 - t0).count();

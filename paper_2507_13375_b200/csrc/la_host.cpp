@@ -89,11 +89,26 @@ struct la_ctx {
     la_stats stats{};
     ncclComm_t comm = nullptr;
 
+    // CUDA-event profiling of kernel launches
+    struct Span { int kind; cudaEvent_t a, b; };
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<Span> spans;
+    la_profile acc{};
+    cudaEvent_t ev_get() {
+        if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+
     ~la_ctx() {
         for (void *p : dev_allocs) cudaFree(p);
         void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab};
         for (void *p : gp) if (p) cudaFree(p);
         if (comm) ncclCommDestroy(comm);
+        for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
+        for (auto e : ev_pool) cudaEventDestroy(e);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
 };
@@ -131,8 +146,25 @@ la_status dev_upload(la_ctx *ctx, T **dst, const T *src, size_t n) {
     }
     ctx->dev_allocs.push_back(p);
     *dst = static_cast<T *>(p);
-    if (src && n) CK(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    if (src && n) {
+        CK(cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->stats.h2d_bytes += (int64_t)(n * sizeof(T));
+    }
     return LA_OK;
+}
+
+enum { K_ASSIGN = 0, K_COMMIT = 1, K_ELMORE = 2, K_RECONCILE = 3 };
+
+// Profiling brackets: record a CUDA event before / after a launch on the context stream.
+int prof_begin(la_ctx *ctx, int kind) {
+    if (!ctx->prof) return -1;
+    la_ctx::Span sp{kind, ctx->ev_get(), ctx->ev_get()};
+    cudaEventRecord(sp.a, ctx->stream);
+    ctx->spans.push_back(sp);
+    return (int)ctx->spans.size() - 1;
+}
+void prof_end(la_ctx *ctx, int i) {
+    if (i >= 0) cudaEventRecord(ctx->spans[i].b, ctx->stream);
 }
 
 template <class T>
@@ -172,11 +204,13 @@ struct BuiltNet {
     std::vector<int64_t> p_orig;
     std::vector<uint64_t> fp;      // footprint elements
     int64_t wl = 0;
+    int64_t wsw = 0;               // sum over tree edges of len x #legal layers of the edge direction
 };
 
 struct Builder {
     const la_ctx *ctx;
     const la_net_desc *nd;
+    int nlegal[2] = {0, 0};        // routable layers per direction
     // scratch
     std::vector<uint64_t> ek;      // edge keys: gcell * 2 + t  (t = 0 H (x,y)-(x+1,y), 1 V (x,y)-(x,y+1))
     std::vector<uint64_t> vs;      // vertex gcells
@@ -405,6 +439,9 @@ struct Builder {
         const uint64_t gbase = (uint64_t)2 * X * Y;
         for (size_t n = 0; n < nn; n++) out.fp.push_back(gbase + (uint64_t)py[n] * X + px[n]);
         out.wl = (int64_t)ek.size();
+        out.wsw = 0;
+        for (size_t n = 0; n < nn; n++)
+            if (ppar[n] >= 0) out.wsw += (int64_t)plen[n] * nlegal[(pedir[n] == DIR_E || pedir[n] == DIR_W) ? 0 : 1];
         return "";
     }
 };
@@ -416,7 +453,7 @@ struct Chunk {
     BuiltNet acc;                                      // concatenated arrays
     std::string err;
     int64_t err_net = -1;
-    int64_t wl = 0;
+    int64_t wl = 0, wsw = 0;
     int max_height = 0;
 };
 
@@ -539,6 +576,7 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
         if (src && n) {
             ee = cudaMemcpyAsync(p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream);
             if (ee != cudaSuccess) return set_err(LA_ECUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(ee));
+            ctx->stats.h2d_bytes += (int64_t)(n * sizeof(T));
         }
         return LA_OK;
     };
@@ -629,6 +667,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     std::atomic<int64_t> next{0};
     auto worker = [&]() {
         Builder B{ctx, n};
+        for (int l = 0; l < ctx->L; l++) if (ctx->routable[l]) B.nlegal[ctx->dir[l]]++;
         BuiltNet bn;
         for (;;) {
             int64_t c = next.fetch_add(1);
@@ -650,6 +689,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                 ch.sink_off.push_back((int64_t)a.p_layer.size());
                 ch.fp_off.push_back((int64_t)a.fp.size());
                 ch.wl += bn.wl;
+                ch.wsw += bn.wsw;
                 if (!bn.height.empty()) ch.max_height = std::max<int>(ch.max_height, bn.height.back());
             }
         }
@@ -804,9 +844,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         for (auto &t : th) t.join();
     }
     if (NN >= ((int64_t)1 << 31) || NS >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "forest too large");
-    int64_t wl = 0;
+    int64_t wl = 0, wsw = 0;
     int maxh = 0;
-    for (auto &ch : chunks) { wl += ch.wl; maxh = std::max(maxh, ch.max_height); }
+    for (auto &ch : chunks) { wl += ch.wl; wsw += ch.wsw; maxh = std::max(maxh, ch.max_height); }
     chunks.clear();
     chunks.shrink_to_fit();
 
@@ -849,6 +889,10 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     stt.n_nets = N; stt.n_pins = ctx->n_pins; stt.n_nodes = NN; stt.n_sinks = NS;
     stt.wirelength = wl; stt.footprint = n_fp; stt.n_batches = nb; stt.max_height = maxh;
     stt.max_net_nodes = max_nodes;
+    stt.wire_state_words = wsw;
+    stt.via_state_words = NN * (ctx->L - 1);
+    stt.h2d_bytes += n_fp * 8;      // batching keys
+    stt.d2h_bytes += N * 4;         // batch ids
     stt.max_batch_nets = 0;
     for (int32_t b = 0; b < nb; b++)
         stt.max_batch_nets = std::max(stt.max_batch_nets, ctx->batch_net0[b + 1] - ctx->batch_net0[b]);
@@ -878,7 +922,9 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
     if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
+    int pi = prof_begin(ctx, K_ASSIGN);
     CK(launch_assign(ctx->G, ctx->F, ctx->S, b0 + s0, b0 + s1, ctx->stream));
+    prof_end(ctx, pi);
     ctx->stats.launches += 1;
     ctx->pending_commit = true;
     return LA_OK;
@@ -895,6 +941,7 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
         int64_t s0, s1;
         la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
         const int64_t m0 = ctx->h_net_node0[b0 + s0], m1 = ctx->h_net_node0[b0 + s1];
+        int pr = prof_begin(ctx, K_RECONCILE);
         CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
         CK(launch_pack_decisions(ctx->S, m0, m1, ctx->stream));
         NK(ncclAllReduce(ctx->S.dec + n0, ctx->S.dec + n0, (size_t)(n1 - n0), ncclUint32, ncclSum, ctx->comm,
@@ -902,9 +949,12 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
         NK(ncclAllReduce(ctx->S.froot + b0, ctx->S.froot + b0, (size_t)(b1 - b0), ncclFloat64, ncclSum, ctx->comm,
                          ctx->stream));
         CK(launch_unpack_decisions(ctx->S, n0, n1, ctx->stream));
+        prof_end(ctx, pr);
         ctx->stats.launches += 2;
     }
+    int pc = prof_begin(ctx, K_COMMIT);
     CK(launch_commit(ctx->G, ctx->F, ctx->S, n0, n1, ctx->stream));
+    prof_end(ctx, pc);
     ctx->stats.launches += 1;
     ctx->pending_commit = false;
     ctx->next_batch = batch + 1;
@@ -931,7 +981,9 @@ static la_status require_done(la_ctx *ctx) {
 la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, double *net_rc) {
     TRY(require_done(ctx));
     if (ctx->n_pins) CK(cudaMemsetAsync(ctx->S.sink_delay, 0, sizeof(double) * ctx->n_pins, ctx->stream));
+    int pe = prof_begin(ctx, K_ELMORE);
     CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_nets, ctx->stream));
+    prof_end(ctx, pe);
     ctx->stats.launches += 1;
     if (sink_delay && ctx->n_pins)
         CK(cudaMemcpyAsync(sink_delay, ctx->S.sink_delay, sizeof(double) * ctx->n_pins, cudaMemcpyDeviceToHost, ctx->stream));
@@ -940,6 +992,8 @@ la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, doubl
     if (net_rc && ctx->n_nets)
         CK(cudaMemcpyAsync(net_rc, ctx->S.net_rc, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.d2h_bytes += (sink_delay ? 8 * ctx->n_pins : 0) + (net_cap ? 8 * ctx->n_nets : 0) +
+                            (net_rc ? 8 * ctx->n_nets : 0);
     return LA_OK;
 }
 
@@ -956,6 +1010,7 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     }
     if (N) CK(cudaMemcpyAsync(froot.data(), ctx->S.froot, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.d2h_bytes += 3 * NN + 8 * N;
     // per input net: counts
     std::vector<int64_t> nw(N + 1, 0), nv(N + 1, 0);
     std::vector<int64_t> pos_of(N);
@@ -1024,6 +1079,8 @@ la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem) {
     if (e == cudaSuccess && via_dem)
         e = cudaMemcpyAsync(via_dem, dv, sizeof(int32_t) * ctx->n_via_api, cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess)
+        ctx->stats.d2h_bytes += (wire_dem ? 4 * ctx->n_wire_api : 0) + (via_dem ? 4 * ctx->n_via_api : 0);
     cudaFree(dw);
     if (dv) cudaFree(dv);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_demand");
@@ -1052,6 +1109,43 @@ la_status la_reset(la_ctx *ctx) {
 la_status la_get_stats(la_ctx *ctx, la_stats *out) {
     if (!ctx || !out) return set_err(LA_EINVAL, "null argument");
     *out = ctx->stats;
+    return LA_OK;
+}
+
+la_status la_set_profiling(la_ctx *ctx, int32_t enable) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    ctx->prof = enable != 0;
+    return LA_OK;
+}
+
+la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset) {
+    if (!ctx || !out) return set_err(LA_EINVAL, "null argument");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto &sp : ctx->spans) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, sp.a, sp.b));
+        switch (sp.kind) {
+            case K_ASSIGN: ctx->acc.assign_ms += ms; ctx->acc.assign_launches++; break;
+            case K_COMMIT: ctx->acc.commit_ms += ms; ctx->acc.commit_launches++; break;
+            case K_ELMORE: ctx->acc.elmore_ms += ms; ctx->acc.elmore_launches++; break;
+            default: ctx->acc.reconcile_ms += ms; ctx->acc.reconcile_calls++; break;
+        }
+        ctx->ev_pool.push_back(sp.a);
+        ctx->ev_pool.push_back(sp.b);
+    }
+    ctx->spans.clear();
+    *out = ctx->acc;
+    if (reset) ctx->acc = la_profile{};
+    return LA_OK;
+}
+
+la_status la_nccl_unique_id(void *out128) {
+    if (!out128) return set_err(LA_EINVAL, "null argument");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return set_err(LA_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, &id, sizeof(id));
     return LA_OK;
 }
 

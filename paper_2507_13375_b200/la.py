@@ -53,7 +53,17 @@ class la_stats(ctypes.Structure):
     _fields_ = [("n_nets", c_i64), ("n_pins", c_i64), ("n_nodes", c_i64), ("n_sinks", c_i64),
                 ("wirelength", c_i64), ("footprint", c_i64), ("n_batches", c_i32), ("max_height", c_i32),
                 ("max_batch_nets", c_i64), ("max_net_nodes", c_i64), ("via_cuts", c_i64), ("launches", c_i64),
-                ("load_ms", c_f64), ("batch_ms", c_f64)]
+                ("load_ms", c_f64), ("batch_ms", c_f64), ("wire_state_words", c_i64), ("via_state_words", c_i64),
+                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class la_profile(ctypes.Structure):
+    _fields_ = [("assign_launches", c_i64), ("commit_launches", c_i64), ("elmore_launches", c_i64),
+                ("reconcile_calls", c_i64), ("assign_ms", c_f64), ("commit_ms", c_f64), ("elmore_ms", c_f64),
+                ("reconcile_ms", c_f64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -80,6 +90,9 @@ def _load():
         "la_destroy": ([c_void_p], None),
         "la_last_error": ([], ctypes.c_char_p),
         "la_shard_range": ([c_i64, c_i32, c_i32, P(c_i64), P(c_i64)], None),
+        "la_set_profiling": ([c_void_p, c_i32], c_i32),
+        "la_get_profile": ([c_void_p, P(la_profile), c_i32], c_i32),
+        "la_nccl_unique_id": ([c_void_p], c_i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -91,7 +104,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
-           "la_last_error", "la_shard_range")
+           "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id")
 
 
 def _check(st):
@@ -175,6 +188,22 @@ def la_shard_range(n: int, world: int, rank: int):
     b, e = c_i64(), c_i64()
     _lib.la_shard_range(n, world, rank, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+def la_set_profiling(ctx, enable: bool):
+    _check(_lib.la_set_profiling(ctx, 1 if enable else 0))
+
+
+def la_get_profile(ctx, reset: bool = True) -> dict:
+    p = la_profile()
+    _check(_lib.la_get_profile(ctx, ctypes.byref(p), 1 if reset else 0))
+    return p.as_dict()
+
+
+def la_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.la_nccl_unique_id(ctypes.cast(buf, c_void_p)))
+    return buf.raw
 
 
 # ------------------------------------------------------------ convenience ---
@@ -279,6 +308,12 @@ class LayerAssigner:
 
     def stats(self):
         return la_get_stats(self.ctx)
+
+    def profiling(self, enable: bool):
+        la_set_profiling(self.ctx, enable)
+
+    def profile(self, reset: bool = True):
+        return la_get_profile(self.ctx, reset)
 
     def sync(self):
         la_sync(self.ctx)
