@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 SO = os.path.join(LIBDIR, "libgapla.so")
-SOURCES = ["la_host.cpp", "la_kernels.cu", "la_batch.cu"]
+SOURCES = ["la_host.cpp", "la_kernels.cu", "la_assign.cu", "la_batch.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -26,7 +26,8 @@ def nccl_dir() -> str:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "la_internal.h"), os.path.join(ROOT, "include", "la.h")]
+    deps = srcs + [os.path.join(CSRC, "la_internal.h"), os.path.join(CSRC, "la_device.cuh"),
+                   os.path.join(ROOT, "include", "la.h")]
     if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in deps):
         return SO
     os.makedirs(LIBDIR, exist_ok=True)

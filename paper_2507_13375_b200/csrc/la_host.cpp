@@ -81,6 +81,9 @@ struct la_ctx {
     std::vector<uint8_t> h_edir;
     std::vector<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
+    std::vector<int64_t> batch_nbig;          // per batch: leading nets that take the CTA-per-net path
+    int32_t LD = 0, MP = 0;                   // layer slots per direction; max pair tasks per node
+    bool fuse_commit = true;
     std::vector<int32_t> batch_of_net;        // input order
     DevForest F{};
     DevScratch S{};
@@ -197,7 +200,7 @@ struct BuiltNet {
     std::vector<int32_t> sink0;    // local sink offset
     std::vector<uint16_t> nsink;
     std::vector<double> wd, ur;
-    std::vector<uint8_t> height;
+    std::vector<uint16_t> height;
     // sinks grouped by node in final node order
     std::vector<uint8_t> p_layer;
     std::vector<double> p_cap, p_w;
@@ -422,7 +425,7 @@ struct Builder {
             out.nh[i] = (uint8_t)(pnh[n] < 0 ? 255 : pnh[n]);
             out.wd[i] = ctx->W_D * w[n];
             out.ur[i] = ur[n];
-            out.height[i] = (uint8_t)std::min(pheight[n], 255);
+            out.height[i] = (uint16_t)std::min(pheight[n], 65535);
             out.sink0[i] = (int32_t)out.p_layer.size();
             out.nsink[i] = (uint16_t)psinks[n].size();
             for (int64_t q : psinks[n]) {
@@ -712,6 +715,13 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         int64_t i = net - ch.beg;
         return ch.node_off[i + 1] - ch.node_off[i];
     };
+    auto nsinks_of = [&](int64_t net) {
+        const Chunk &ch = chunks[chunk_of[net]];
+        int64_t i = net - ch.beg;
+        return ch.sink_off[i + 1] - ch.sink_off[i];
+    };
+    // nets whose whole DP state fits a warp's shared memory take the warp path
+    auto is_big = [&](int64_t net) { return nnodes_of(net) > NS_MAX || nsinks_of(net) > NP_MAX; };
 
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
@@ -778,9 +788,23 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             int64_t net = by_rank[r];
             pos_net[cur[ctx->batch_of_net[net]]++] = net;
         }
+        // big nets (CTA path) first, then by node count descending: the longest nets start first
         for (int32_t b = 0; b < nb; b++)
             std::stable_sort(pos_net.begin() + ctx->batch_net0[b], pos_net.begin() + ctx->batch_net0[b + 1],
-                             [&](int64_t a, int64_t c) { return nnodes_of(a) > nnodes_of(c); });
+                             [&](int64_t a, int64_t c) {
+                                 const bool ba = is_big(a), bc = is_big(c);
+                                 if (ba != bc) return ba;
+                                 return nnodes_of(a) > nnodes_of(c);
+                             });
+    }
+    // per batch: number of big nets (they lead the batch) and their node count
+    ctx->batch_nbig.assign(nb, 0);
+    int64_t max_big_nodes = 0;
+    for (int32_t b = 0; b < nb; b++) {
+        int64_t k = ctx->batch_net0[b], nodes = 0;
+        while (k < ctx->batch_net0[b + 1] && is_big(pos_net[k])) { nodes += nnodes_of(pos_net[k]); k++; }
+        ctx->batch_nbig[b] = k - ctx->batch_net0[b];
+        max_big_nodes = std::max(max_big_nodes, nodes);
     }
     // offsets in final order
     std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
@@ -801,7 +825,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     std::vector<uint32_t> xy(NN);
     std::vector<int32_t> kid(NN * 4), len(NN), sink0(NN);
     std::vector<uint8_t> edir(NN), nkid(NN), nl(NN), nh(NN), pdrv(N);
-    std::vector<uint16_t> nsink(NN);
+    std::vector<uint16_t> nsink(NN), height(NN);
     std::vector<double> wd(NN), ur(NN);
     std::vector<uint8_t> p_layer(NS);
     std::vector<double> p_cap(NS), p_w(NS);
@@ -829,7 +853,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                         for (int j = 0; j < 4; j++) kid[d * 4 + j] = A.kid[k * 4 + j] < 0 ? -1 : (int32_t)(d0 + A.kid[k * 4 + j]);
                         len[d] = A.len[k]; edir[d] = A.edir[k]; nkid[d] = A.nkid[k]; nl[d] = A.nl[k]; nh[d] = A.nh[k];
                         sink0[d] = (int32_t)(e0 + A.sink0[k]);
-                        nsink[d] = A.nsink[k]; wd[d] = A.wd[k]; ur[d] = A.ur[k];
+                        nsink[d] = A.nsink[k]; wd[d] = A.wd[k]; ur[d] = A.ur[k]; height[d] = A.height[k];
                     }
                     for (int64_t q = q0; q < ch.sink_off[i + 1]; q++) {
                         int64_t d = e0 + (q - q0);
@@ -850,27 +874,36 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     chunks.clear();
     chunks.shrink_to_fit();
 
+    ctx->LD = std::max(ctx->LH, ctx->LV);
+    {
+        int mp[2] = {0, 0};
+        for (int l = 0; l < ctx->L; l++) mp[ctx->dir[l]] += l + 1;
+        ctx->MP = std::max(ctx->L, std::max(mp[0], mp[1]));
+    }
+
     // ---- upload forest, allocate scratch
     DevForest &F = ctx->F;
     F.n_nets = N; F.n_nodes = NN; F.n_sinks = NS;
     uint32_t *d_xy; int32_t *d_kid, *d_len, *d_sink0; uint8_t *d_edir, *d_nkid, *d_nl, *d_nh, *d_pl, *d_pdrv;
-    uint16_t *d_nsink; double *d_wd, *d_ur, *d_pc, *d_pw; int64_t *d_po, *d_node0, *d_netid;
+    uint16_t *d_nsink, *d_height; double *d_wd, *d_ur, *d_pc, *d_pw; int64_t *d_po, *d_node0, *d_netid;
     TRY(dev_upload(ctx, &d_xy, xy.data(), NN)); TRY(dev_upload(ctx, &d_kid, kid.data(), NN * 4));
     TRY(dev_upload(ctx, &d_len, len.data(), NN)); TRY(dev_upload(ctx, &d_sink0, sink0.data(), NN));
     TRY(dev_upload(ctx, &d_edir, edir.data(), NN)); TRY(dev_upload(ctx, &d_nkid, nkid.data(), NN));
     TRY(dev_upload(ctx, &d_nl, nl.data(), NN)); TRY(dev_upload(ctx, &d_nh, nh.data(), NN));
     TRY(dev_upload(ctx, &d_nsink, nsink.data(), NN)); TRY(dev_upload(ctx, &d_wd, wd.data(), NN));
+    TRY(dev_upload(ctx, &d_height, height.data(), NN));
     TRY(dev_upload(ctx, &d_ur, ur.data(), NN)); TRY(dev_upload(ctx, &d_pl, p_layer.data(), NS));
     TRY(dev_upload(ctx, &d_pc, p_cap.data(), NS)); TRY(dev_upload(ctx, &d_pw, p_w.data(), NS));
     TRY(dev_upload(ctx, &d_po, p_orig.data(), NS)); TRY(dev_upload(ctx, &d_node0, node0.data(), N + 1));
     TRY(dev_upload(ctx, &d_netid, net_id.data(), N)); TRY(dev_upload(ctx, &d_pdrv, pdrv.data(), N));
     F.xy = d_xy; F.kid = d_kid; F.len = d_len; F.edir = d_edir; F.nkid = d_nkid; F.nl = d_nl; F.nh = d_nh;
     F.sink0 = d_sink0; F.nsink = d_nsink; F.wd = d_wd; F.ur = d_ur; F.p_layer = d_pl; F.p_cap = d_pc; F.p_w = d_pw;
-    F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv;
+    F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv; F.height = d_height;
     DevScratch &S = ctx->S;
-    const size_t NL = (size_t)NN * ctx->L;
-    TRY(dev_alloc(ctx, &S.A, NL)); TRY(dev_alloc(ctx, &S.B, NL)); TRY(dev_alloc(ctx, &S.Cap, NL));
-    TRY(dev_alloc(ctx, &S.choice, NL)); TRY(dev_alloc(ctx, &S.entry, NL)); TRY(dev_alloc(ctx, &S.froot, N));
+    const size_t BL = (size_t)std::max<int64_t>(max_big_nodes, 1) * ctx->LD;
+    TRY(dev_alloc(ctx, &S.bkap, (size_t)std::max<int64_t>(max_big_nodes, 1) * (ctx->L - 1)));
+    TRY(dev_alloc(ctx, &S.bA, BL)); TRY(dev_alloc(ctx, &S.bB, BL)); TRY(dev_alloc(ctx, &S.bC, BL));
+    TRY(dev_alloc(ctx, &S.bchoice, BL)); TRY(dev_alloc(ctx, &S.bentry, BL)); TRY(dev_alloc(ctx, &S.froot, N));
     TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
     TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
@@ -922,8 +955,16 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
     if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
+    AssignLaunch al;
+    al.net_beg = b0 + s0;
+    al.net_end = b0 + s1;
+    al.nbig = std::max<int64_t>(0, std::min<int64_t>(ctx->batch_nbig[batch], s1) - s0);
+    al.node_base = ctx->h_net_node0[b0];
+    al.LD = ctx->LD;
+    al.MP = ctx->MP;
+    al.commit = (ctx->world == 1 && ctx->fuse_commit) ? 1 : 0;
     int pi = prof_begin(ctx, K_ASSIGN);
-    CK(launch_assign(ctx->G, ctx->F, ctx->S, b0 + s0, b0 + s1, ctx->stream));
+    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, ctx->stream));
     prof_end(ctx, pi);
     ctx->stats.launches += 1;
     ctx->pending_commit = true;
@@ -952,10 +993,12 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
         prof_end(ctx, pr);
         ctx->stats.launches += 2;
     }
-    int pc = prof_begin(ctx, K_COMMIT);
-    CK(launch_commit(ctx->G, ctx->F, ctx->S, n0, n1, ctx->stream));
-    prof_end(ctx, pc);
-    ctx->stats.launches += 1;
+    if (!(ctx->world == 1 && ctx->fuse_commit)) {   // else already committed inside k_assign
+        int pc = prof_begin(ctx, K_COMMIT);
+        CK(launch_commit(ctx->G, ctx->F, ctx->S, n0, n1, ctx->stream));
+        prof_end(ctx, pc);
+        ctx->stats.launches += 1;
+    }
     ctx->pending_commit = false;
     ctx->next_batch = batch + 1;
     return LA_OK;

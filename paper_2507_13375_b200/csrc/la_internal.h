@@ -48,6 +48,7 @@ struct DevForest {
     const int32_t *len;                       // parent-edge length (unit edges)
     const uint8_t *edir;                      // direction parent -> node (0 E, 1 W, 2 N, 3 S); NO_DIR at root
     const uint8_t *nkid, *nl, *nh;            // #children; lowest / highest pin layer (driver incl.); nl=255 if none
+    const uint16_t *height;                   // height (leaves 0)
     const int32_t *sink0;                     // first sink (pin arrays) of the node
     const uint16_t *nsink;
     const double *wd, *ur;                    // W_D * w_n (Eq. 5), ur (O3)
@@ -59,10 +60,20 @@ struct DevForest {
     const uint8_t *net_pdrv;                  // driver pin layer
 };
 
+// Capacities of the warp-per-net (small) path of k_assign: a net whose LA tree
+// has at most NS_MAX nodes and at most NP_MAX sinks keeps all its DP state in
+// shared memory; larger nets take the CTA-per-net (big) path.
+constexpr int NS_MAX = 32;
+constexpr int NP_MAX = 64;
+constexpr int ASSIGN_WARPS = 4;
+
 struct DevScratch {
-    double *A, *B, *Cap;                      // [n_nodes][L] O5 parent-edge terms of each node
-    uint16_t *choice;                         // [n_nodes][L] b | t << 8
-    uint32_t *entry;                          // [n_nodes][L] son layers, byte i = son i
+    // big-path DP state, indexed by (node - first node of the batch); sized for
+    // the largest total node count of big nets in any batch
+    double *bkap;                             // [.][L-1] ViaCong per cut
+    double *bA, *bB, *bC;                     // [.][LD] O5 parent-edge terms by layer slot (bA holds S first)
+    uint16_t *bchoice;                        // [.][LD] b | t << 8
+    uint32_t *bentry;                         // [.][LD] son layers, byte i = son i
     double *froot;                            // [n_nets] f[root][p_drv]
     uint8_t *lay, *sb, *st;                   // decisions per node: entry layer, span (b, t)
     uint32_t *dec;                            // packed decisions for the multi-GPU reconcile
@@ -75,8 +86,17 @@ cudaError_t launch_pack_state(const DevGrid &G, const int32_t *wcap, const int32
                               const int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
 cudaError_t launch_unpack_demand(const DevGrid &G, const int32_t *wcap, const int32_t *vcap, int32_t *wdem,
                                  int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
-cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
-                          int64_t net_end, cudaStream_t s);
+struct AssignLaunch {
+    int64_t net_beg, net_end;                 // nets of this launch (batch-major)
+    int64_t nbig;                             // the first nbig of them take the big path
+    int64_t node_base;                        // first node of the batch: base of the big-path scratch
+    int32_t LD;                               // max(#H layers, #V layers): layer slots per direction
+    int32_t MP;                               // max (entry layer, span bottom) tasks of one node
+    int32_t commit;                           // fuse the demand commit (K8) into the kernel
+};
+size_t assign_smem_bytes(int L, int LD, int MP);
+cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a,
+                          cudaStream_t s);
 cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t node_beg,
                           int64_t node_end, cudaStream_t s);
 cudaError_t launch_pack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);
