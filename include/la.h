@@ -142,8 +142,8 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out);
  * Writes the number of batches.  Collective when world > 1.
  * Errors: LA_EINVAL for a pin layer >= L, a pin or segment outside the grid,
  * a non-axis-aligned segment, a route that is not a tree, a pin GCell not on
- * the route, a net without pins (message names the net); LA_ESTATE if nets
- * were already loaded. */
+ * the route, a net without pins, a net with more than 65534 LA-tree nodes or
+ * sinks (message names the net); LA_ESTATE if nets were already loaded. */
 la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches);
 
 /* Alg. 3 + Alg. 4 for batch k on this rank's shard of the batch: bottom-up
@@ -158,9 +158,18 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch);
  * Errors: LA_ESTATE unless batch k was just assigned. */
 la_status la_commit_demand(la_ctx *ctx, int32_t batch);
 
-/* Convenience: la_assign_batch + la_commit_demand for every remaining batch
- * (the whole Alg. 2 loop), enqueued back to back.  Collective. */
+/* Every remaining batch (the whole Alg. 2 loop), enqueued.  Collective.
+ * With one rank, schedule LA_SCHED_DATAFLOW (the default) and no batch assigned
+ * since the last load / la_reset, this is ONE persistent launch in which each
+ * net starts as soon as every earlier-priority net sharing a footprint element
+ * with it has committed; the results are bit-identical to the
+ * batch-by-batch schedule and to sequential assignment.  Otherwise it is
+ * la_assign_batch + la_commit_demand for every remaining batch. */
 la_status la_assign_all(la_ctx *ctx);
+
+/* Schedule used by la_assign_all on one rank. */
+enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };
+la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an unknown value */
 
 /* Elmore delay / downstream capacitance over the 3D RC trees of every net
  * (DESIGN §3 O9).  Outputs (any may be NULL): sink_delay[n_pins] in input pin

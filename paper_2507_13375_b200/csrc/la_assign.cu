@@ -1,27 +1,30 @@
-// K4 + K5 (+ fused K8): Alg. 3 getSubtreeCandidate + Alg. 4 traceBackSolution
-// for every net of one conflict-free batch, in ONE launch.
+// K4 + K5 + fused K8: Alg. 3 getSubtreeCandidate + Alg. 4 traceBackSolution
+// and the demand commit, for every net, as ONE kernel.
 //
-// Design ("k_assign"): the paper launches one thread per (node,
-// layer) and one launch per tree level (Alg. 2, l.345-351).  On B200 that is
-// launch- and latency-bound (~100 batches x tens of levels), so here:
-//   * small nets (<= NS_MAX nodes, <= NP_MAX sinks, ~99% of nets): ONE WARP PER
-//     NET.  The warp first gathers everything the DP reads from HBM -- node
-//     records, sinks, the via-cut words of every node GCell (-> ViaCong kappa)
-//     and the wire words of every parent run on every legal layer (-> the
-//     congestion sum S) -- with all loads of the net in flight at once, into
-//     shared memory.  The DP then runs entirely out of shared memory, node by
-//     node in height order: lanes own (entry layer l, span bottom b) tasks and
-//     sweep the span top t upward with each son's running argmin of cost'
-//     (l.370-395); one lane per entry layer reduces by the key (G', t-b, b)
-//     (l.404).  Backtrack is level-parallel over lanes (l.418-435).
-//   * big nets: ONE CTA PER NET, the same node routine with DP state in a
-//     global (L2-resident) scratch, nodes of one height level spread over the
-//     CTA's warps, one __syncthreads per level.
-//   * the demand commit of the batch (K8) is fused at the end when there is a
-//     single rank: batches are conflict-free, so no net of the batch reads what
-//     another commits.
-// Bit-exactness: compiled with --fmad=false; expression trees and operand order
-// exactly as DESIGN §3 O5/O6; min/argmin only across lanes, never sums.
+// Design (DESIGN §5 "k_assign", §2):
+//   * Work items.  The forest is batch-major; items are, in that
+//     order, either ONE big net (more than NS nodes or NP sinks) run by the whole
+//     CTA, or up to ASSIGN_WARPS consecutive small nets, one warp each.  CTAs are
+//     persistent and grab items with an atomic ticket.
+//   * Batch mode (la_assign_batch): the items of one conflict-free batch.
+//     Dataflow mode (la_assign_all, one GPU): ALL items in one cooperative launch;
+//     a net waits until its per-net count of unfinished predecessors (the
+//     conflict DAG) is 0, and after its commit releases its
+//     successors.  Items are taken in a topological order, so every waited-on
+//     net is held by a running CTA: no deadlock.
+//   * Per net: (1) gather everything the DP reads from HBM -- node records,
+//     sinks, the via-cut words of every node GCell and the congestion sum S of
+//     every parent run on every legal layer -- with all loads in flight at once,
+//     into shared memory; (2) leaves, all at once, lanes over (leaf, entry
+//     layer); (3) internal nodes in height order, one warp per node: per-son
+//     candidate table cost'(l; s, j) for all (entry layer, son layer) pairs,
+//     lanes over (entry layer l, span-bottom group) sweep the span top t upward
+//     with each son's running argmin (Alg. 3 l.370-395), a segmented shuffle
+//     argmin by the key (G', t-b, b) (l.404, reading R21) picks each entry
+//     layer's span; (4) level-parallel backtrack (Alg. 4); (5) decisions to HBM
+//     and the integer-atomic demand commit (O8).
+// Bit-exactness: compiled with --fmad=false; every fp64 value is the DESIGN §3
+// expression tree in operand order; cross-lane reductions are min/argmin only.
 #include <cuda_runtime.h>
 
 #include "la_device.cuh"
@@ -31,276 +34,320 @@ namespace gapla {
 namespace {
 
 // ---------------------------------------------------------------- layouts --
-// Per-warp shared-memory layout of the small path (byte offsets).
-struct WLay {
-    int wd, ur, kap, A, B, C, pcap, pw, pGp, pG, pK;        // double
-    int xy, len, entry, pjs;                                // uint32
-    int choice, nsink, sink0;                               // uint16
-    int edir, nkid, nl, nh, kid, height, lay, sb, st, player, pl, pb, pt;   // uint8
+// One net's DP state (NS nodes, NP sinks), as byte offsets from a base.
+struct NetLay {
+    int wd, ur, A, C, pcap, pw, froot;                      // double
+    int xy, vw;                                              // 32-bit
+    int len, height, nsink, sink0, kid, entry;               // 16-bit
+    int edir, nkid, nl, nh, choice, lay, sb, st, player;     // 8-bit
     int bytes;
 };
 
-__host__ __device__ inline WLay wlayout(int L, int LD, int MP) {
-    WLay w;
+__host__ __device__ inline NetLay net_layout(int NS, int NP, int L, int LD) {
+    NetLay w;
     int o = 0;
     auto take = [&](int bytes) { int r = o; o += (bytes + 7) & ~7; return r; };
-    const int NS = NS_MAX, NP = NP_MAX;
-    w.wd = take(8 * NS); w.ur = take(8 * NS); w.kap = take(8 * NS * (L - 1));
-    w.A = take(8 * NS * LD); w.B = take(8 * NS * LD); w.C = take(8 * NS * LD);
-    w.pcap = take(8 * NP); w.pw = take(8 * NP);
-    w.pGp = take(8 * MP); w.pG = take(8 * MP); w.pK = take(8 * MP);
-    w.xy = take(4 * NS); w.len = take(4 * NS); w.entry = take(4 * NS * LD); w.pjs = take(4 * MP);
-    w.choice = take(2 * NS * LD); w.nsink = take(2 * NS); w.sink0 = take(2 * NS);
-    w.edir = take(NS); w.nkid = take(NS); w.nl = take(NS); w.nh = take(NS); w.kid = take(4 * NS);
-    w.height = take(NS); w.lay = take(NS); w.sb = take(NS); w.st = take(NS); w.player = take(NP);
-    w.pl = take(MP); w.pb = take(MP); w.pt = take(MP);
-    w.bytes = o;
+    w.wd = take(8 * NS); w.ur = take(8 * NS); w.A = take(8 * NS * LD); w.C = take(8 * NS * LD);
+    w.pcap = take(8 * NP); w.pw = take(8 * NP); w.froot = take(8);
+    w.xy = take(4 * NS); w.vw = take(4 * NS * (L - 1));
+    w.len = take(2 * NS); w.height = take(2 * NS); w.nsink = take(2 * NS); w.sink0 = take(2 * NS);
+    w.kid = take(2 * NS * MAXKIDS); w.entry = take(2 * NS * LD);
+    w.edir = take(NS); w.nkid = take(NS); w.nl = take(NS); w.nh = take(NS); w.choice = take(NS * LD);
+    w.lay = take(NS); w.sb = take(NS); w.st = take(NS); w.player = take(NP);
+    w.bytes = (o + 15) & ~15;
     return w;
 }
 
-constexpr int MAX_LEVELS = 512;
+// Per-warp scratch of the node routine.
+struct WarpLay {
+    int CP, kap, map, bytes;
+};
+
+__host__ __device__ inline WarpLay warp_layout(int L, int LD) {
+    WarpLay w;
+    w.CP = 0;
+    w.kap = w.CP + 8 * MAXKIDS * LD * LD;
+    w.map = w.kap + 8 * (L - 1);
+    w.bytes = (w.map + 2 * 32 + 15) & ~15;
+    return w;
+}
+
+struct NetBuf {
+    double *wd, *ur, *A, *C, *pcap, *pw, *froot;
+    uint32_t *xy;
+    int32_t *vw;
+    uint16_t *len, *height, *nsink, *sink0, *kid, *entry;
+    uint8_t *edir, *nkid, *nl, *nh, *choice, *lay, *sb, *st, *player;
+};
+
+__device__ __forceinline__ NetBuf net_buf(char *b, const NetLay &w) {
+    NetBuf n;
+    n.wd = (double *)(b + w.wd); n.ur = (double *)(b + w.ur); n.A = (double *)(b + w.A); n.C = (double *)(b + w.C);
+    n.pcap = (double *)(b + w.pcap); n.pw = (double *)(b + w.pw); n.froot = (double *)(b + w.froot);
+    n.xy = (uint32_t *)(b + w.xy); n.vw = (int32_t *)(b + w.vw);
+    n.len = (uint16_t *)(b + w.len); n.height = (uint16_t *)(b + w.height); n.nsink = (uint16_t *)(b + w.nsink);
+    n.sink0 = (uint16_t *)(b + w.sink0); n.kid = (uint16_t *)(b + w.kid); n.entry = (uint16_t *)(b + w.entry);
+    n.edir = (uint8_t *)(b + w.edir); n.nkid = (uint8_t *)(b + w.nkid); n.nl = (uint8_t *)(b + w.nl);
+    n.nh = (uint8_t *)(b + w.nh); n.choice = (uint8_t *)(b + w.choice); n.lay = (uint8_t *)(b + w.lay);
+    n.sb = (uint8_t *)(b + w.sb); n.st = (uint8_t *)(b + w.st); n.player = (uint8_t *)(b + w.player);
+    return n;
+}
+
+struct WarpBuf {
+    double *CP, *kap;
+    uint16_t *map;
+};
 
 struct Shared {          // per-CTA static shared memory
     TechTab T;
     uint8_t dir[MAXL], routable[MAXL], lidx[MAXL];
-    uint16_t lvl[MAX_LEVELS + 1];   // big path: level boundaries
-    int nlvl;
+    uint8_t lay_of[2][MAXL];   // layer of slot s in direction d
+    int ndir[2];               // legal layers per direction
+    int64_t item;
+    int lo, hi;                // big path: current level [lo, hi)
 };
 
-// Per-warp task scratch of the pair phase (both paths).
-struct PairScratch {
-    double *Gp, *G, *K;
-    uint32_t *js;
-    uint8_t *l, *b, *t;
+// Context of one net inside the node routines.
+struct NetCtx {
+    NetBuf nb;
+    int L, LD, nn;
 };
 
-__device__ __forceinline__ PairScratch pair_scratch(char *base, const WLay &w) {
-    return PairScratch{reinterpret_cast<double *>(base + w.pGp), reinterpret_cast<double *>(base + w.pG),
-                       reinterpret_cast<double *>(base + w.pK), reinterpret_cast<uint32_t *>(base + w.pjs),
-                       reinterpret_cast<uint8_t *>(base + w.pl), reinterpret_cast<uint8_t *>(base + w.pb),
-                       reinterpret_cast<uint8_t *>(base + w.pt)};
+__device__ __forceinline__ double kappa_w(const DevGrid &G, const Shared &sh, int32_t w, int k) {
+    return G.W_VIA + (G.W_CONG * sh.T.ofw[k]) * marginal(G, w);    // ViaCong, reading R11
 }
 
-// ------------------------------------------------------------- net views --
-// Node-local view of one net: everything the node routine reads or writes,
-// in shared memory (small path) or global memory (big path).
-struct SmallView {
-    const uint32_t *xy_; const int32_t *len_; const uint16_t *sink0_, *nsink_;
-    const uint8_t *edir_, *nkid_, *nl_, *nh_, *kid_;
-    const double *wd_, *ur_, *kap_;
-    double *A_, *B_, *C_;
-    uint16_t *choice_; uint32_t *entry_;
-    const uint8_t *player_; const double *pcap_, *pw_;
-    int Lm1, LD;
-    __device__ int nkid(int i) const { return nkid_[i]; }
-    __device__ int kid(int i, int k) const { return kid_[i * 4 + k]; }
-    __device__ int nl(int i) const { return nl_[i]; }
-    __device__ int nh(int i) const { return nh_[i]; }
-    __device__ int edir(int i) const { return edir_[i]; }
-    __device__ double ur(int i) const { return ur_[i]; }
-    __device__ double wd(int i) const { return wd_[i]; }
-    __device__ int len(int i) const { return len_[i]; }
-    __device__ const double *kap(int i) const { return kap_ + i * Lm1; }
-    __device__ int sbeg(int i) const { return sink0_[i]; }
-    __device__ int scnt(int i) const { return nsink_[i]; }
-    __device__ double pcap(int q) const { return pcap_[q]; }
-    __device__ double pw(int q) const { return pw_[q]; }
-    __device__ int player(int q) const { return player_[q]; }
-};
-
-struct BigView {
-    const DevForest *F; int64_t n0;
-    const double *kap_; double *A_, *B_, *C_;
-    uint16_t *choice_; uint32_t *entry_;
-    int Lm1, LD;
-    __device__ int nkid(int i) const { return F->nkid[n0 + i]; }
-    __device__ int kid(int i, int k) const { return (int)(F->kid[(n0 + i) * 4 + k] - n0); }
-    __device__ int nl(int i) const { return F->nl[n0 + i]; }
-    __device__ int nh(int i) const { return F->nh[n0 + i]; }
-    __device__ int edir(int i) const { return F->edir[n0 + i]; }
-    __device__ double ur(int i) const { return F->ur[n0 + i]; }
-    __device__ double wd(int i) const { return F->wd[n0 + i]; }
-    __device__ int len(int i) const { return F->len[n0 + i]; }
-    __device__ const double *kap(int i) const { return kap_ + (int64_t)i * Lm1; }
-    __device__ int sbeg(int i) const { return F->sink0[n0 + i]; }
-    __device__ int scnt(int i) const { return F->nsink[n0 + i]; }
-    __device__ double pcap(int q) const { return F->p_cap[q]; }
-    __device__ double pw(int q) const { return F->p_w[q]; }
-    __device__ int player(int q) const { return F->p_layer[q]; }
-};
-
-// ------------------------------------------------------------ node routine --
-// Final step for entry layer l of node i once its best span is known: pin terms
-// (Alg. 3 l.4-7), f and dlc (l.405), choice / entry (l.406-408), and for a
-// non-root node the O5 parent-edge terms A, B, capb on layer l (its edge layer).
-template <class VW>
-__device__ __forceinline__ void finish_layer(const VW &v, const Shared &sh, const DevGrid &G, int i, bool root, int l,
-                                             bool have, double Gv, double K, int b, int t, uint32_t js,
-                                             double *froot) {
-    const int slot = root ? 0 : sh.lidx[l];
-    const int64_t at = (int64_t)i * v.LD + slot;
+// -------------------------------------------------------- node finishing --
+// Entry layer l (slot `slot`) of node i once its span is chosen: pin terms
+// (Alg. 3 l.4-7), f and dlc (l.405), choice / entry (l.406-408); for a non-root
+// node also the O5 parent-edge terms A and capb on layer l (its edge layer).
+__device__ __forceinline__ void finish_layer(const NetCtx &c, const Shared &sh, const DevGrid &G, int i, bool root,
+                                             int l, int slot, bool have, double Gv, double K, int b, int t,
+                                             uint32_t ent) {
+    const NetBuf &nb = c.nb;
+    const int at = i * c.LD + slot;
     if (!have) {
-        if (root) *froot = dinf();
-        else v.A_[at] = dinf();
+        if (root) *nb.froot = dinf();
+        else nb.A[at] = dinf();
         return;
     }
     double F0 = 0.0, C0 = 0.0;
-    const int q0 = v.sbeg(i), qn = v.scnt(i);
+    const int q0 = nb.sink0[i], qn = nb.nsink[i];
     for (int q = q0; q < q0 + qn; ++q) {
-        const double cq = v.pcap(q);
-        F0 = F0 + v.pw(q) * (cq * sh.T.VR[v.player(q) * MAXL + l]);
+        const double cq = nb.pcap[q];
+        F0 = F0 + nb.pw[q] * (cq * sh.T.VR[nb.player[q] * MAXL + l]);
         C0 = C0 + cq;
     }
     const double f = F0 + Gv;
     const double dlc = C0 + K;
-    v.choice_[at] = (uint16_t)(b | (t << 8));
-    v.entry_[at] = js;
+    nb.choice[at] = (uint8_t)(b | (t << 4));
+    nb.entry[at] = (uint16_t)ent;
     if (root) {
-        *froot = f;
+        *nb.froot = f;
         return;
     }
-    const int len = v.len(i);
-    const double Sc = v.A_[at];                         // congestion sum gathered up front
-    const double Rw = sh.T.r[l] * (double)len;
-    const double Cw = sh.T.c[l] * (double)len;
-    const double wd = v.wd(i);
-    v.A_[at] = ((f + wd * (Rw * (0.5 * Cw + dlc))) + G.W_CAP * Cw) + (G.W_CONG * sh.T.ofw[l]) * Sc;
-    v.B_[at] = wd * (Cw + dlc);
-    v.C_[at] = Cw + dlc;
+    const double Sc = nb.A[at];                 // congestion sum gathered up front
+    const double len = (double)nb.len[i];
+    const double Rw = sh.T.r[l] * len;
+    const double Cw = sh.T.c[l] * len;
+    const double wd = nb.wd[i];
+    nb.A[at] = ((f + wd * (Rw * (0.5 * Cw + dlc))) + G.W_CAP * Cw) + (G.W_CONG * sh.T.ofw[l]) * Sc;
+    nb.C[at] = Cw + dlc;
 }
 
-// Alg. 3 for node i, all entry layers, executed by one warp (lanes 0..31).
-template <class VW>
-__device__ void node_dp(const VW &v, const Shared &sh, const DevGrid &G, const PairScratch &ps, int i, bool root,
-                        int pdrv, double *froot, int lane) {
-    const int L = G.L;
-    const int nk = v.nkid(i);
-    const int nl = v.nl(i), nh = v.nh(i);
-    const bool has_pins = nl != 255;
-    const int dtype = v.edir(i) <= 1 ? 0 : 1;
-    const double *kap = v.kap(i);
-    // entry layers (R13 root: driver pin layer only; R15 otherwise: legal layers of
-    // the parent edge) and the number of span bottoms b <= b0 (Alg. 3 l.10-12, R14)
-    int cnt = 0;
-    if (lane < L) {
-        const bool ent = root ? (lane == pdrv) : (sh.routable[lane] && sh.dir[lane] == dtype);
-        if (ent) cnt = (has_pins ? min(lane, nl) : lane) + 1;
+// ----------------------------------------------------------------- leaves --
+// Every non-root leaf i < nleaf, all entry layers, threads over (leaf, slot).
+// A leaf has no son terms, G' = V(b, t) >= V(b0, t0) for every admissible span
+// (kappa >= 0, rounded addition is monotone) and the key prefers the smaller
+// span on ties, so the choice is (b0, t0) with G = V(b0, t0).
+__device__ void leaves_dp(const NetCtx &c, const Shared &sh, const DevGrid &G, int nleaf, int tid, int nthr) {
+    const NetBuf &nb = c.nb;
+    const int LD = c.LD, Lm1 = c.L - 1;
+    for (int idx = tid; idx < nleaf * LD; idx += nthr) {
+        const int i = idx / LD, s = idx - i * LD;
+        const int dt = nb.edir[i] <= 1 ? 0 : 1;
+        if (s >= sh.ndir[dt]) continue;
+        const int l = sh.lay_of[dt][s];
+        if (!sh.routable[l]) continue;           // illegal entry layer (R15): A keeps +inf
+        const int nl = nb.nl[i], nh = nb.nh[i];
+        const bool pins = nl != 255;
+        const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+        double V = 0.0;
+        for (int k = b0; k < t0; ++k) V = V + kappa_w(G, sh, nb.vw[i * Lm1 + k], k);
+        finish_layer(c, sh, G, i, false, l, s, true, V, 0.0, b0, t0, 0u);
     }
-    if (nk == 0) {
-        // Leaf: no son terms, G' = V(b, t) >= V(b0, t0) for every admissible span
-        // (kappa >= 0 and rounded addition is monotone), and the key prefers the
-        // smaller span on ties -> the choice is (b0, t0) with G = V(b0, t0).
-        if (cnt > 0) {
-            const int l = lane, b0 = cnt - 1, t0 = has_pins ? max(l, nh) : l;
-            double V = 0.0;
-            for (int k = b0; k < t0; ++k) V = V + kap[k];
-            finish_layer(v, sh, G, i, root, l, true, V, 0.0, b0, t0, 0u, froot);
+}
+
+// -------------------------------------------------------------- node DP --
+// Alg. 3 for node i (internal, or the root), all entry layers, one warp.
+__device__ void node_dp(const NetCtx &c, const WarpBuf &wb, const Shared &sh, const DevGrid &G, int i, bool root,
+                        int pdrv, int lane) {
+    const NetBuf &nb = c.nb;
+    const int L = c.L, LD = c.LD, Lm1 = L - 1;
+    const int nk = nb.nkid[i];
+    const int nl = nb.nl[i], nh = nb.nh[i];
+    const bool pins = nl != 255;
+    const int dt = root ? 0 : (nb.edir[i] <= 1 ? 0 : 1);
+    const int nE = root ? 1 : sh.ndir[dt];
+    const double urn = nb.ur[i];
+    int kid[MAXKIDS], kdt[MAXKIDS];
+#pragma unroll
+    for (int k = 0; k < MAXKIDS; ++k) {
+        kid[k] = k < nk ? nb.kid[i * MAXKIDS + k] : 0;
+        kdt[k] = k < nk ? (nb.edir[kid[k]] <= 1 ? 0 : 1) : 0;
+    }
+    // ViaCong per cut of this node's GCell
+    if (lane < Lm1) wb.kap[lane] = kappa_w(G, sh, nb.vw[i * Lm1 + lane], lane);
+    // candidate table CP[k][e][js] = cost'(l_e; s_k, j) (O5): +inf where the son is infeasible
+    const int per_k = nE * LD;
+    for (int idx = lane; idx < nk * per_k; idx += 32) {
+        const int k = idx / per_k, r = idx - k * per_k;
+        const int e = r / LD, js = r - e * LD;
+        int kk = 0, dk = 0;
+#pragma unroll
+        for (int q = 0; q < MAXKIDS; ++q) if (q == k) { kk = kid[q]; dk = kdt[q]; }
+        if (js >= sh.ndir[dk]) continue;
+        const int l = root ? pdrv : sh.lay_of[dt][e];
+        const int j = sh.lay_of[dk][js];
+        const int at = kk * LD + js;
+        const double A = nb.A[at];
+        double cp = dinf();
+        if (A < dinf()) {
+            const double Bv = nb.wd[kk] * nb.C[at];          // B = wd_s (Cw + D)
+            const double cost = A + Bv * sh.T.VR[l * MAXL + j];
+            cp = cost + Bv * urn;
         }
-        return;
+        wb.CP[(k * LD + e) * LD + js] = cp;
     }
-    int inc = cnt;
+    // span-bottom tasks: entry e has b in [0, b0(e)]; a lane owns up to m of them
+    int cnt = 0;
+    if (lane < nE) {
+        const int l = root ? pdrv : sh.lay_of[dt][lane];
+        if (root || sh.routable[l]) cnt = (pins ? min(l, nl) : l) + 1;   // R13, R15
+    }
+    int m = 1, g = cnt, P = 0;
+    for (;;) {
+        g = (cnt + m - 1) / m;
+        P = g;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(FULL_MASK, P, o);
+        if (P <= 32) break;
+        ++m;
+    }
+    int inc = g;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int x = __shfl_up_sync(FULL_MASK, inc, o);
         if (lane >= o) inc += x;
     }
-    const int P = __shfl_sync(FULL_MASK, inc, 31);
-    for (int b = 0; b < cnt; ++b) {
-        ps.l[inc - cnt + b] = (uint8_t)lane;
-        ps.b[inc - cnt + b] = (uint8_t)b;
-    }
-    int kid[MAXKIDS], kdt[MAXKIDS];
-#pragma unroll
-    for (int k = 0; k < MAXKIDS; ++k) {
-        kid[k] = k < nk ? v.kid(i, k) : 0;
-        kdt[k] = k < nk ? (v.edir(kid[k]) <= 1 ? 0 : 1) : 0;
-    }
-    const double urn = v.ur(i);
+    for (int q = 0; q < g; ++q) wb.map[inc - g + q] = (uint16_t)(lane | (q << 8));
     __syncwarp();
 
-    for (int p = lane; p < P; p += 32) {
-        const int l = ps.l[p], b = ps.b[p];
-        const int t0 = has_pins ? max(l, nh) : l;
-        const double *VRl = &sh.T.VR[l * MAXL];
-        double V = 0.0;
-        for (int k = b; k < t0; ++k) V = V + kap[k];
-        int jb[MAXKIDS];
-        double cpb[MAXKIDS], cbv[MAXKIDS], capv[MAXKIDS];
+    bool have = false;
+    double bGp = 0.0, bV = 0.0;
+    int bt = 0, bb = 0;
+    uint32_t bjs = 0;
+    int e = 0, seg_end = 0;
+    if (lane < P) {
+        const uint16_t mp = wb.map[lane];
+        e = mp & 0xff;
+        const int q = mp >> 8;
+        const int l = root ? pdrv : sh.lay_of[dt][e];
+        const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+        const double *CPe = wb.CP + e * LD;
+        const int bend = min(q * m + m, b0 + 1);
+        for (int b = q * m; b < bend; ++b) {
+            double V = 0.0;
+            for (int k = b; k < t0; ++k) V = V + wb.kap[k];
+            double mv[MAXKIDS];
+            int jb[MAXKIDS];
 #pragma unroll
-        for (int k = 0; k < MAXKIDS; ++k) { jb[k] = -1; cpb[k] = 0.0; cbv[k] = 0.0; capv[k] = 0.0; }
-        // cost(l; s, j) = A + B*VR[l][j]; cost' = cost + B*ur_n; son argmin of cost', ties -> lowest j
-        auto cand = [&](int j) {
-            const bool rj = sh.routable[j];
-            const int dj = sh.dir[j], sj = sh.lidx[j];
+            for (int k = 0; k < MAXKIDS; ++k) { mv[k] = dinf(); jb[k] = -1; }
+            // son argmin of cost' over j in [b, t], ties -> lowest j (ascending j, strict <)
+            auto consider = [&](int j) {
+                if (!sh.routable[j]) return;
+                const int dj = sh.dir[j], sj = sh.lidx[j];
 #pragma unroll
-            for (int k = 0; k < MAXKIDS; ++k) {
-                if (k < nk && rj && dj == kdt[k]) {
-                    const int64_t at = (int64_t)kid[k] * v.LD + sj;
-                    const double A = v.A_[at];
-                    if (A < dinf()) {
-                        const double Bv = v.B_[at];
-                        const double cost = A + Bv * VRl[j];
-                        const double cp = cost + Bv * urn;
-                        if (isfinite(cp) && (jb[k] < 0 || cp < cpb[k])) {
-                            jb[k] = j; cpb[k] = cp; cbv[k] = cost; capv[k] = v.C_[at];
-                        }
+                for (int k = 0; k < MAXKIDS; ++k) {
+                    if (k < nk && kdt[k] == dj) {
+                        const double cp = CPe[k * LD * LD + sj];
+                        if (cp < mv[k]) { mv[k] = cp; jb[k] = j; }
                     }
                 }
-            }
-        };
-        for (int j = b; j <= t0; ++j) cand(j);
-        bool have = false;
-        double bGp = 0.0, bG = 0.0, bK = 0.0;
-        int bt = 255;
-        uint32_t bjs = 0;
-        for (int t = t0; t < L; ++t) {
-            if (t > t0) {
-                V = V + kap[t - 1];
-                cand(t);
-            }
-            bool feas = true;
+            };
+            for (int j = b; j <= t0; ++j) consider(j);
+            for (int t = t0; t < L; ++t) {
+                if (t > t0) {
+                    V = V + wb.kap[t - 1];
+                    consider(t);
+                }
+                bool feas = true;
+                double Gp = V;
+                uint32_t js = 0;
 #pragma unroll
-            for (int k = 0; k < MAXKIDS; ++k) if (k < nk && jb[k] < 0) feas = false;
-            if (!feas) continue;
-            double Gp = V, Gv = V, K = 0.0;
-            uint32_t js = 0;
+                for (int k = 0; k < MAXKIDS; ++k) {
+                    if (k < nk) {
+                        feas = feas && jb[k] >= 0;
+                        Gp = Gp + mv[k];
+                        js |= (uint32_t)(jb[k] & 0xf) << (4 * k);
+                    }
+                }
+                if (!feas) continue;
+                // key (G', t - b, b), lexicographic (reading R21)
+                const bool better = !have || Gp < bGp ||
+                                    (Gp == bGp && ((t - b) < (bt - bb) || ((t - b) == (bt - bb) && b < bb)));
+                if (better) { have = true; bGp = Gp; bt = t; bb = b; bjs = js; bV = V; }
+            }
+        }
+    }
+    // segmented argmin over the lanes of one entry layer (contiguous lanes)
+    seg_end = __shfl_sync(FULL_MASK, inc, e);
+    if (lane >= P) seg_end = 0;
+    uint32_t key = (have ? 1u << 16 : 0u) | ((uint32_t)bt << 8) | ((uint32_t)bb << 4) | 0u;
+    int src = lane;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double oG = __shfl_down_sync(FULL_MASK, bGp, o);
+        const uint32_t ok = __shfl_down_sync(FULL_MASK, key, o);
+        const int os = __shfl_down_sync(FULL_MASK, src, o);
+        if (lane + o < seg_end && (ok >> 16)) {
+            const int ot = (ok >> 8) & 0xff, ob = (ok >> 4) & 0xf;
+            const int mt = (key >> 8) & 0xff, mb = (key >> 4) & 0xf;
+            const bool better = !(key >> 16) || oG < bGp ||
+                                (oG == bGp && ((ot - ob) < (mt - mb) || ((ot - ob) == (mt - mb) && ob < mb)));
+            if (better) { bGp = oG; key = ok; src = os; }
+        }
+    }
+    const uint32_t wjs = __shfl_sync(FULL_MASK, bjs, src);
+    const double wV = __shfl_sync(FULL_MASK, bV, src);
+    if (lane < P && (wb.map[lane] >> 8) == 0) {      // head lane of entry e
+        const int l = root ? pdrv : sh.lay_of[dt][e];
+        const int slot = root ? 0 : e;
+        if (!(key >> 16)) {
+            finish_layer(c, sh, G, i, root, l, slot, false, 0.0, 0.0, 0, 0, 0u);
+        } else {
+            const int t = (key >> 8) & 0xff, b = (key >> 4) & 0xf;
+            double Gv = wV, K = 0.0;
 #pragma unroll
             for (int k = 0; k < MAXKIDS; ++k) {
                 if (k < nk) {
-                    Gp = Gp + cpb[k];
-                    Gv = Gv + cbv[k];
-                    K = K + capv[k];
-                    js |= (uint32_t)jb[k] << (8 * k);
+                    const int j = (wjs >> (4 * k)) & 0xf;
+                    const int at = kid[k] * LD + sh.lidx[j];
+                    const double A = nb.A[at], Cc = nb.C[at];
+                    const double Bv = nb.wd[kid[k]] * Cc;
+                    Gv = Gv + (A + Bv * sh.T.VR[l * MAXL + j]);
+                    K = K + Cc;
                 }
             }
-            if (!have || Gp < bGp) {        // same b: a later t has a larger t-b and loses ties
-                have = true; bGp = Gp; bG = Gv; bK = K; bt = t; bjs = js;
-            }
+            finish_layer(c, sh, G, i, root, l, slot, true, Gv, K, b, t, wjs);
         }
-        ps.Gp[p] = bGp; ps.G[p] = bG; ps.K[p] = bK; ps.js[p] = bjs;
-        ps.t[p] = have ? (uint8_t)bt : (uint8_t)255;
     }
     __syncwarp();
-    if (cnt > 0) {
-        const int l = lane, g0 = inc - cnt;
-        int best = -1;
-        for (int q = g0; q < g0 + cnt; ++q) {
-            if (ps.t[q] == 255) continue;
-            if (best < 0) { best = q; continue; }
-            const double a = ps.Gp[q], c = ps.Gp[best];
-            const int sq = ps.t[q] - ps.b[q], sbst = ps.t[best] - ps.b[best];
-            if (a < c || (a == c && (sq < sbst || (sq == sbst && ps.b[q] < ps.b[best])))) best = q;
-        }
-        if (best >= 0)
-            finish_layer(v, sh, G, i, root, l, true, ps.G[best], ps.K[best], ps.b[best], ps.t[best], ps.js[best],
-                         froot);
-        else
-            finish_layer(v, sh, G, i, root, l, false, 0.0, 0.0, 0, 0, 0u, froot);
-    }
 }
 
-// Congestion sum S of node i's parent run on the layer with slot s of its direction:
-// ((m1 + m2) + ...) + m_len in ascending coordinate, loads issued 4 at a time.
+// ------------------------------------------------------------- gathering --
+// Congestion sum S of a parent run on the layer with slot s of its direction:
+// ((m1 + m2) + ...) + m_len in ascending coordinate (reading R23).
 __device__ __forceinline__ double run_sum(const DevGrid &G, int dtype, int lslot, int x, int y, int edir, int len) {
     const int a = run_lo(edir, x, y, len);
     const int32_t *wp;
@@ -319,10 +366,57 @@ __device__ __forceinline__ double run_sum(const DevGrid &G, int dtype, int lslot
     return Sc;
 }
 
-__device__ __forceinline__ double via_kappa(const DevGrid &G, const Shared &sh, uint32_t xy, int k) {
-    const int x = xy & 0xffff, y = xy >> 16;
-    const int32_t w = __ldcg(G.via + ((int64_t)y * G.X + x) * (G.L - 1) + k);
-    return G.W_VIA + (G.W_CONG * sh.T.ofw[k]) * marginal(G, w);   // ViaCong, reading R11
+// Node records and sinks of net [n0, n0+nn) into nb (threads tid of nthr).
+__device__ __forceinline__ void gather_nodes(const NetBuf &nb, const DevForest &F, int64_t n0, int nn, int tid,
+                                             int nthr) {
+    const int q_base = F.sink0[n0];
+    for (int i = tid; i < nn; i += nthr) {
+        const int64_t n = n0 + i;
+        nb.xy[i] = F.xy[n];
+        nb.len[i] = (uint16_t)F.len[n];
+        nb.edir[i] = F.edir[n];
+        nb.nkid[i] = F.nkid[n];
+        nb.nl[i] = F.nl[n];
+        nb.nh[i] = F.nh[n];
+        nb.height[i] = F.height[n];
+        nb.nsink[i] = F.nsink[n];
+        nb.sink0[i] = (uint16_t)(F.sink0[n] - q_base);
+        nb.wd[i] = F.wd[n];
+        nb.ur[i] = F.ur[n];
+        const int4 k4 = *reinterpret_cast<const int4 *>(F.kid + n * 4);
+        nb.kid[i * 4 + 0] = (uint16_t)(k4.x - n0);
+        nb.kid[i * 4 + 1] = (uint16_t)(k4.y - n0);
+        nb.kid[i * 4 + 2] = (uint16_t)(k4.z - n0);
+        nb.kid[i * 4 + 3] = (uint16_t)(k4.w - n0);
+    }
+    const int64_t nlast = n0 + nn - 1;
+    const int ns = F.sink0[nlast] + F.nsink[nlast] - q_base;
+    for (int q = tid; q < ns; q += nthr) {
+        nb.player[q] = F.p_layer[q_base + q];
+        nb.pcap[q] = F.p_cap[q_base + q];
+        nb.pw[q] = F.p_w[q_base + q];
+    }
+}
+
+// Via-cut words per (node, cut) and S per (non-root node, layer slot).
+__device__ __forceinline__ void gather_state(const NetBuf &nb, const DevGrid &G, const Shared &sh, int nn, int LD,
+                                             int tid, int nthr) {
+    const int Lm1 = G.L - 1;
+    for (int idx = tid; idx < nn * Lm1; idx += nthr) {
+        const int i = idx / Lm1, k = idx - i * Lm1;
+        const uint32_t xy = nb.xy[i];
+        nb.vw[idx] = __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k);
+    }
+    for (int idx = tid; idx < nn * LD; idx += nthr) {
+        const int i = idx / LD, s = idx - i * LD;
+        const int ed = nb.edir[i];
+        if (ed == NO_DIR) continue;
+        const int dt = ed <= 1 ? 0 : 1;
+        if (s >= sh.ndir[dt]) continue;
+        if (!sh.routable[sh.lay_of[dt][s]]) { nb.A[idx] = dinf(); continue; }
+        const uint32_t xy = nb.xy[i];
+        nb.A[idx] = run_sum(G, dt, s, xy & 0xffff, xy >> 16, ed, nb.len[i]);
+    }
 }
 
 // Fused K8 for node n: +1 per unit edge of its parent run on its layer, +1 per via cut.
@@ -342,207 +436,226 @@ __device__ __forceinline__ void commit_node(const DevGrid &G, uint32_t xy, int e
     for (int k = b; k < t; ++k) atomicAdd(vp + k, 2);
 }
 
+// Backtrack of node i (Alg. 4): its span from choice[i][l_i], its sons' layers from entry.
+__device__ __forceinline__ void backtrack_node(const NetCtx &c, const Shared &sh, int i) {
+    const NetBuf &nb = c.nb;
+    const int l = nb.lay[i];
+    const int slot = (i == c.nn - 1) ? 0 : sh.lidx[l];
+    const uint8_t ch = nb.choice[i * c.LD + slot];
+    nb.sb[i] = ch & 0xf;
+    nb.st[i] = ch >> 4;
+    const uint32_t js = nb.entry[i * c.LD + slot];
+    const int nk = nb.nkid[i];
+    for (int k = 0; k < nk; ++k) nb.lay[nb.kid[i * 4 + k]] = (uint8_t)((js >> (4 * k)) & 0xf);
+}
+
+// CTA barrier that is correct when a warp arrives diverged (e.g. one lane
+// spinning on a dependency counter while the others wait): the NON-aligned
+// barrier.sync counts threads, whereas __syncthreads (bar.sync, .aligned)
+// requires every warp to arrive converged.
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ------------------------------------------------------------------ kernel --
-__global__ void __launch_bounds__(ASSIGN_WARPS * 32) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
+__global__ void __launch_bounds__(ASSIGN_WARPS * 32, 5) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
     extern __shared__ __align__(16) char dyn[];
     stage_tab(sh.T, G.tab);
     if (threadIdx.x < MAXL) {
-        sh.dir[threadIdx.x] = G.dir[threadIdx.x];
-        sh.routable[threadIdx.x] = G.routable[threadIdx.x];
-        sh.lidx[threadIdx.x] = (uint8_t)G.lidx[threadIdx.x];
+        const int l = threadIdx.x;
+        sh.dir[l] = G.dir[l];
+        sh.routable[l] = G.routable[l];
+        sh.lidx[l] = (uint8_t)G.lidx[l];
+        if (l < G.L) sh.lay_of[G.dir[l]][G.lidx[l]] = (uint8_t)l;
     }
-    __syncthreads();
-    const int L = G.L, Lm1 = L - 1, LD = a.LD;
+    if (threadIdx.x == 0) { sh.ndir[0] = G.LH; sh.ndir[1] = G.LV; }
+    const int L = G.L, LD = a.LD;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const WLay wl = wlayout(L, LD, a.MP);
-    char *wbase = dyn + warp * wl.bytes;
-    const PairScratch ps = pair_scratch(wbase, wl);
+    const WarpLay wlay = warp_layout(L, LD);
+    const NetLay slay = net_layout(a.NS, a.NP, L, LD);
+    char *wscr = dyn + warp * wlay.bytes;
+    char *nets = dyn + ASSIGN_WARPS * wlay.bytes;
+    const WarpBuf wb{reinterpret_cast<double *>(wscr + wlay.CP), reinterpret_cast<double *>(wscr + wlay.kap),
+                     reinterpret_cast<uint16_t *>(wscr + wlay.map)};
+    const bool flow = a.wait != nullptr;
 
-    if ((int64_t)blockIdx.x < a.nbig) {
-        // =========================== big path: one CTA per net ===========================
-        const int64_t net = a.net_beg + blockIdx.x;
+    for (;;) {
+        cta_sync();
+        if (threadIdx.x == 0) {
+            const unsigned long long t = atomicAdd(a.ticket, 1ull);
+            sh.item = (int64_t)t < a.item_end - a.item_beg ? a.item_beg + (int64_t)t : -1;
+        }
+        cta_sync();
+        const int64_t item = sh.item;
+        if (item < 0) return;
+        const uint64_t it = a.items[item];
+        const int64_t net_first = (int64_t)(it & 0xffffffffull);
+        const int cnt = (int)((it >> 32) & 0xff);
+        const bool big = (it >> 40) & 1;
+
+        if (big) {
+            // ======================= big net: the whole CTA =======================
+            const int64_t net = net_first;
+            const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
+            const int nn = (int)(n1 - n0);
+            const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - F.sink0[n0];
+            const NetLay blay = net_layout(nn, ns, L, LD);
+            char *base = blay.bytes <= a.big_smem ? nets : a.gscratch + (int64_t)blockIdx.x * a.gslot_bytes;
+            const NetCtx c{net_buf(base, blay), L, LD, nn};
+            const int pdrv = F.net_pdrv[net];
+            if (flow) {
+                if (threadIdx.x == 0) while (ld_acquire(a.wait + net) > 0) __nanosleep(100);
+                cta_sync();
+                __threadfence();
+            }
+            gather_nodes(c.nb, F, n0, nn, threadIdx.x, blockDim.x);
+            cta_sync();
+            gather_state(c.nb, G, sh, nn, LD, threadIdx.x, blockDim.x);
+            if (threadIdx.x == 0) {
+                int hi = 0;
+                while (hi < nn - 1 && c.nb.height[hi] == 0) ++hi;
+                sh.lo = 0;
+                sh.hi = hi;
+            }
+            cta_sync();
+            leaves_dp(c, sh, G, sh.hi, threadIdx.x, blockDim.x);
+            for (;;) {
+                cta_sync();
+                if (threadIdx.x == 0) {
+                    int lo = sh.hi, hi = lo;
+                    if (lo < nn) {
+                        const int h = c.nb.height[lo];
+                        while (hi < nn && c.nb.height[hi] == h) ++hi;
+                    }
+                    sh.lo = lo;
+                    sh.hi = hi;
+                }
+                cta_sync();
+                const int lo = sh.lo, hi = sh.hi;
+                if (lo >= nn) break;
+                for (int i = lo + warp; i < hi; i += ASSIGN_WARPS) node_dp(c, wb, sh, G, i, i == nn - 1, pdrv, lane);
+            }
+            // Alg. 4, level-parallel from the root (root entry = driver pin layer, R13)
+            if (threadIdx.x == 0) {
+                c.nb.lay[nn - 1] = (uint8_t)pdrv;
+                S.froot[net] = *c.nb.froot;
+                sh.lo = nn;
+            }
+            for (;;) {
+                cta_sync();
+                if (threadIdx.x == 0) {
+                    const int hi = sh.lo;
+                    int lo = hi;
+                    if (hi > 0) {
+                        const int h = c.nb.height[hi - 1];
+                        while (lo > 0 && c.nb.height[lo - 1] == h) --lo;
+                    }
+                    sh.hi = hi;
+                    sh.lo = lo;
+                }
+                cta_sync();
+                const int lo = sh.lo, hi = sh.hi;
+                if (hi <= 0) break;
+                for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) backtrack_node(c, sh, i);
+            }
+            cta_sync();
+            for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+                S.lay[n0 + i] = c.nb.lay[i];
+                S.sb[n0 + i] = c.nb.sb[i];
+                S.st[n0 + i] = c.nb.st[i];
+                if (a.commit) commit_node(G, c.nb.xy[i], c.nb.edir[i], c.nb.len[i], c.nb.lay[i], c.nb.sb[i], c.nb.st[i]);
+            }
+            if (flow) {
+                __threadfence();
+                cta_sync();
+                for (int64_t e = a.succ_off[net] + threadIdx.x; e < a.succ_off[net + 1]; e += blockDim.x)
+                    atomicSub(a.wait + a.succ[e], 1);
+            }
+            continue;
+        }
+
+        // ========================= small nets: one warp each =========================
+        if (warp >= cnt) continue;
+        const int64_t net = net_first + warp;
         const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
         const int nn = (int)(n1 - n0);
+        const NetCtx c{net_buf(nets + warp * slay.bytes, slay), L, LD, nn};
         const int pdrv = F.net_pdrv[net];
-        const int64_t sbase = n0 - a.node_base;
-        BigView v{&F, n0, S.bkap + sbase * Lm1, S.bA + sbase * LD, S.bB + sbase * LD, S.bC + sbase * LD,
-                  S.bchoice + sbase * LD, S.bentry + sbase * LD, Lm1, LD};
-        // gather kappa and S for all nodes (all loads of the net in flight)
-        for (int idx = threadIdx.x; idx < nn * Lm1; idx += blockDim.x) {
-            const int i = idx / Lm1, k = idx - i * Lm1;
-            S.bkap[(sbase + i) * Lm1 + k] = via_kappa(G, sh, F.xy[n0 + i], k);
+        if (flow) {
+            while (ld_acquire(a.wait + net) > 0) __nanosleep(64);
+            __syncwarp();
         }
-        for (int idx = threadIdx.x; idx < nn * LD; idx += blockDim.x) {
-            const int i = idx / LD, s = idx - i * LD;
-            const int ed = F.edir[n0 + i];
-            if (ed == NO_DIR) continue;
-            const int dt = ed <= 1 ? 0 : 1;
-            if (s >= (dt == 0 ? G.LH : G.LV)) continue;
-            const uint32_t xy = F.xy[n0 + i];
-            S.bA[(sbase + i) * LD + s] = run_sum(G, dt, s, xy & 0xffff, xy >> 16, ed, F.len[n0 + i]);
-        }
-        if (threadIdx.x == 0) {           // level boundaries (nodes are height-sorted)
-            int nlv = 0, prev = -1;
-            for (int i = 0; i < nn && nlv < MAX_LEVELS; ++i) {
-                const int h = F.height[n0 + i];
-                if (h != prev) { sh.lvl[nlv++] = (uint16_t)i; prev = h; }
-            }
-            sh.lvl[nlv] = (uint16_t)nn;
-            sh.nlvl = nlv;
-        }
-        __syncthreads();
-        const int nlv = sh.nlvl;
-        for (int lv = 0; lv < nlv; ++lv) {
-            for (int i = sh.lvl[lv] + warp; i < sh.lvl[lv + 1]; i += ASSIGN_WARPS)
-                node_dp(v, sh, G, ps, i, i == nn - 1, pdrv, S.froot + net, lane);
-            __syncthreads();
-        }
-        // Alg. 4, level-parallel from the root
-        if (threadIdx.x == 0) S.lay[n1 - 1] = (uint8_t)pdrv;
-        __syncthreads();
-        for (int lv = nlv - 1; lv >= 0; --lv) {
-            for (int i = sh.lvl[lv] + threadIdx.x; i < sh.lvl[lv + 1]; i += blockDim.x) {
-                const int64_t n = n0 + i;
-                const int l = S.lay[n];
-                const int slot = (i == nn - 1) ? 0 : sh.lidx[l];
-                const uint16_t ch = v.choice_[(int64_t)i * LD + slot];
-                const int b = ch & 0xff, t = ch >> 8;
-                S.sb[n] = (uint8_t)b;
-                S.st[n] = (uint8_t)t;
-                const uint32_t js = v.entry_[(int64_t)i * LD + slot];
-                const int nk = F.nkid[n];
-                for (int k = 0; k < nk; ++k) S.lay[F.kid[n * 4 + k]] = (uint8_t)((js >> (8 * k)) & 0xff);
-                if (a.commit) commit_node(G, F.xy[n], F.edir[n], F.len[n], l, b, t);
-            }
-            __syncthreads();
-        }
-        return;
-    }
-
-    // ============================= small path: one warp per net =============================
-    const int64_t net = a.net_beg + a.nbig + ((int64_t)blockIdx.x - a.nbig) * ASSIGN_WARPS + warp;
-    if (net >= a.net_end) return;
-    const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
-    const int nn = (int)(n1 - n0);
-    const int pdrv = F.net_pdrv[net];
-    uint32_t *xy = reinterpret_cast<uint32_t *>(wbase + wl.xy);
-    int32_t *len = reinterpret_cast<int32_t *>(wbase + wl.len);
-    uint16_t *nsink = reinterpret_cast<uint16_t *>(wbase + wl.nsink), *sink0 = reinterpret_cast<uint16_t *>(wbase + wl.sink0);
-    uint8_t *edir = reinterpret_cast<uint8_t *>(wbase + wl.edir), *nkid = reinterpret_cast<uint8_t *>(wbase + wl.nkid);
-    uint8_t *nl = reinterpret_cast<uint8_t *>(wbase + wl.nl), *nh = reinterpret_cast<uint8_t *>(wbase + wl.nh);
-    uint8_t *kid = reinterpret_cast<uint8_t *>(wbase + wl.kid), *height = reinterpret_cast<uint8_t *>(wbase + wl.height);
-    uint8_t *lay = reinterpret_cast<uint8_t *>(wbase + wl.lay), *sb = reinterpret_cast<uint8_t *>(wbase + wl.sb);
-    uint8_t *st = reinterpret_cast<uint8_t *>(wbase + wl.st), *player = reinterpret_cast<uint8_t *>(wbase + wl.player);
-    double *wd = reinterpret_cast<double *>(wbase + wl.wd), *ur = reinterpret_cast<double *>(wbase + wl.ur);
-    double *kap = reinterpret_cast<double *>(wbase + wl.kap);
-    double *A = reinterpret_cast<double *>(wbase + wl.A), *B = reinterpret_cast<double *>(wbase + wl.B);
-    double *C = reinterpret_cast<double *>(wbase + wl.C);
-    double *pcap = reinterpret_cast<double *>(wbase + wl.pcap), *pw = reinterpret_cast<double *>(wbase + wl.pw);
-    uint16_t *choice = reinterpret_cast<uint16_t *>(wbase + wl.choice);
-    uint32_t *entry = reinterpret_cast<uint32_t *>(wbase + wl.entry);
-
-    // ---- gather 1: node records and sinks
-    const int q_base = F.sink0[n0];
-    for (int i = lane; i < nn; i += 32) {
-        const int64_t n = n0 + i;
-        xy[i] = F.xy[n];
-        len[i] = F.len[n];
-        edir[i] = F.edir[n];
-        nkid[i] = F.nkid[n];
-        nl[i] = F.nl[n];
-        nh[i] = F.nh[n];
-        height[i] = F.height[n];
-        nsink[i] = F.nsink[n];
-        sink0[i] = (uint16_t)(F.sink0[n] - q_base);
-        wd[i] = F.wd[n];
-        ur[i] = F.ur[n];
-        const int4 k4 = *reinterpret_cast<const int4 *>(F.kid + n * 4);
-        kid[i * 4 + 0] = (uint8_t)(k4.x - n0);
-        kid[i * 4 + 1] = (uint8_t)(k4.y - n0);
-        kid[i * 4 + 2] = (uint8_t)(k4.z - n0);
-        kid[i * 4 + 3] = (uint8_t)(k4.w - n0);
-    }
-    const int ns_net = F.sink0[n1 - 1] + F.nsink[n1 - 1] - q_base;
-    for (int q = lane; q < ns_net; q += 32) {
-        player[q] = F.p_layer[q_base + q];
-        pcap[q] = F.p_cap[q_base + q];
-        pw[q] = F.p_w[q_base + q];
-    }
-    __syncwarp();
-    // ---- gather 2: kappa per (node, cut) and S per (non-root node, layer slot)
-    for (int idx = lane; idx < nn * Lm1; idx += 32) {
-        const int i = idx / Lm1, k = idx - i * Lm1;
-        kap[idx] = via_kappa(G, sh, xy[i], k);
-    }
-    for (int idx = lane; idx < nn * LD; idx += 32) {
-        const int i = idx / LD, s = idx - i * LD;
-        const int ed = edir[i];
-        if (ed == NO_DIR) continue;
-        const int dt = ed <= 1 ? 0 : 1;
-        if (s >= (dt == 0 ? G.LH : G.LV)) continue;
-        A[idx] = run_sum(G, dt, s, xy[i] & 0xffff, xy[i] >> 16, ed, len[i]);
-    }
-    __syncwarp();
-    // ---- Alg. 3, nodes in height order (children before parents)
-    SmallView v{xy, len, sink0, nsink, edir, nkid, nl, nh, kid, wd, ur, kap, A, B, C, choice, entry,
-                player, pcap, pw, Lm1, LD};
-    double froot = 0.0;
-    for (int i = 0; i < nn; ++i) {
-        node_dp(v, sh, G, ps, i, i == nn - 1, pdrv, &froot, lane);
+        gather_nodes(c.nb, F, n0, nn, lane, 32);
         __syncwarp();
-    }
-    // root entry layer has a single lane; broadcast its f
-    {
-        const int src = pdrv;   // lane that finished the root's only entry layer
-        froot = __shfl_sync(FULL_MASK, froot, src);
-        if (lane == 0) S.froot[net] = froot;
-    }
-    // ---- Alg. 4, level-parallel from the root (root entry = driver pin layer, R13)
-    if (lane == 0) lay[nn - 1] = (uint8_t)pdrv;
-    __syncwarp();
-    int hi = nn - 1;
-    while (hi >= 0) {
-        const int h = height[hi];
-        int lo = hi;
-        while (lo > 0 && height[lo - 1] == h) --lo;
-        for (int i = lo + lane; i <= hi; i += 32) {
-            const int l = lay[i];
-            const int slot = (i == nn - 1) ? 0 : sh.lidx[l];
-            const uint16_t ch = choice[i * LD + slot];
-            sb[i] = (uint8_t)(ch & 0xff);
-            st[i] = (uint8_t)(ch >> 8);
-            const uint32_t js = entry[i * LD + slot];
-            for (int k = 0; k < nkid[i]; ++k) lay[kid[i * 4 + k]] = (uint8_t)((js >> (8 * k)) & 0xff);
+        gather_state(c.nb, G, sh, nn, LD, lane, 32);
+        __syncwarp();
+        int nleaf = 0;
+        while (nleaf < nn - 1 && c.nb.height[nleaf] == 0) ++nleaf;
+        leaves_dp(c, sh, G, nleaf, lane, 32);
+        __syncwarp();
+        for (int i = nleaf; i < nn; ++i) node_dp(c, wb, sh, G, i, i == nn - 1, pdrv, lane);
+        if (lane == 0) {
+            S.froot[net] = *c.nb.froot;
+            c.nb.lay[nn - 1] = (uint8_t)pdrv;
         }
         __syncwarp();
-        hi = lo - 1;
-    }
-    for (int i = lane; i < nn; i += 32) {
-        S.lay[n0 + i] = lay[i];
-        S.sb[n0 + i] = sb[i];
-        S.st[n0 + i] = st[i];
-        if (a.commit) commit_node(G, xy[i], edir[i], len[i], lay[i], sb[i], st[i]);
+        int hi = nn;
+        while (hi > 0) {
+            const int h = c.nb.height[hi - 1];
+            int lo = hi - 1;
+            while (lo > 0 && c.nb.height[lo - 1] == h) --lo;
+            for (int i = lo + lane; i < hi; i += 32) backtrack_node(c, sh, i);
+            __syncwarp();
+            hi = lo;
+        }
+        for (int i = lane; i < nn; i += 32) {
+            S.lay[n0 + i] = c.nb.lay[i];
+            S.sb[n0 + i] = c.nb.sb[i];
+            S.st[n0 + i] = c.nb.st[i];
+            if (a.commit) commit_node(G, c.nb.xy[i], c.nb.edir[i], c.nb.len[i], c.nb.lay[i], c.nb.sb[i], c.nb.st[i]);
+        }
+        if (flow) {
+            __threadfence();
+            __syncwarp();
+            for (int64_t e = a.succ_off[net] + lane; e < a.succ_off[net + 1]; e += 32) atomicSub(a.wait + a.succ[e], 1);
+        }
     }
 }
 
 }  // namespace
 
-size_t assign_smem_bytes(int L, int LD, int MP) { return (size_t)ASSIGN_WARPS * wlayout(L, LD, MP).bytes; }
+size_t assign_smem_bytes(int L, int LD, int NS, int NP) {
+    return (size_t)ASSIGN_WARPS * (warp_layout(L, LD).bytes + net_layout(NS, NP, L, LD).bytes);
+}
 
-cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a,
+size_t assign_net_bytes(int nodes, int sinks, int L, int LD) { return (size_t)net_layout(nodes, sinks, L, LD).bytes; }
+
+cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm) {
+    const size_t smem = assign_smem_bytes(L, LD, NS, NP);
+    cudaError_t e = cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_assign, ASSIGN_WARPS * 32, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    return cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
+}
+
+cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           cudaStream_t s) {
-    const int64_t n = a.net_end - a.net_beg;
-    if (n <= 0) return cudaSuccess;
-    const size_t smem = assign_smem_bytes(G.L, a.LD, a.MP);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
+    if (a.item_end <= a.item_beg || grid <= 0) return cudaSuccess;
+    const size_t smem = assign_smem_bytes(G.L, a.LD, a.NS, a.NP);
+    if (a.wait) {
+        // dataflow mode: every CTA must be co-resident (nets wait on each other)
+        void *args[] = {(void *)&G, (void *)&F, (void *)&S, (void *)&a};
+        return cudaLaunchCooperativeKernel((const void *)k_assign, dim3(grid), dim3(ASSIGN_WARPS * 32), args, smem, s);
     }
-    const int64_t nsmall = n - a.nbig;
-    const int64_t grid = a.nbig + (nsmall + ASSIGN_WARPS - 1) / ASSIGN_WARPS;
     k_assign<<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
     return cudaGetLastError();
 }

@@ -71,6 +71,32 @@ __global__ void k_widen(const int32_t *__restrict__ a, int64_t *__restrict__ b, 
     if (i < n) b[i] = a[i];
 }
 
+// Forest-order DAG: position p holds the net of rank r = rank_of_pos[p].
+__global__ void k_dag_deg(const int64_t *__restrict__ off_r, const int32_t *__restrict__ indeg_r,
+                          const int64_t *__restrict__ rank_of_pos, int64_t n, int64_t *__restrict__ deg_p,
+                          int32_t *__restrict__ indeg_p) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t r = rank_of_pos[p];
+    deg_p[p] = off_r[r + 1] - off_r[r];
+    indeg_p[p] = indeg_r[r];
+}
+
+__global__ void k_dag_fill(const int64_t *__restrict__ off_r, const int32_t *__restrict__ succ_r,
+                           const int64_t *__restrict__ rank_of_pos, const int32_t *__restrict__ pos_of_rank,
+                           const int64_t *__restrict__ off_p, int64_t n, int32_t *__restrict__ succ_p) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t r = rank_of_pos[p];
+    int64_t o = off_p[p];
+    for (int64_t e = off_r[r]; e < off_r[r + 1]; ++e) succ_p[o++] = pos_of_rank[succ_r[e]];
+}
+
+__global__ void k_inverse(const int64_t *__restrict__ rank_of_pos, int64_t n, int32_t *__restrict__ pos_of_rank) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < n) pos_of_rank[rank_of_pos[p]] = (int32_t)p;
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 struct DevBuf {
@@ -84,9 +110,17 @@ struct DevBuf {
 
 }  // namespace
 
+void DagDev::release() {
+    if (off) cudaFree(off);
+    if (succ) cudaFree(succ);
+    if (indeg) cudaFree(indeg);
+    off = nullptr; succ = nullptr; indeg = nullptr;
+    n = n_edges = 0;
+}
+
 cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int elem_bits, int64_t n_nets,
                                  std::vector<int32_t> &batch_of_rank, int32_t &n_batches, cudaStream_t s,
-                                 int64_t *launches) {
+                                 int64_t *launches, DagDev *dag) {
     batch_of_rank.assign(n_nets, 0);
     n_batches = n_nets > 0 ? 1 : 0;
     if (n_nets == 0) return cudaSuccess;
@@ -131,6 +165,17 @@ cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int ele
                                                     cursor.as<int32_t>(), succ.as<int32_t>());
     BCK(cudaGetLastError());
     *launches += 3;
+    if (dag) {   // keep the DAG (Kahn below consumes indeg)
+        dag->release();
+        dag->n = n_nets;
+        dag->n_edges = n_edges;
+        BCK(cudaMalloc(&dag->off, 8 * (n_nets + 1)));
+        BCK(cudaMalloc(&dag->succ, 4 * std::max<int64_t>(n_edges, 1)));
+        BCK(cudaMalloc(&dag->indeg, 4 * n_nets));
+        BCK(cudaMemcpyAsync(dag->off, off.p, 8 * (n_nets + 1), cudaMemcpyDeviceToDevice, s));
+        BCK(cudaMemcpyAsync(dag->succ, succ.p, 4 * std::max<int64_t>(n_edges, 1), cudaMemcpyDeviceToDevice, s));
+        BCK(cudaMemcpyAsync(dag->indeg, indeg.p, 4 * n_nets, cudaMemcpyDeviceToDevice, s));
+    }
     // Kahn frontiers
     BCK(batch.alloc(4 * n_nets));
     BCK(fa.alloc(4 * n_nets));
@@ -165,6 +210,39 @@ cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int ele
     n_batches = round;
     BCK(cudaMemcpyAsync(batch_of_rank.data(), batch.p, 4 * n_nets, cudaMemcpyDeviceToHost, s));
     BCK(cudaStreamSynchronize(s));
+    return cudaSuccess;
+}
+
+cudaError_t gpu_dag_to_positions(DagDev &dag, const int64_t *h_rank_of_pos, int64_t **off_p, int32_t **succ_p,
+                                 int32_t **indeg_p, cudaStream_t s, int64_t *launches) {
+    const int64_t n = dag.n;
+    *off_p = nullptr; *succ_p = nullptr; *indeg_p = nullptr;
+    DevBuf rop, por, deg, tmp;
+    BCK(rop.alloc(8 * std::max<int64_t>(n, 1)));
+    BCK(por.alloc(4 * std::max<int64_t>(n, 1)));
+    BCK(deg.alloc(8 * (n + 1)));
+    BCK(cudaMalloc(off_p, 8 * (n + 1)));
+    BCK(cudaMalloc(succ_p, 4 * std::max<int64_t>(dag.n_edges, 1)));
+    BCK(cudaMalloc(indeg_p, 4 * std::max<int64_t>(n, 1)));
+    if (n == 0) {
+        BCK(cudaMemsetAsync(*off_p, 0, 8, s));
+        return cudaStreamSynchronize(s);
+    }
+    BCK(cudaMemcpyAsync(rop.p, h_rank_of_pos, 8 * n, cudaMemcpyHostToDevice, s));
+    BCK(cudaMemsetAsync(deg.p, 0, 8 * (n + 1), s));
+    k_inverse<<<nblk(n, 256), 256, 0, s>>>(rop.as<int64_t>(), n, por.as<int32_t>());
+    k_dag_deg<<<nblk(n, 256), 256, 0, s>>>(dag.off, dag.indeg, rop.as<int64_t>(), n, deg.as<int64_t>(), *indeg_p);
+    BCK(cudaGetLastError());
+    size_t scan_bytes = 0;
+    BCK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, deg.as<int64_t>(), *off_p, n + 1, s));
+    BCK(tmp.alloc(scan_bytes));
+    BCK(cub::DeviceScan::ExclusiveSum(tmp.p, scan_bytes, deg.as<int64_t>(), *off_p, n + 1, s));
+    k_dag_fill<<<nblk(n, 256), 256, 0, s>>>(dag.off, dag.succ, rop.as<int64_t>(), por.as<int32_t>(), *off_p, n,
+                                             *succ_p);
+    BCK(cudaGetLastError());
+    *launches += 4;
+    BCK(cudaStreamSynchronize(s));
+    dag.release();
     return cudaSuccess;
 }
 

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -81,9 +82,23 @@ struct la_ctx {
     std::vector<uint8_t> h_edir;
     std::vector<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
-    std::vector<int64_t> batch_nbig;          // per batch: leading nets that take the CTA-per-net path
-    int32_t LD = 0, MP = 0;                   // layer slots per direction; max pair tasks per node
+    std::vector<int64_t> batch_item0;         // [n_batches+1] first work item of each batch
+    int64_t n_items = 0;
+    int32_t LD = 0;                           // layer slots per direction
+    int32_t NS = NS_DEFAULT, NP = NP_DEFAULT; // small-path capacities of k_assign
+    int32_t grid = 0;                         // resident k_assign CTAs (persistent grid)
+    int64_t big_smem = 0;                     // shared-memory bytes a big net may use
+    int32_t schedule = LA_SCHED_DATAFLOW;
+    bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
+    std::vector<uint64_t> h_items;
     bool fuse_commit = true;
+    // work items and the dataflow DAG (device)
+    uint64_t *d_items = nullptr;
+    unsigned long long *d_ticket = nullptr;   // [n_batches + 1]: [0] dataflow, [1 + b] batch b
+    int64_t *d_succ_off = nullptr;
+    int32_t *d_succ = nullptr, *d_indeg = nullptr, *d_wait = nullptr;
+    char *d_gscratch = nullptr;
+    int64_t gslot_bytes = 0;
     std::vector<int32_t> batch_of_net;        // input order
     DevForest F{};
     DevScratch S{};
@@ -107,7 +122,8 @@ struct la_ctx {
 
     ~la_ctx() {
         for (void *p : dev_allocs) cudaFree(p);
-        void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab};
+        void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab,
+                      d_items, d_ticket, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
         for (void *p : gp) if (p) cudaFree(p);
         if (comm) ncclCommDestroy(comm);
         for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -721,7 +737,12 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         return ch.sink_off[i + 1] - ch.sink_off[i];
     };
     // nets whose whole DP state fits a warp's shared memory take the warp path
-    auto is_big = [&](int64_t net) { return nnodes_of(net) > NS_MAX || nsinks_of(net) > NP_MAX; };
+    if (const char *e = getenv("GAPLA_NS")) ctx->NS = std::max(1, std::min(1024, atoi(e)));   // tuning knobs
+    if (const char *e = getenv("GAPLA_NP")) ctx->NP = std::max(1, std::min(4096, atoi(e)));
+    auto is_big = [&](int64_t net) { return nnodes_of(net) > ctx->NS || nsinks_of(net) > ctx->NP; };
+    for (int64_t net = 0; net < N; net++)
+        if (nnodes_of(net) >= 65535 || nsinks_of(net) >= 65535)
+            return set_err(LA_EINVAL, "net " + std::to_string(net) + ": more than 65534 LA-tree nodes or sinks");
 
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
@@ -766,10 +787,11 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     // ---- GPU conflict-free batching (K1/K2)
     std::vector<int32_t> batch_of_rank;
     int32_t nb = 0;
+    DagDev dag;
     {
         cudaError_t e = gpu_conflict_batches(keys.data(), n_fp, elem_bits, N, batch_of_rank, nb, ctx->stream,
-                                             &ctx->stats.launches);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "conflict-free batching");
+                                             &ctx->stats.launches, &dag);
+        if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "conflict-free batching"); }
     }
     std::vector<uint64_t>().swap(keys);
     auto t2 = std::chrono::steady_clock::now();
@@ -797,14 +819,39 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                                  return nnodes_of(a) > nnodes_of(c);
                              });
     }
-    // per batch: number of big nets (they lead the batch) and their node count
-    ctx->batch_nbig.assign(nb, 0);
-    int64_t max_big_nodes = 0;
+    // work items: per batch, each big net alone, then runs of up to
+    // ASSIGN_WARPS small nets; the largest big net sizes the global big-net slot
+    std::vector<uint64_t> items;
+    ctx->batch_item0.assign(1, 0);
+    int64_t max_big_nodes = 0, max_big_sinks = 0;
     for (int32_t b = 0; b < nb; b++) {
-        int64_t k = ctx->batch_net0[b], nodes = 0;
-        while (k < ctx->batch_net0[b + 1] && is_big(pos_net[k])) { nodes += nnodes_of(pos_net[k]); k++; }
-        ctx->batch_nbig[b] = k - ctx->batch_net0[b];
-        max_big_nodes = std::max(max_big_nodes, nodes);
+        int64_t k = ctx->batch_net0[b];
+        const int64_t kend = ctx->batch_net0[b + 1];
+        while (k < kend) {
+            if (is_big(pos_net[k])) {
+                max_big_nodes = std::max(max_big_nodes, nnodes_of(pos_net[k]));
+                max_big_sinks = std::max(max_big_sinks, nsinks_of(pos_net[k]));
+                items.push_back((uint64_t)k | (1ull << 32) | (1ull << 40));
+                k++;
+                continue;
+            }
+            int64_t c = 0;
+            while (k + c < kend && c < ASSIGN_WARPS && !is_big(pos_net[k + c])) c++;
+            items.push_back((uint64_t)k | ((uint64_t)c << 32));
+            k += c;
+        }
+        ctx->batch_item0.push_back((int64_t)items.size());
+    }
+    ctx->n_items = (int64_t)items.size();
+    // dataflow DAG in forest order
+    {
+        std::vector<int64_t> rank_of_net(N), rank_of_pos(N);
+        for (int64_t r = 0; r < N; r++) rank_of_net[by_rank[r]] = r;
+        for (int64_t p = 0; p < N; p++) rank_of_pos[p] = rank_of_net[pos_net[p]];
+        cudaError_t e = gpu_dag_to_positions(dag, rank_of_pos.data(), &ctx->d_succ_off, &ctx->d_succ, &ctx->d_indeg,
+                                             ctx->stream, &ctx->stats.launches);
+        if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "dependency DAG"); }
+        ctx->stats.h2d_bytes += 8 * N;
     }
     // offsets in final order
     std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
@@ -875,11 +922,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     chunks.shrink_to_fit();
 
     ctx->LD = std::max(ctx->LH, ctx->LV);
-    {
-        int mp[2] = {0, 0};
-        for (int l = 0; l < ctx->L; l++) mp[ctx->dir[l]] += l + 1;
-        ctx->MP = std::max(ctx->L, std::max(mp[0], mp[1]));
-    }
 
     // ---- upload forest, allocate scratch
     DevForest &F = ctx->F;
@@ -900,15 +942,36 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     F.sink0 = d_sink0; F.nsink = d_nsink; F.wd = d_wd; F.ur = d_ur; F.p_layer = d_pl; F.p_cap = d_pc; F.p_w = d_pw;
     F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv; F.height = d_height;
     DevScratch &S = ctx->S;
-    const size_t BL = (size_t)std::max<int64_t>(max_big_nodes, 1) * ctx->LD;
-    TRY(dev_alloc(ctx, &S.bkap, (size_t)std::max<int64_t>(max_big_nodes, 1) * (ctx->L - 1)));
-    TRY(dev_alloc(ctx, &S.bA, BL)); TRY(dev_alloc(ctx, &S.bB, BL)); TRY(dev_alloc(ctx, &S.bC, BL));
-    TRY(dev_alloc(ctx, &S.bchoice, BL)); TRY(dev_alloc(ctx, &S.bentry, BL)); TRY(dev_alloc(ctx, &S.froot, N));
+    TRY(dev_alloc(ctx, &S.froot, N));
     TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
     TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
     TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
     if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
+    // persistent k_assign grid, work items, tickets, dataflow counters, big-net slots
+    {
+        int per_sm = 0, n_sm = 0;
+        CK(assign_resident_ctas(ctx->L, ctx->LD, ctx->NS, ctx->NP, &per_sm, &n_sm));
+        if (per_sm < 1) return set_err(LA_ECUDA, "k_assign does not fit on an SM");
+        ctx->grid = per_sm * n_sm;
+        TRY(dev_upload(ctx, &ctx->d_items, items.data(), items.size()));
+        ctx->h_items = items;
+        ctx->dev_allocs.pop_back();   // owned by the ctx field, freed in ~la_ctx
+        CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned long long) * (nb + 1)));
+        CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * (nb + 1), ctx->stream));
+        CK(cudaMalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+        if (N) CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        // a big net runs out of the CTA's four small-net buffers when it fits there
+        size_t small = (size_t)ASSIGN_WARPS * assign_net_bytes(ctx->NS, ctx->NP, ctx->L, ctx->LD);
+        if (const char *e = getenv("GAPLA_BIG_SMEM")) small = std::min<size_t>(small, (size_t)atoll(e));
+        ctx->big_smem = (int64_t)small;
+        const size_t need = assign_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD);
+        ctx->gslot_bytes = 0;
+        if (max_big_nodes > 0 && need > small) {
+            ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
+            CK(cudaMalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));
+        }
+    }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->h_xy.swap(xy);
@@ -945,28 +1008,45 @@ static la_status check_ready(la_ctx *ctx) {
     return LA_OK;
 }
 
+// This rank's share of batch k: a contiguous range of the batch's work items.
+static void rank_items(const la_ctx *ctx, int32_t batch, int64_t *i0, int64_t *i1) {
+    const int64_t b0 = ctx->batch_item0[batch], b1 = ctx->batch_item0[batch + 1];
+    int64_t s0, s1;
+    la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
+    *i0 = b0 + s0;
+    *i1 = b0 + s1;
+}
+
+static AssignLaunch assign_launch(const la_ctx *ctx) {
+    AssignLaunch al{};
+    al.items = ctx->d_items;
+    al.gscratch = ctx->d_gscratch;
+    al.gslot_bytes = ctx->gslot_bytes;
+    al.NS = ctx->NS;
+    al.NP = ctx->NP;
+    al.big_smem = ctx->big_smem;
+    al.LD = ctx->LD;
+    al.commit = (ctx->world == 1 && ctx->fuse_commit) ? 1 : 0;
+    return al;
+}
+
 la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     TRY(check_ready(ctx));
     const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
     if (batch < 0 || batch >= nb) return set_err(LA_ERANGE, "batch index out of range");
     if (ctx->pending_commit || batch != ctx->next_batch)
         return set_err(LA_ESTATE, "batches must be assigned in order, each committed before the next");
-    int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1], s0, s1;
-    la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
     if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
-    AssignLaunch al;
-    al.net_beg = b0 + s0;
-    al.net_end = b0 + s1;
-    al.nbig = std::max<int64_t>(0, std::min<int64_t>(ctx->batch_nbig[batch], s1) - s0);
-    al.node_base = ctx->h_net_node0[b0];
-    al.LD = ctx->LD;
-    al.MP = ctx->MP;
-    al.commit = (ctx->world == 1 && ctx->fuse_commit) ? 1 : 0;
+    AssignLaunch al = assign_launch(ctx);
+    rank_items(ctx, batch, &al.item_beg, &al.item_end);
+    al.ticket = ctx->d_ticket + 1 + batch;
+    const int grid = (int)std::min<int64_t>(ctx->grid, al.item_end - al.item_beg);
     int pi = prof_begin(ctx, K_ASSIGN);
-    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, ctx->stream));
+    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
     prof_end(ctx, pi);
-    ctx->stats.launches += 1;
+    if (grid > 0) ctx->stats.launches += 1;
     ctx->pending_commit = true;
     return LA_OK;
 }
@@ -979,9 +1059,13 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
     if (ctx->world > 1) {
         // reconcile: every rank contributes its shard's packed decisions (others 0) -> sum
-        int64_t s0, s1;
-        la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
-        const int64_t m0 = ctx->h_net_node0[b0 + s0], m1 = ctx->h_net_node0[b0 + s1];
+        int64_t i0, i1;
+        rank_items(ctx, batch, &i0, &i1);
+        const int64_t e0 = i0 < i1 ? (int64_t)(ctx->h_items[i0] & 0xffffffffull) : b0;
+        const int64_t e1 = i0 < i1 ? (int64_t)(ctx->h_items[i1 - 1] & 0xffffffffull) +
+                                         (int64_t)((ctx->h_items[i1 - 1] >> 32) & 0xff)
+                                   : b0;
+        const int64_t m0 = ctx->h_net_node0[e0], m1 = ctx->h_net_node0[e1];
         int pr = prof_begin(ctx, K_RECONCILE);
         CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
         CK(launch_pack_decisions(ctx->S, m0, m1, ctx->stream));
@@ -1007,10 +1091,36 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
 la_status la_assign_all(la_ctx *ctx) {
     TRY(check_ready(ctx));
     const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    if (ctx->world == 1 && ctx->fuse_commit && ctx->schedule == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
+        ctx->next_batch == 0 && !ctx->flow_dirty) {
+        // one persistent launch over every work item, nets ordered by the dependency DAG
+        AssignLaunch al = assign_launch(ctx);
+        al.item_beg = 0;
+        al.item_end = ctx->n_items;
+        al.ticket = ctx->d_ticket;
+        al.wait = ctx->d_wait;
+        al.succ_off = ctx->d_succ_off;
+        al.succ = ctx->d_succ;
+        const int grid = (int)std::min<int64_t>(ctx->grid, ctx->n_items);
+        int pi = prof_begin(ctx, K_ASSIGN);
+        CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
+        prof_end(ctx, pi);
+        if (grid > 0) ctx->stats.launches += 1;
+        ctx->flow_dirty = true;
+        ctx->next_batch = nb;
+        return LA_OK;
+    }
     for (int32_t b = ctx->next_batch; b < nb; b++) {
         if (!ctx->pending_commit) TRY(la_assign_batch(ctx, b));
         TRY(la_commit_demand(ctx, b));
     }
+    return LA_OK;
+}
+
+la_status la_set_schedule(la_ctx *ctx, int32_t schedule) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (schedule != LA_SCHED_DATAFLOW && schedule != LA_SCHED_BATCH) return set_err(LA_EINVAL, "unknown schedule");
+    ctx->schedule = schedule;
     return LA_OK;
 }
 
@@ -1144,6 +1254,12 @@ la_status la_reset(la_ctx *ctx) {
     CK(cudaMemcpyAsync(ctx->d_wH, ctx->d_wH0, bH, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_wV, ctx->d_wV0, bV, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_via, ctx->d_via0, bVia, cudaMemcpyDeviceToDevice, ctx->stream));
+    const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * (nb + 1), ctx->stream));
+    if (ctx->n_nets)
+        CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * ctx->n_nets, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+    ctx->flow_dirty = false;
     ctx->next_batch = 0;
     ctx->pending_commit = false;
     return LA_OK;

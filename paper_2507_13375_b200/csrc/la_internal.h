@@ -60,20 +60,14 @@ struct DevForest {
     const uint8_t *net_pdrv;                  // driver pin layer
 };
 
-// Capacities of the warp-per-net (small) path of k_assign: a net whose LA tree
-// has at most NS_MAX nodes and at most NP_MAX sinks keeps all its DP state in
-// shared memory; larger nets take the CTA-per-net (big) path.
-constexpr int NS_MAX = 32;
-constexpr int NP_MAX = 64;
+// Default capacities of the warp-per-net (small) path of k_assign: a net whose LA
+// tree has at most NS nodes and at most NP sinks keeps all its DP state in its
+// warp's shared memory; larger nets take the CTA-per-net (big) path.
+constexpr int NS_DEFAULT = 32;
+constexpr int NP_DEFAULT = 64;
 constexpr int ASSIGN_WARPS = 4;
 
 struct DevScratch {
-    // big-path DP state, indexed by (node - first node of the batch); sized for
-    // the largest total node count of big nets in any batch
-    double *bkap;                             // [.][L-1] ViaCong per cut
-    double *bA, *bB, *bC;                     // [.][LD] O5 parent-edge terms by layer slot (bA holds S first)
-    uint16_t *bchoice;                        // [.][LD] b | t << 8
-    uint32_t *bentry;                         // [.][LD] son layers, byte i = son i
     double *froot;                            // [n_nets] f[root][p_drv]
     uint8_t *lay, *sb, *st;                   // decisions per node: entry layer, span (b, t)
     uint32_t *dec;                            // packed decisions for the multi-GPU reconcile
@@ -86,16 +80,26 @@ cudaError_t launch_pack_state(const DevGrid &G, const int32_t *wcap, const int32
                               const int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
 cudaError_t launch_unpack_demand(const DevGrid &G, const int32_t *wcap, const int32_t *vcap, int32_t *wdem,
                                  int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
+// One k_assign launch.  Items (batch-major): bits 0-31 first net, 32-39 net
+// count, bit 40 big (the CTA runs one net).  wait == nullptr: batch mode.
 struct AssignLaunch {
-    int64_t net_beg, net_end;                 // nets of this launch (batch-major)
-    int64_t nbig;                             // the first nbig of them take the big path
-    int64_t node_base;                        // first node of the batch: base of the big-path scratch
+    const uint64_t *items;
+    int64_t item_beg, item_end;               // items of this launch
+    unsigned long long *ticket;               // zeroed before the launch
+    int32_t *wait;                            // dataflow mode: unfinished predecessors per net
+    const int64_t *succ_off;                  // [n_nets+1] successor CSR (forest order)
+    const int32_t *succ;
+    char *gscratch;                           // big nets that do not fit shared memory:
+    int64_t gslot_bytes;                      //   one slot per CTA
+    int32_t NS, NP;                           // small-path capacities
+    int64_t big_smem;                         // bytes of shared memory a big net may use (else gscratch)
     int32_t LD;                               // max(#H layers, #V layers): layer slots per direction
-    int32_t MP;                               // max (entry layer, span bottom) tasks of one node
     int32_t commit;                           // fuse the demand commit (K8) into the kernel
 };
-size_t assign_smem_bytes(int L, int LD, int MP);
-cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a,
+size_t assign_smem_bytes(int L, int LD, int NS, int NP);
+size_t assign_net_bytes(int nodes, int sinks, int L, int LD);
+cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm);
+cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           cudaStream_t s);
 cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t node_beg,
                           int64_t node_end, cudaStream_t s);
@@ -105,9 +109,26 @@ cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch
                           int64_t net_end, cudaStream_t s);
 
 // GPU conflict-free batching (la_batch.cu): keys = (element << 32) | rank,
-// returns batch id per rank (host vector) and the number of batches.
+// returns batch id per rank (host vector) and the number of batches.  The
+// predecessor DAG (successor CSR over ranks, in-degrees) stays on the device in
+// `dag` until gpu_dag_to_positions re-indexes it into forest order.
+struct DagDev {
+    int64_t n = 0, n_edges = 0;
+    int64_t *off = nullptr;                   // [n+1]
+    int32_t *succ = nullptr;                  // [n_edges]
+    int32_t *indeg = nullptr;                 // [n]
+    void release();
+    DagDev() = default;
+    DagDev(const DagDev &) = delete;
+    DagDev &operator=(const DagDev &) = delete;
+    ~DagDev() { release(); }
+};
 cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int elem_bits, int64_t n_nets,
                                  std::vector<int32_t> &batch_of_rank, int32_t &n_batches, cudaStream_t s,
-                                 int64_t *launches);
+                                 int64_t *launches, DagDev *dag);
+// pos_of_rank / rank_of_pos: host arrays [n].  Outputs (device, caller frees
+// with cudaFree): off_p [n+1], succ_p [n_edges], indeg_p [n], all in positions.
+cudaError_t gpu_dag_to_positions(DagDev &dag, const int64_t *h_rank_of_pos, int64_t **off_p, int32_t **succ_p,
+                                 int32_t **indeg_p, cudaStream_t s, int64_t *launches);
 
 }  // namespace gapla

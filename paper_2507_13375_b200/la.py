@@ -80,6 +80,7 @@ def _load():
         "la_assign_batch": ([c_void_p, c_i32], c_i32),
         "la_commit_demand": ([c_void_p, c_i32], c_i32),
         "la_assign_all": ([c_void_p], c_i32),
+        "la_set_schedule": ([c_void_p, c_i32], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
         "la_get_demand": ([c_void_p, P(c_i32), P(c_i32)], c_i32),
@@ -104,7 +105,8 @@ def _load():
 _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
-           "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id")
+           "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
+           "la_set_schedule")
 
 
 def _check(st):
@@ -164,6 +166,13 @@ def la_get_demand(ctx, wire_dem=None, via_dem=None):
 
 def la_get_batches(ctx, out):
     _check(_lib.la_get_batches(ctx, _p(out, c_i32)))
+
+
+LA_SCHED_DATAFLOW, LA_SCHED_BATCH = 0, 1
+
+
+def la_set_schedule(ctx, schedule: int):
+    _check(_lib.la_set_schedule(ctx, int(schedule)))
 
 
 def la_reset(ctx):
@@ -280,6 +289,9 @@ class LayerAssigner:
 
     def assign_all(self):
         la_assign_all(self.ctx)
+
+    def set_schedule(self, schedule: int):
+        la_set_schedule(self.ctx, schedule)
 
     def eval_timing(self):
         d = self.d

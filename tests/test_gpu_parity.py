@@ -28,9 +28,11 @@ def la():
     return mod
 
 
-def run_gpu(la, d, per_batch=False):
+def run_gpu(la, d, per_batch=False, schedule=None):
     A = la.LayerAssigner(d, device=0)
     nb = A.load()
+    if schedule is not None:
+        A.set_schedule(schedule)
     if per_batch:
         for k in range(nb):
             A.assign_batch(k)
@@ -100,6 +102,27 @@ def test_per_batch_api_equals_assign_all(la):
     b = run_gpu(la, d, per_batch=False)
     for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost", "sink_delay"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("cfg,n", [(2, None), (4, 150_000)])
+def test_dataflow_equals_batch_schedule(la, cfg, n):
+    """the one-launch dataflow schedule and the batch-by-batch schedule
+    give bit-identical results (big nets, global-scratch nets and ties included)."""
+    d = synth.make_config(cfg, n_nets=n)
+    a = run_gpu(la, d, schedule=la.LA_SCHED_DATAFLOW)
+    b = run_gpu(la, d, schedule=la.LA_SCHED_BATCH)
+    for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost", "sink_delay", "net_cap", "net_rc"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_dense_conflicts_deep_dag(la):
+    """20K nets on a 24x24 grid: long conflict chains (hundreds of batches), so the
+    dataflow schedule's waits and releases are exercised on every net."""
+    d = synth.generate(20_000, 24, 24, 6, seed=77, pin_max=16, rdrv_mode=1, name="dense")
+    got = run_gpu(la, d)
+    ref = oracle.run(d)
+    assert got["n_batches"] > 200
+    assert_parity(got, ref, bitwise_fp=True)
 
 
 def test_reset_and_rerun_identical(la):
