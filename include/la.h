@@ -159,15 +159,16 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch);
 la_status la_commit_demand(la_ctx *ctx, int32_t batch);
 
 /* Every remaining batch (the whole Alg. 2 loop), enqueued.  Collective.
- * With one rank, schedule LA_SCHED_DATAFLOW (the default) and no batch assigned
- * since the last load / la_reset, this is ONE persistent launch in which each
- * net starts as soon as every earlier-priority net sharing a footprint element
- * with it has committed; the results are bit-identical to the
- * batch-by-batch schedule and to sequential assignment.  Otherwise it is
- * la_assign_batch + la_commit_demand for every remaining batch. */
+ * Default (LA_SCHED_BATCH): la_assign_batch + la_commit_demand for every
+ * remaining batch, one k_assign launch per batch in which every CTA first takes
+ * the batch's big nets, then its small nets.  With one rank, schedule
+ * LA_SCHED_DATAFLOW and no batch assigned since the last load / la_reset, this
+ * is ONE persistent launch in which each net starts as soon as every
+ * earlier-priority net sharing a footprint element with it has committed
+ * (DESIGN §2).  Both are bit-identical to sequential assignment. */
 la_status la_assign_all(la_ctx *ctx);
 
-/* Schedule used by la_assign_all on one rank. */
+/* Schedule used by la_assign_all on one rank; LA_SCHED_BATCH is the default. */
 enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an unknown value */
 
@@ -206,6 +207,16 @@ la_status la_set_profiling(la_ctx *ctx, int32_t enable);
 /* Accumulated per-kernel device times since the last reset (synchronises).
  * reset != 0 clears the accumulators after reading. */
 la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset);
+
+/* Diagnostics: enable (1) / disable (0) per-net timestamps in k_assign (device
+ * %globaltimer, ns).  While enabled every k_assign launch records, for each net
+ * it runs, [0] the time its warp took the net, [1] the time its predecessors
+ * were all committed (dataflow mode; = [0] otherwise), [2] the end of the
+ * gather, [3] the end of its commit, [4] the SM it ran on.  la_get_trace copies
+ * them to out[n_nets][5] in INPUT net order (synchronises); LA_ESTATE when
+ * tracing was never enabled.  Tracing adds one 40-byte store per net. */
+la_status la_set_tracing(la_ctx *ctx, int32_t enable);
+la_status la_get_trace(la_ctx *ctx, int64_t *out);
 
 /* Create an ncclUniqueId (128 bytes) on rank 0, to be broadcast to every rank
  * and passed as la_grid_desc.nccl_id. */

@@ -2,29 +2,50 @@
 // and the demand commit, for every net, as ONE kernel.
 //
 // Design (DESIGN §5 "k_assign", §2):
-//   * Work items.  The forest is batch-major; items are, in that
-//     order, either ONE big net (more than NS nodes or NP sinks) run by the whole
-//     CTA, or up to ASSIGN_WARPS consecutive small nets, one warp each.  CTAs are
-//     persistent and grab items with an atomic ticket.
-//   * Batch mode (la_assign_batch): the items of one conflict-free batch.
-//     Dataflow mode (la_assign_all, one GPU): ALL items in one cooperative launch;
+//   * Work.  The forest is batch-major.  CTAs are persistent and have
+//     one of two roles.  SMALL nets (at most NS nodes and NP sinks; ~99%): every
+//     warp takes the next one with its own atomic ticket and runs it alone, DP
+//     state in the warp's shared-memory slot.  BIG nets: the first n_big_ctas CTAs
+//     take one at a time and spread each height level's nodes over their warps,
+//     DP state in the CTA's whole shared memory (a global slot beyond that).  Big
+//     nets are few but long, and sit on the critical path of the conflict DAG.
+//   * Batch mode (la_assign_batch): the nets of one conflict-free batch.
+//     Dataflow mode (la_assign_all, one GPU): ALL nets in one cooperative launch;
 //     a net waits until its per-net count of unfinished predecessors (the
 //     conflict DAG) is 0, and after its commit releases its
-//     successors.  Items are taken in a topological order, so every waited-on
-//     net is held by a running CTA: no deadlock.
+//     successors.  Each role takes its nets in a topological priority order and
+//     waits only for the net it holds, so the earliest unfinished net is always
+//     held or next in its role's line: no deadlock.
 //   * Per net: (1) gather everything the DP reads from HBM -- node records,
-//     sinks, the via-cut words of every node GCell and the congestion sum S of
-//     every parent run on every legal layer -- with all loads in flight at once,
-//     into shared memory; (2) leaves, all at once, lanes over (leaf, entry
-//     layer); (3) internal nodes in height order, one warp per node: per-son
-//     candidate table cost'(l; s, j) for all (entry layer, son layer) pairs,
-//     lanes over (entry layer l, span-bottom group) sweep the span top t upward
-//     with each son's running argmin (Alg. 3 l.370-395), a segmented shuffle
-//     argmin by the key (G', t-b, b) (l.404, reading R21) picks each entry
-//     layer's span; (4) level-parallel backtrack (Alg. 4); (5) decisions to HBM
+//     sinks, the ViaCong kappa of every cut of every node GCell and the
+//     congestion sum S of every parent run on every legal layer -- with all
+//     loads in flight at once; (2) all leaves at once, lanes over (leaf, entry
+//     layer); (3) internal nodes in height order, one WARP per node ("wide
+//     node", below); (4) level-parallel backtrack (Alg. 4); (5) decisions to HBM
 //     and the integer-atomic demand commit (O8).
+//
+// Wide node (Alg. 3 l.360-409 for one node, all entry layers).  Tables first,
+// lanes in parallel: V(b, t) for every b <= t (R10, each row summed ascending
+// from b), cost'(l_e; s_k, j) for every (entry, son, son layer) (O5).  Then the
+// CANDIDATE spans of every entry are tasks spread over the lanes; each task
+// takes every son's window argmin from the table and its G', and a segmented
+// warp argmin by the key (G', t-b, b) (R21) keeps each entry's best; the entry's
+// lane then recomputes G, K and the son layers of the winner and finishes.
+//
+// Candidate spans (exact; DESIGN §5 "minimal covers").  Alg. 3 enumerates every
+// span (b, t) with b <= b0 = min(l, nl), t >= t0 = max(l, nh).  Let S* be the
+// winner under the key and J* its per-son argmins (lowest j on ties).  The
+// smallest span S' covering {b0, t0} and J* lies inside S*; since kappa >= 0 and
+// rounded addition is monotone, V(S') <= V(S*), and every son keeps its argmin
+// (m_s(S') = cost'(j*_s)), so G'(S') <= G'(S*) with t'-b' <= t*-b*: the key
+// forces S' = S*.  Hence S* is the minimal cover of its own argmins, so
+//   b* in {b0} U {legal son layers < b0},  t* in {t0} U {legal son layers > t0},
+// and with ONE son (83% of internal nodes) also b* == b0 or t* == t0.  The
+// kernel evaluates exactly those spans, each with the oracle's expression
+// tree, so the argmin equals the full enumeration's.
+//
 // Bit-exactness: compiled with --fmad=false; every fp64 value is the DESIGN §3
-// expression tree in operand order; cross-lane reductions are min/argmin only.
+// expression tree in operand order; cross-lane reductions are argmins only.
 #include <cuda_runtime.h>
 
 #include "la_device.cuh"
@@ -33,78 +54,82 @@
 namespace gapla {
 namespace {
 
+constexpr int MAXE = 8;                               // entry layer slots per direction (L <= 16)
+
 // ---------------------------------------------------------------- layouts --
-// One net's DP state (NS nodes, NP sinks), as byte offsets from a base.
+// One net's DP state in a warp's slot (shared memory; a big net: the CTA's
+// slots, or a global slot): node records, (node, entry slot) records, kappa of
+// every (node, cut), sinks, decisions.
+struct NodeRec {
+    double wd, ur;                    // W_D w_n (Eq. 5), ur (O3)
+    uint32_t xy;                      // x | y << 16
+    uint16_t len, height, nsink, sink0;
+    uint16_t kid[MAXKIDS];            // children (net-local), E W N S order
+    uint8_t edir, nkid, nl, nh, lay, sb, st, pad;
+};
+static_assert(sizeof(NodeRec) == 48, "NodeRec layout");
+struct SlotRec {                      // node i, entry layer slot e
+    double A, C;                      // gathered S, then O5 A(l) and capb(l) of the parent edge
+};
+struct SinkRec {
+    double cap, w;                    // C_q, weight of its pin-via delay term
+};
+
 struct NetLay {
-    int wd, ur, A, C, pcap, pw, froot;                      // double
-    int xy, vw;                                              // 32-bit
-    int len, height, nsink, sink0, kid, entry;               // 16-bit
-    int edir, nkid, nl, nh, choice, lay, sb, st, player;     // 8-bit
-    int bytes;
+    int node, slot, sink, kap, dec, player, froot, bytes;
 };
 
 __host__ __device__ inline NetLay net_layout(int NS, int NP, int L, int LD) {
     NetLay w;
     int o = 0;
-    auto take = [&](int bytes) { int r = o; o += (bytes + 7) & ~7; return r; };
-    w.wd = take(8 * NS); w.ur = take(8 * NS); w.A = take(8 * NS * LD); w.C = take(8 * NS * LD);
-    w.pcap = take(8 * NP); w.pw = take(8 * NP); w.froot = take(8);
-    w.xy = take(4 * NS); w.vw = take(4 * NS * (L - 1));
-    w.len = take(2 * NS); w.height = take(2 * NS); w.nsink = take(2 * NS); w.sink0 = take(2 * NS);
-    w.kid = take(2 * NS * MAXKIDS); w.entry = take(2 * NS * LD);
-    w.edir = take(NS); w.nkid = take(NS); w.nl = take(NS); w.nh = take(NS); w.choice = take(NS * LD);
-    w.lay = take(NS); w.sb = take(NS); w.st = take(NS); w.player = take(NP);
-    w.bytes = (o + 15) & ~15;
-    return w;
-}
-
-// Per-warp scratch of the node routine.
-struct WarpLay {
-    int CP, kap, map, bytes;
-};
-
-__host__ __device__ inline WarpLay warp_layout(int L, int LD) {
-    WarpLay w;
-    w.CP = 0;
-    w.kap = w.CP + 8 * MAXKIDS * LD * LD;
-    w.map = w.kap + 8 * (L - 1);
-    w.bytes = (w.map + 2 * 32 + 15) & ~15;
+    auto take = [&](int bytes) { int r = o; o += (bytes + 15) & ~15; return r; };
+    w.node = take(48 * NS);
+    w.slot = take(16 * NS * LD);
+    w.sink = take(16 * NP);
+    w.kap = take(8 * NS * (L - 1));
+    w.dec = take(4 * NS * LD);        // (choice | entry << 8) per (node, slot)
+    w.player = take(NP);
+    w.froot = take(8);
+    w.bytes = o;
     return w;
 }
 
 struct NetBuf {
-    double *wd, *ur, *A, *C, *pcap, *pw, *froot;
-    uint32_t *xy;
-    int32_t *vw;
-    uint16_t *len, *height, *nsink, *sink0, *kid, *entry;
-    uint8_t *edir, *nkid, *nl, *nh, *choice, *lay, *sb, *st, *player;
+    NodeRec *nd;
+    SlotRec *sl;
+    SinkRec *sk;
+    double *kap;
+    uint32_t *dec;
+    uint8_t *player;
+    double *froot;
 };
 
 __device__ __forceinline__ NetBuf net_buf(char *b, const NetLay &w) {
     NetBuf n;
-    n.wd = (double *)(b + w.wd); n.ur = (double *)(b + w.ur); n.A = (double *)(b + w.A); n.C = (double *)(b + w.C);
-    n.pcap = (double *)(b + w.pcap); n.pw = (double *)(b + w.pw); n.froot = (double *)(b + w.froot);
-    n.xy = (uint32_t *)(b + w.xy); n.vw = (int32_t *)(b + w.vw);
-    n.len = (uint16_t *)(b + w.len); n.height = (uint16_t *)(b + w.height); n.nsink = (uint16_t *)(b + w.nsink);
-    n.sink0 = (uint16_t *)(b + w.sink0); n.kid = (uint16_t *)(b + w.kid); n.entry = (uint16_t *)(b + w.entry);
-    n.edir = (uint8_t *)(b + w.edir); n.nkid = (uint8_t *)(b + w.nkid); n.nl = (uint8_t *)(b + w.nl);
-    n.nh = (uint8_t *)(b + w.nh); n.choice = (uint8_t *)(b + w.choice); n.lay = (uint8_t *)(b + w.lay);
-    n.sb = (uint8_t *)(b + w.sb); n.st = (uint8_t *)(b + w.st); n.player = (uint8_t *)(b + w.player);
+    n.nd = (NodeRec *)(b + w.node); n.sl = (SlotRec *)(b + w.slot); n.sk = (SinkRec *)(b + w.sink);
+    n.kap = (double *)(b + w.kap); n.dec = (uint32_t *)(b + w.dec); n.player = (uint8_t *)(b + w.player);
+    n.froot = (double *)(b + w.froot);
     return n;
 }
 
-struct WarpBuf {
-    double *CP, *kap;
-    uint16_t *map;
+// Per-warp scratch of the wide node routine.
+struct WarpScr {
+    double Vt[MAXL * MAXL];               // V(b, t) of the current node, [b][t]
+    double cpt[MAXE * MAXKIDS * MAXE];    // cost'(l_e; s_k, slot s), [e][k][s]
+    double bestG[MAXE];                   // per entry: best G' so far
+    uint32_t bestK[MAXE];                 // per entry: (t - b) << 4 | b, bit 8 = none
+    int32_t off[MAXE + 1];                // task offsets per entry
+    uint32_t mT[MAXE], mB[MAXE];          // candidate tops above t0 / bottoms below b0
+    uint8_t el[MAXE], eb0[MAXE], et0[MAXE], enT[MAXE];
 };
+constexpr int SCR_BYTES = (int)((sizeof(WarpScr) + 15) & ~(size_t)15);
 
 struct Shared {          // per-CTA static shared memory
     TechTab T;
     uint8_t dir[MAXL], routable[MAXL], lidx[MAXL];
     uint8_t lay_of[2][MAXL];   // layer of slot s in direction d
     int ndir[2];               // legal layers per direction
-    int64_t item;
-    int lo, hi;                // big path: current level [lo, hi)
+    uint32_t legal[2];         // bit j: layer j is routable and of direction d
 };
 
 // Context of one net inside the node routines.
@@ -117,42 +142,42 @@ __device__ __forceinline__ double kappa_w(const DevGrid &G, const Shared &sh, in
     return G.W_VIA + (G.W_CONG * sh.T.ofw[k]) * marginal(G, w);    // ViaCong, reading R11
 }
 
+// n-th (1-based) set bit of m
+__device__ __forceinline__ int nth_bit(uint32_t m, int n) {
+    for (int k = 1; k < n; ++k) m &= m - 1;
+    return __ffs(m) - 1;
+}
+
 // -------------------------------------------------------- node finishing --
 // Entry layer l (slot `slot`) of node i once its span is chosen: pin terms
 // (Alg. 3 l.4-7), f and dlc (l.405), choice / entry (l.406-408); for a non-root
 // node also the O5 parent-edge terms A and capb on layer l (its edge layer).
 __device__ __forceinline__ void finish_layer(const NetCtx &c, const Shared &sh, const DevGrid &G, int i, bool root,
-                                             int l, int slot, bool have, double Gv, double K, int b, int t,
-                                             uint32_t ent) {
+                                             int l, int slot, double Gv, double K, int b, int t, uint32_t ent) {
     const NetBuf &nb = c.nb;
     const int at = i * c.LD + slot;
-    if (!have) {
-        if (root) *nb.froot = dinf();
-        else nb.A[at] = dinf();
-        return;
-    }
+    const NodeRec &nd = nb.nd[i];
     double F0 = 0.0, C0 = 0.0;
-    const int q0 = nb.sink0[i], qn = nb.nsink[i];
+    const int q0 = nd.sink0, qn = nd.nsink;
     for (int q = q0; q < q0 + qn; ++q) {
-        const double cq = nb.pcap[q];
-        F0 = F0 + nb.pw[q] * (cq * sh.T.VR[nb.player[q] * MAXL + l]);
+        const double cq = nb.sk[q].cap;
+        F0 = F0 + nb.sk[q].w * (cq * sh.T.VR[nb.player[q] * MAXL + l]);
         C0 = C0 + cq;
     }
     const double f = F0 + Gv;
     const double dlc = C0 + K;
-    nb.choice[at] = (uint8_t)(b | (t << 4));
-    nb.entry[at] = (uint16_t)ent;
+    nb.dec[at] = (uint32_t)(b | (t << 4)) | (ent << 8);
     if (root) {
         *nb.froot = f;
         return;
     }
-    const double Sc = nb.A[at];                 // congestion sum gathered up front
-    const double len = (double)nb.len[i];
+    const double Sc = nb.sl[at].A;              // congestion sum gathered up front
+    const double len = (double)nd.len;
     const double Rw = sh.T.r[l] * len;
     const double Cw = sh.T.c[l] * len;
-    const double wd = nb.wd[i];
-    nb.A[at] = ((f + wd * (Rw * (0.5 * Cw + dlc))) + G.W_CAP * Cw) + (G.W_CONG * sh.T.ofw[l]) * Sc;
-    nb.C[at] = Cw + dlc;
+    const double wd = nd.wd;
+    nb.sl[at].A = ((f + wd * (Rw * (0.5 * Cw + dlc))) + G.W_CAP * Cw) + (G.W_CONG * sh.T.ofw[l]) * Sc;
+    nb.sl[at].C = Cw + dlc;
 }
 
 // ----------------------------------------------------------------- leaves --
@@ -165,181 +190,292 @@ __device__ void leaves_dp(const NetCtx &c, const Shared &sh, const DevGrid &G, i
     const int LD = c.LD, Lm1 = c.L - 1;
     for (int idx = tid; idx < nleaf * LD; idx += nthr) {
         const int i = idx / LD, s = idx - i * LD;
-        const int dt = nb.edir[i] <= 1 ? 0 : 1;
+        const NodeRec &nd = nb.nd[i];
+        const int dt = nd.edir <= 1 ? 0 : 1;
         if (s >= sh.ndir[dt]) continue;
         const int l = sh.lay_of[dt][s];
         if (!sh.routable[l]) continue;           // illegal entry layer (R15): A keeps +inf
-        const int nl = nb.nl[i], nh = nb.nh[i];
+        const int nl = nd.nl, nh = nd.nh;
         const bool pins = nl != 255;
         const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
         double V = 0.0;
-        for (int k = b0; k < t0; ++k) V = V + kappa_w(G, sh, nb.vw[i * Lm1 + k], k);
-        finish_layer(c, sh, G, i, false, l, s, true, V, 0.0, b0, t0, 0u);
+        for (int k = b0; k < t0; ++k) V = V + nb.kap[i * Lm1 + k];
+        finish_layer(c, sh, G, i, false, l, s, V, 0.0, b0, t0, 0u);
     }
 }
 
-// -------------------------------------------------------------- node DP --
-// Alg. 3 for node i (internal, or the root), all entry layers, one warp.
-__device__ void node_dp(const NetCtx &c, const WarpBuf &wb, const Shared &sh, const DevGrid &G, int i, bool root,
-                        int pdrv, int lane) {
-    const NetBuf &nb = c.nb;
-    const int L = c.L, LD = c.LD, Lm1 = L - 1;
-    const int nk = nb.nkid[i];
-    const int nl = nb.nl[i], nh = nb.nh[i];
-    const bool pins = nl != 255;
-    const int dt = root ? 0 : (nb.edir[i] <= 1 ? 0 : 1);
-    const int nE = root ? 1 : sh.ndir[dt];
-    const double urn = nb.ur[i];
-    int kid[MAXKIDS], kdt[MAXKIDS];
+// -------------------------------------------------------------- wide node --
+// Son k's window argmin over [b, t] on entry e: lowest layer among the minima
+// of the finite cost' values (ascending slots = ascending layers, strict <).
+__device__ __forceinline__ int window_argmin(const WarpScr &w, const Shared &sh, int e, int k, int dk, int b, int t,
+                                             double *mv) {
+    double m = dinf();
+    int jb = -1;
+    const double *row = w.cpt + (e * MAXKIDS + k) * MAXE;
 #pragma unroll
-    for (int k = 0; k < MAXKIDS; ++k) {
-        kid[k] = k < nk ? nb.kid[i * MAXKIDS + k] : 0;
-        kdt[k] = k < nk ? (nb.edir[kid[k]] <= 1 ? 0 : 1) : 0;
-    }
-    // ViaCong per cut of this node's GCell
-    if (lane < Lm1) wb.kap[lane] = kappa_w(G, sh, nb.vw[i * Lm1 + lane], lane);
-    // candidate table CP[k][e][js] = cost'(l_e; s_k, j) (O5): +inf where the son is infeasible
-    const int per_k = nE * LD;
-    for (int idx = lane; idx < nk * per_k; idx += 32) {
-        const int k = idx / per_k, r = idx - k * per_k;
-        const int e = r / LD, js = r - e * LD;
-        int kk = 0, dk = 0;
-#pragma unroll
-        for (int q = 0; q < MAXKIDS; ++q) if (q == k) { kk = kid[q]; dk = kdt[q]; }
-        if (js >= sh.ndir[dk]) continue;
-        const int l = root ? pdrv : sh.lay_of[dt][e];
-        const int j = sh.lay_of[dk][js];
-        const int at = kk * LD + js;
-        const double A = nb.A[at];
-        double cp = dinf();
-        if (A < dinf()) {
-            const double Bv = nb.wd[kk] * nb.C[at];          // B = wd_s (Cw + D)
-            const double cost = A + Bv * sh.T.VR[l * MAXL + j];
-            cp = cost + Bv * urn;
-        }
-        wb.CP[(k * LD + e) * LD + js] = cp;
-    }
-    // span-bottom tasks: entry e has b in [0, b0(e)]; a lane owns up to m of them
-    int cnt = 0;
-    if (lane < nE) {
-        const int l = root ? pdrv : sh.lay_of[dt][lane];
-        if (root || sh.routable[l]) cnt = (pins ? min(l, nl) : l) + 1;   // R13, R15
-    }
-    int m = 1, g = cnt, P = 0;
-    for (;;) {
-        g = (cnt + m - 1) / m;
-        P = g;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(FULL_MASK, P, o);
-        if (P <= 32) break;
-        ++m;
-    }
-    int inc = g;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int x = __shfl_up_sync(FULL_MASK, inc, o);
-        if (lane >= o) inc += x;
-    }
-    for (int q = 0; q < g; ++q) wb.map[inc - g + q] = (uint16_t)(lane | (q << 8));
-    __syncwarp();
-
-    bool have = false;
-    double bGp = 0.0, bV = 0.0;
-    int bt = 0, bb = 0;
-    uint32_t bjs = 0;
-    int e = 0, seg_end = 0;
-    if (lane < P) {
-        const uint16_t mp = wb.map[lane];
-        e = mp & 0xff;
-        const int q = mp >> 8;
-        const int l = root ? pdrv : sh.lay_of[dt][e];
-        const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
-        const double *CPe = wb.CP + e * LD;
-        const int bend = min(q * m + m, b0 + 1);
-        for (int b = q * m; b < bend; ++b) {
-            double V = 0.0;
-            for (int k = b; k < t0; ++k) V = V + wb.kap[k];
-            double mv[MAXKIDS];
-            int jb[MAXKIDS];
-#pragma unroll
-            for (int k = 0; k < MAXKIDS; ++k) { mv[k] = dinf(); jb[k] = -1; }
-            // son argmin of cost' over j in [b, t], ties -> lowest j (ascending j, strict <)
-            auto consider = [&](int j) {
-                if (!sh.routable[j]) return;
-                const int dj = sh.dir[j], sj = sh.lidx[j];
-#pragma unroll
-                for (int k = 0; k < MAXKIDS; ++k) {
-                    if (k < nk && kdt[k] == dj) {
-                        const double cp = CPe[k * LD * LD + sj];
-                        if (cp < mv[k]) { mv[k] = cp; jb[k] = j; }
-                    }
-                }
-            };
-            for (int j = b; j <= t0; ++j) consider(j);
-            for (int t = t0; t < L; ++t) {
-                if (t > t0) {
-                    V = V + wb.kap[t - 1];
-                    consider(t);
-                }
-                bool feas = true;
-                double Gp = V;
-                uint32_t js = 0;
-#pragma unroll
-                for (int k = 0; k < MAXKIDS; ++k) {
-                    if (k < nk) {
-                        feas = feas && jb[k] >= 0;
-                        Gp = Gp + mv[k];
-                        js |= (uint32_t)(jb[k] & 0xf) << (4 * k);
-                    }
-                }
-                if (!feas) continue;
-                // key (G', t - b, b), lexicographic (reading R21)
-                const bool better = !have || Gp < bGp ||
-                                    (Gp == bGp && ((t - b) < (bt - bb) || ((t - b) == (bt - bb) && b < bb)));
-                if (better) { have = true; bGp = Gp; bt = t; bb = b; bjs = js; bV = V; }
+    for (int s = 0; s < MAXE; ++s) {
+        if (s < sh.ndir[dk]) {
+            const int j = sh.lay_of[dk][s];
+            if (j >= b && j <= t) {
+                const double cp = row[s];
+                if (cp < m) { m = cp; jb = j; }
             }
         }
     }
-    // segmented argmin over the lanes of one entry layer (contiguous lanes)
-    seg_end = __shfl_sync(FULL_MASK, inc, e);
-    if (lane >= P) seg_end = 0;
-    uint32_t key = (have ? 1u << 16 : 0u) | ((uint32_t)bt << 8) | ((uint32_t)bb << 4) | 0u;
-    int src = lane;
+    *mv = m;
+    return jb;
+}
+
+// Alg. 3 for a node with ONE son (83% of internal nodes), all entries, by one
+// warp: 8-lane segments, one per entry layer, lane s of a segment = son layer
+// slot s.  Candidates (header: minimal covers): (b0, t0), (b0, j) for son layers
+// j > t0 and (j, t0) for son layers j < b0; the window minima come from two
+// segmented scans -- upward from b0 (strict <: the lower layer keeps ties) and
+// downward from t0 (the lower layer wins ties) -- and a butterfly argmin by the
+// key (G', t-b, b) picks each entry's span.
+__device__ __forceinline__ void node_dp_1son(const NetCtx &c, const WarpScr &w, const Shared &sh, const DevGrid &G,
+                                             int i, bool root, int pdrv, int dt, int nE, int kk, int dk, int lane) {
+    const NetBuf &nb = c.nb;
+    const NodeRec &nd = nb.nd[i];
+    const int LD = c.LD, ndk = sh.ndir[dk], s = lane & 7;
+    const double urn = nd.ur, wdk = nb.nd[kk].wd;
+    const int nl = nd.nl, nh = nd.nh;
+    const bool pins = nl != 255;
+    const int j = s < ndk ? sh.lay_of[dk][s] : MAXL;
+    const int jnext = s + 1 < ndk ? sh.lay_of[dk][s + 1] : MAXL;
+    for (int e0 = 0; e0 < nE; e0 += 4) {
+        const int e = e0 + (lane >> 3);
+        const int l = root ? pdrv : sh.lay_of[dt][e < nE ? e : 0];
+        const bool eok = e < nE && (root || sh.routable[l]);
+        const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+        double cp = dinf();
+        if (eok && s < ndk) {
+            const SlotRec &rr = nb.sl[kk * LD + s];
+            const double A = rr.A;
+            if (A < dinf()) {
+                const double Bv = wdk * rr.C;                // B = wd_s (Cw + D)
+                const double cost = A + Bv * sh.T.VR[l * MAXL + j];
+                cp = cost + Bv * urn;
+            }
+        }
+        // windows [b0, j]: inclusive prefix min over layers >= b0, lowest layer on ties
+        double pu = (j >= b0 && cp < dinf()) ? cp : dinf();
+        int ju = pu < dinf() ? j : -1;
+        // windows [j, t0]: inclusive suffix min over layers <= t0, lowest layer on ties
+        double pd = (j <= t0 && cp < dinf()) ? cp : dinf();
+        int jd = pd < dinf() ? j : -1;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const double oG = __shfl_down_sync(FULL_MASK, bGp, o);
-        const uint32_t ok = __shfl_down_sync(FULL_MASK, key, o);
-        const int os = __shfl_down_sync(FULL_MASK, src, o);
-        if (lane + o < seg_end && (ok >> 16)) {
-            const int ot = (ok >> 8) & 0xff, ob = (ok >> 4) & 0xf;
-            const int mt = (key >> 8) & 0xff, mb = (key >> 4) & 0xf;
-            const bool better = !(key >> 16) || oG < bGp ||
-                                (oG == bGp && ((ot - ob) < (mt - mb) || ((ot - ob) == (mt - mb) && ob < mb)));
-            if (better) { bGp = oG; key = ok; src = os; }
+        for (int o = 1; o < 8; o <<= 1) {
+            const double ou = __shfl_up_sync(FULL_MASK, pu, o, 8);
+            const int oju = __shfl_up_sync(FULL_MASK, ju, o, 8);
+            const double od = __shfl_down_sync(FULL_MASK, pd, o, 8);
+            const int ojd = __shfl_down_sync(FULL_MASK, jd, o, 8);
+            if (s >= o && ou <= pu && oju >= 0) { pu = ou; ju = oju; }
+            if (s + o < 8 && od < pd) { pd = od; jd = ojd; }
+        }
+        double Gp = dinf();
+        uint32_t key = 0x1ffu;
+        int jm = -1;
+        if (eok && s < ndk) {
+            int b = b0, t = t0;
+            double m = dinf();
+            if (j > t0) { t = j; m = pu; jm = ju; }
+            else if (j < b0) { b = j; m = pd; jm = jd; }
+            else if (jnext > t0) { m = pu; jm = ju; }        // last son layer inside [b0, t0]: the base span
+            if (jm >= 0) {
+                Gp = w.Vt[b * MAXL + t] + m;
+                key = (uint32_t)(((t - b) << 4) | b);
+            }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const double oG = __shfl_xor_sync(FULL_MASK, Gp, o, 8);
+            const uint32_t ok = __shfl_xor_sync(FULL_MASK, key, o, 8);
+            const int oj = __shfl_xor_sync(FULL_MASK, jm, o, 8);
+            if (oG < Gp || (oG == Gp && ok < key)) { Gp = oG; key = ok; jm = oj; }
+        }
+        if (eok && s == 0) {
+            const int slot = root ? 0 : e;
+            if (key & 0x100u) {
+                if (root) *nb.froot = dinf();
+                else nb.sl[i * LD + slot].A = dinf();
+            } else {
+                const int b = key & 0xf, t = b + (int)(key >> 4);
+                const SlotRec &rr = nb.sl[kk * LD + sh.lidx[jm]];
+                const double Bv = wdk * rr.C;
+                const double Gv = w.Vt[b * MAXL + t] + (rr.A + Bv * sh.T.VR[l * MAXL + jm]);   // G: cost, not cost'
+                finish_layer(c, sh, G, i, root, l, slot, Gv, 0.0 + rr.C, b, t, (uint32_t)jm);
+            }
         }
     }
-    const uint32_t wjs = __shfl_sync(FULL_MASK, bjs, src);
-    const double wV = __shfl_sync(FULL_MASK, bV, src);
-    if (lane < P && (wb.map[lane] >> 8) == 0) {      // head lane of entry e
+}
+
+// Alg. 3 for internal node (or root) i by one warp.
+__device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, const DevGrid &G, int i, int pdrv,
+                             int lane) {
+    const NetBuf &nb = c.nb;
+    const int L = c.L, LD = c.LD, Lm1 = L - 1;
+    const bool root = i == c.nn - 1;
+    const NodeRec &nd = nb.nd[i];
+    const int nk = nd.nkid;
+    const int dt = root ? 0 : (nd.edir <= 1 ? 0 : 1);
+    const int nE = root ? 1 : sh.ndir[dt];
+    const double urn = nd.ur;
+    int kid[MAXKIDS], kdt[MAXKIDS];
+    uint32_t legal_any = 0;
+#pragma unroll
+    for (int k = 0; k < MAXKIDS; ++k) {
+        kid[k] = k < nk ? nd.kid[k] : 0;
+        kdt[k] = k < nk ? (nb.nd[kid[k]].edir <= 1 ? 0 : 1) : 0;
+        if (k < nk) legal_any |= sh.legal[kdt[k]];
+    }
+    const double *kap = nb.kap + i * Lm1;
+    // (1) V table: lane b sums its row ascending from b (R10, R23)
+    if (lane < L) {
+        double V = 0.0;
+        w.Vt[lane * MAXL + lane] = 0.0;
+#pragma unroll
+        for (int t = 1; t < MAXL; ++t) {
+            if (t > lane && t < L) {
+                V = V + kap[t - 1];
+                w.Vt[lane * MAXL + t] = V;
+            }
+        }
+    }
+    if (nk == 1) {
+        __syncwarp();
+        node_dp_1son(c, w, sh, G, i, root, pdrv, dt, nE, kid[0], kdt[0], lane);
+        __syncwarp();
+        return;
+    }
+    // (2) cost' table (O5, R16-R17): +inf where the son is infeasible on the layer
+    const int ncp = nE * nk * MAXE;
+    for (int idx = lane; idx < ncp; idx += 32) {
+        const int e = idx / (nk * MAXE), r = idx - e * (nk * MAXE);
+        const int k = r / MAXE, s = r - k * MAXE;
+        int kk = 0, dk = 0;
+#pragma unroll
+        for (int q = 0; q < MAXKIDS; ++q) if (q == k) { kk = kid[q]; dk = kdt[q]; }
+        if (s >= sh.ndir[dk]) continue;
         const int l = root ? pdrv : sh.lay_of[dt][e];
-        const int slot = root ? 0 : e;
-        if (!(key >> 16)) {
-            finish_layer(c, sh, G, i, root, l, slot, false, 0.0, 0.0, 0, 0, 0u);
-        } else {
-            const int t = (key >> 8) & 0xff, b = (key >> 4) & 0xf;
-            double Gv = wV, K = 0.0;
+        const int j = sh.lay_of[dk][s];
+        const SlotRec &rr = nb.sl[kk * LD + s];
+        const double A = rr.A;
+        double cp = dinf();
+        if (A < dinf()) {
+            const double Bv = nb.nd[kk].wd * rr.C;           // B = wd_s (Cw + D)
+            const double cost = A + Bv * sh.T.VR[l * MAXL + j];
+            cp = cost + Bv * urn;
+        }
+        w.cpt[(e * MAXKIDS + k) * MAXE + s] = cp;
+    }
+    // (3) entries: span bounds, candidate sets, task counts (warp prefix sum)
+    int cnt = 0;
+    if (lane < nE) {
+        const int l = root ? pdrv : sh.lay_of[dt][lane];
+        w.el[lane] = (uint8_t)l;
+        if (root || sh.routable[l]) {                  // illegal entry layers keep A = +inf (R15)
+            const int nl = nd.nl, nh = nd.nh;
+            const bool pins = nl != 255;
+            const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+            const uint32_t mT = legal_any & ~((2u << t0) - 1u);
+            const uint32_t mB = legal_any & ((1u << b0) - 1u);
+            const int nT = 1 + __popc(mT), nB = 1 + __popc(mB);
+            cnt = nk == 0 ? 1 : (nk == 1 ? nT + nB - 1 : nT * nB);
+            w.eb0[lane] = (uint8_t)b0;
+            w.et0[lane] = (uint8_t)t0;
+            w.enT[lane] = (uint8_t)nT;
+            w.mT[lane] = mT;
+            w.mB[lane] = mB;
+        }
+        w.bestG[lane] = dinf();
+        w.bestK[lane] = 0x1ffu;
+    }
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < MAXE; o <<= 1) {
+        const int x = __shfl_up_sync(FULL_MASK, inc, o);
+        if (lane >= o) inc += x;
+    }
+    if (lane < nE) w.off[lane + 1] = inc;
+    if (lane == 0) w.off[0] = 0;
+    const int total = __shfl_sync(FULL_MASK, inc, nE - 1);
+    __syncwarp();
+    // (4) candidate tasks, 32 per round, segmented argmin per entry
+    for (int base = 0; base < total; base += 32) {
+        const int idx = base + lane;
+        double Gp = dinf();
+        uint32_t key = 0x1ffu;
+        int seg_end = 0, e = 0;
+        if (idx < total) {
+            while (e + 1 < nE && w.off[e + 1] <= idx) ++e;
+            seg_end = min(w.off[e + 1] - base, 32);
+            const int cI = idx - w.off[e];
+            const int b0 = w.eb0[e], t0 = w.et0[e], nT = w.enT[e];
+            int b = b0, t = t0;
+            if (nk == 1) {
+                if (cI < nT) t = cI == 0 ? t0 : nth_bit(w.mT[e], cI);
+                else b = nth_bit(w.mB[e], cI - nT + 1);
+            } else if (nk >= 2) {
+                const int bi = cI / nT, ti = cI - bi * nT;
+                if (bi) b = nth_bit(w.mB[e], bi);
+                if (ti) t = nth_bit(w.mT[e], ti);
+            }
+            double g = w.Vt[b * MAXL + t];
+            bool feas = true;
 #pragma unroll
             for (int k = 0; k < MAXKIDS; ++k) {
                 if (k < nk) {
-                    const int j = (wjs >> (4 * k)) & 0xf;
-                    const int at = kid[k] * LD + sh.lidx[j];
-                    const double A = nb.A[at], Cc = nb.C[at];
-                    const double Bv = nb.wd[kid[k]] * Cc;
+                    double mv;
+                    feas = feas && window_argmin(w, sh, e, k, kdt[k], b, t, &mv) >= 0;
+                    g = g + mv;
+                }
+            }
+            if (feas) {
+                Gp = g;
+                key = (uint32_t)(((t - b) << 4) | b);
+            }
+        }
+        // segmented argmin over the lanes of one entry (contiguous lanes)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double oG = __shfl_down_sync(FULL_MASK, Gp, o);
+            const uint32_t ok = __shfl_down_sync(FULL_MASK, key, o);
+            if (lane + o < seg_end && (oG < Gp || (oG == Gp && ok < key))) { Gp = oG; key = ok; }
+        }
+        if (idx < total && (lane == 0 || idx == w.off[e])) {    // head of entry e's segment in this round
+            if (Gp < w.bestG[e] || (Gp == w.bestG[e] && key < w.bestK[e])) {
+                w.bestG[e] = Gp;
+                w.bestK[e] = key;
+            }
+        }
+        __syncwarp();
+    }
+    // (5) entry lanes: winner's son layers, G (cost, not cost'), K; finish
+    if (lane < nE && (root || sh.routable[w.el[lane]])) {
+        const int e = lane, l = w.el[e];
+        const uint32_t key = w.bestK[e];
+        if (key & 0x100u) {
+            if (root) *nb.froot = dinf();
+            else nb.sl[i * LD + e].A = dinf();
+        } else {
+            const int b = key & 0xf, t = b + (int)(key >> 4);
+            double Gv = w.Vt[b * MAXL + t], K = 0.0;
+            uint32_t js = 0;
+#pragma unroll
+            for (int k = 0; k < MAXKIDS; ++k) {
+                if (k < nk) {
+                    double mv;
+                    const int j = window_argmin(w, sh, e, k, kdt[k], b, t, &mv);
+                    js |= (uint32_t)j << (4 * k);
+                    const SlotRec &rr = nb.sl[kid[k] * LD + sh.lidx[j]];
+                    const double A = rr.A, Cc = rr.C;
+                    const double Bv = nb.nd[kid[k]].wd * Cc;
                     Gv = Gv + (A + Bv * sh.T.VR[l * MAXL + j]);
                     K = K + Cc;
                 }
             }
-            finish_layer(c, sh, G, i, root, l, slot, true, Gv, K, b, t, wjs);
+            finish_layer(c, sh, G, i, root, l, root ? 0 : e, Gv, K, b, t, js);
         }
     }
     __syncwarp();
@@ -367,55 +503,55 @@ __device__ __forceinline__ double run_sum(const DevGrid &G, int dtype, int lslot
 }
 
 // Node records and sinks of net [n0, n0+nn) into nb (threads tid of nthr).
-__device__ __forceinline__ void gather_nodes(const NetBuf &nb, const DevForest &F, int64_t n0, int nn, int tid,
-                                             int nthr) {
-    const int q_base = F.sink0[n0];
+__device__ __forceinline__ void gather_nodes(const NetBuf &nb, const DevForest &F, int64_t n0, int nn, int q_base,
+                                             int ns, int tid, int nthr) {
     for (int i = tid; i < nn; i += nthr) {
         const int64_t n = n0 + i;
-        nb.xy[i] = F.xy[n];
-        nb.len[i] = (uint16_t)F.len[n];
-        nb.edir[i] = F.edir[n];
-        nb.nkid[i] = F.nkid[n];
-        nb.nl[i] = F.nl[n];
-        nb.nh[i] = F.nh[n];
-        nb.height[i] = F.height[n];
-        nb.nsink[i] = F.nsink[n];
-        nb.sink0[i] = (uint16_t)(F.sink0[n] - q_base);
-        nb.wd[i] = F.wd[n];
-        nb.ur[i] = F.ur[n];
+        NodeRec r;
+        r.wd = F.wd[n];
+        r.ur = F.ur[n];
+        r.xy = F.xy[n];
+        r.len = (uint16_t)F.len[n];
+        r.height = F.height[n];
+        r.nsink = F.nsink[n];
+        r.sink0 = (uint16_t)(F.sink0[n] - q_base);
         const int4 k4 = *reinterpret_cast<const int4 *>(F.kid + n * 4);
-        nb.kid[i * 4 + 0] = (uint16_t)(k4.x - n0);
-        nb.kid[i * 4 + 1] = (uint16_t)(k4.y - n0);
-        nb.kid[i * 4 + 2] = (uint16_t)(k4.z - n0);
-        nb.kid[i * 4 + 3] = (uint16_t)(k4.w - n0);
+        r.kid[0] = (uint16_t)(k4.x - n0);
+        r.kid[1] = (uint16_t)(k4.y - n0);
+        r.kid[2] = (uint16_t)(k4.z - n0);
+        r.kid[3] = (uint16_t)(k4.w - n0);
+        r.edir = F.edir[n];
+        r.nkid = F.nkid[n];
+        r.nl = F.nl[n];
+        r.nh = F.nh[n];
+        r.lay = r.sb = r.st = r.pad = 0;
+        nb.nd[i] = r;
     }
-    const int64_t nlast = n0 + nn - 1;
-    const int ns = F.sink0[nlast] + F.nsink[nlast] - q_base;
     for (int q = tid; q < ns; q += nthr) {
         nb.player[q] = F.p_layer[q_base + q];
-        nb.pcap[q] = F.p_cap[q_base + q];
-        nb.pw[q] = F.p_w[q_base + q];
+        nb.sk[q].cap = F.p_cap[q_base + q];
+        nb.sk[q].w = F.p_w[q_base + q];
     }
 }
 
-// Via-cut words per (node, cut) and S per (non-root node, layer slot).
+// kappa per (node, cut) and S per (non-root node, layer slot).
 __device__ __forceinline__ void gather_state(const NetBuf &nb, const DevGrid &G, const Shared &sh, int nn, int LD,
                                              int tid, int nthr) {
     const int Lm1 = G.L - 1;
     for (int idx = tid; idx < nn * Lm1; idx += nthr) {
         const int i = idx / Lm1, k = idx - i * Lm1;
-        const uint32_t xy = nb.xy[i];
-        nb.vw[idx] = __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k);
+        const uint32_t xy = nb.nd[i].xy;
+        nb.kap[idx] = kappa_w(G, sh, __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k), k);
     }
     for (int idx = tid; idx < nn * LD; idx += nthr) {
         const int i = idx / LD, s = idx - i * LD;
-        const int ed = nb.edir[i];
+        const int ed = nb.nd[i].edir;
         if (ed == NO_DIR) continue;
         const int dt = ed <= 1 ? 0 : 1;
         if (s >= sh.ndir[dt]) continue;
-        if (!sh.routable[sh.lay_of[dt][s]]) { nb.A[idx] = dinf(); continue; }
-        const uint32_t xy = nb.xy[i];
-        nb.A[idx] = run_sum(G, dt, s, xy & 0xffff, xy >> 16, ed, nb.len[i]);
+        if (!sh.routable[sh.lay_of[dt][s]]) { nb.sl[idx].A = dinf(); continue; }
+        const uint32_t xy = nb.nd[i].xy;
+        nb.sl[idx].A = run_sum(G, dt, s, xy & 0xffff, xy >> 16, ed, nb.nd[i].len);
     }
 }
 
@@ -439,21 +575,22 @@ __device__ __forceinline__ void commit_node(const DevGrid &G, uint32_t xy, int e
 // Backtrack of node i (Alg. 4): its span from choice[i][l_i], its sons' layers from entry.
 __device__ __forceinline__ void backtrack_node(const NetCtx &c, const Shared &sh, int i) {
     const NetBuf &nb = c.nb;
-    const int l = nb.lay[i];
+    NodeRec &nd = nb.nd[i];
+    const int l = nd.lay;
     const int slot = (i == c.nn - 1) ? 0 : sh.lidx[l];
-    const uint8_t ch = nb.choice[i * c.LD + slot];
-    nb.sb[i] = ch & 0xf;
-    nb.st[i] = ch >> 4;
-    const uint32_t js = nb.entry[i * c.LD + slot];
-    const int nk = nb.nkid[i];
-    for (int k = 0; k < nk; ++k) nb.lay[nb.kid[i * 4 + k]] = (uint8_t)((js >> (4 * k)) & 0xf);
+    const uint32_t dec = nb.dec[i * c.LD + slot];
+    nd.sb = dec & 0xf;
+    nd.st = (dec >> 4) & 0xf;
+    const uint32_t js = dec >> 8;
+    const int nk = nd.nkid;
+    for (int k = 0; k < nk; ++k) nb.nd[nd.kid[k]].lay = (uint8_t)((js >> (4 * k)) & 0xf);
 }
 
-// CTA barrier that is correct when a warp arrives diverged (e.g. one lane
-// spinning on a dependency counter while the others wait): the NON-aligned
-// barrier.sync counts threads, whereas __syncthreads (bar.sync, .aligned)
-// requires every warp to arrive converged.
-__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+__device__ __forceinline__ int64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
     int32_t v;
@@ -461,9 +598,97 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
     return v;
 }
 
+// CTA barrier that is correct when a warp arrives diverged (one thread spins
+// on a dependency counter; warps leave a level's node loop at different
+// times): the NON-aligned barrier.sync counts threads, whereas __syncthreads
+// (bar.sync = barrier.sync.aligned) requires converged warps.
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
+// Wait until net `net` has no unfinished predecessor (dataflow mode), with a
+// growing back-off so waiting warps leave the issue slots to working ones.
+__device__ __forceinline__ void wait_ready(const int32_t *wait, int64_t net) {
+    unsigned ns = 32;
+    while (ld_acquire(wait + net) > 0) {
+        __nanosleep(ns);
+        ns = min(ns * 2, 512u);
+    }
+}
+
+__device__ __forceinline__ void trace_end(int64_t *tr) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[3] = gtimer();
+    tr[4] = smid;
+}
+
+// One net, start to finish, by `nthr` threads (one warp for a small net, the
+// CTA for a big net): wait for its predecessors (dataflow mode), gather,
+// leaves, internal nodes level by level (one warp per node), backtrack,
+// decisions and the fused commit, then release its successors.
+template <bool CTA>
+__device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Shared &sh, const DevGrid &G,
+                                        const DevForest &F, const DevScratch &S, const AssignLaunch &a, int64_t net,
+                                        int64_t n0, int q_base, int ns, int tid, int nthr) {
+    auto sync = [] { if (CTA) cta_sync(); else __syncwarp(); };
+    const int nn = c.nn, lane = threadIdx.x & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    const bool flow = a.wait != nullptr;
+    const int pdrv = F.net_pdrv[net];
+    int64_t *tr = a.trace ? a.trace + 5 * net : nullptr;
+    if (tr && tid == 0) tr[0] = gtimer();
+    if (flow) {
+        if (!CTA || tid == 0) wait_ready(a.wait, net);
+        sync();
+    }
+    if (tr && tid == 0) tr[1] = gtimer();
+    gather_nodes(c.nb, F, n0, nn, q_base, ns, tid, nthr);
+    sync();
+    gather_state(c.nb, G, sh, nn, c.LD, tid, nthr);
+    sync();
+    if (tr && tid == 0) tr[2] = gtimer();
+    int lo = 0;
+    while (lo < nn - 1 && c.nb.nd[lo].height == 0) ++lo;
+    leaves_dp(c, sh, G, lo, tid, nthr);
+    sync();
+    while (lo < nn) {
+        const int h = c.nb.nd[lo].height;
+        int hi = lo + 1;
+        while (hi < nn && c.nb.nd[hi].height == h) ++hi;
+        for (int i = lo + warp; i < hi; i += nwarps) node_dp_wide(c, w, sh, G, i, pdrv, lane);
+        if (CTA) cta_sync();
+        lo = hi;
+    }
+    if (tid == 0) {
+        S.froot[net] = *c.nb.froot;
+        c.nb.nd[nn - 1].lay = (uint8_t)pdrv;
+    }
+    sync();
+    // Alg. 4, level-parallel from the root (root entry = driver pin layer, R13)
+    for (int hi = nn; hi > 0;) {
+        const int h = c.nb.nd[hi - 1].height;
+        int l0 = hi - 1;
+        while (l0 > 0 && c.nb.nd[l0 - 1].height == h) --l0;
+        for (int i = l0 + tid; i < hi; i += nthr) backtrack_node(c, sh, i);
+        sync();
+        hi = l0;
+    }
+    for (int i = tid; i < nn; i += nthr) {
+        const NodeRec &nd = c.nb.nd[i];
+        S.lay[n0 + i] = nd.lay;
+        S.sb[n0 + i] = nd.sb;
+        S.st[n0 + i] = nd.st;
+        if (a.commit) commit_node(G, nd.xy, nd.edir, nd.len, nd.lay, nd.sb, nd.st);
+    }
+    if (flow) __threadfence();
+    sync();
+    if (tr && tid == 0) trace_end(tr);
+    if (flow)
+        for (int64_t e = a.succ_off[net] + tid; e < a.succ_off[net + 1]; e += nthr) atomicSub(a.wait + a.succ[e], 1);
+}
+
 // ------------------------------------------------------------------ kernel --
-__global__ void __launch_bounds__(ASSIGN_WARPS * 32, 5) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
+__global__ void __launch_bounds__(ASSIGN_WARPS * 32, 4) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
+    __shared__ int64_t big_item;
     extern __shared__ __align__(16) char dyn[];
     stage_tab(sh.T, G.tab);
     if (threadIdx.x < MAXL) {
@@ -473,167 +698,79 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, 5) k_assign(DevGrid G, DevF
         sh.lidx[l] = (uint8_t)G.lidx[l];
         if (l < G.L) sh.lay_of[G.dir[l]][G.lidx[l]] = (uint8_t)l;
     }
-    if (threadIdx.x == 0) { sh.ndir[0] = G.LH; sh.ndir[1] = G.LV; }
+    if (threadIdx.x == 0) {
+        sh.ndir[0] = G.LH;
+        sh.ndir[1] = G.LV;
+        uint32_t m0 = 0, m1 = 0;
+        for (int l = 0; l < G.L; ++l)
+            if (G.routable[l]) (G.dir[l] == 0 ? m0 : m1) |= 1u << l;
+        sh.legal[0] = m0;
+        sh.legal[1] = m1;
+    }
+    __syncthreads();
     const int L = G.L, LD = a.LD;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const WarpLay wlay = warp_layout(L, LD);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const NetLay slay = net_layout(a.NS, a.NP, L, LD);
-    char *wscr = dyn + warp * wlay.bytes;
-    char *nets = dyn + ASSIGN_WARPS * wlay.bytes;
-    const WarpBuf wb{reinterpret_cast<double *>(wscr + wlay.CP), reinterpret_cast<double *>(wscr + wlay.kap),
-                     reinterpret_cast<uint16_t *>(wscr + wlay.map)};
-    const bool flow = a.wait != nullptr;
+    WarpScr &w = *reinterpret_cast<WarpScr *>(dyn + ASSIGN_WARPS * slay.bytes + warp * SCR_BYTES);
 
-    for (;;) {
-        cta_sync();
-        if (threadIdx.x == 0) {
-            const unsigned long long t = atomicAdd(a.ticket, 1ull);
-            sh.item = (int64_t)t < a.item_end - a.item_beg ? a.item_beg + (int64_t)t : -1;
-        }
-        cta_sync();
-        const int64_t item = sh.item;
-        if (item < 0) return;
-        const uint64_t it = a.items[item];
-        const int64_t net_first = (int64_t)(it & 0xffffffffull);
-        const int cnt = (int)((it >> 32) & 0xff);
-        const bool big = (it >> 40) & 1;
-
-        if (big) {
-            // ======================= big net: the whole CTA =======================
-            const int64_t net = net_first;
+    // hybrid (batch mode: no waits): every CTA first takes big nets, then small ones
+    if (a.hybrid || (int)blockIdx.x < a.n_big_ctas) {
+        // ---------------- big nets: the whole CTA per net ----------------
+        const int64_t n_work = a.big_end - a.big_beg;
+        char *gmine = a.gscratch ? a.gscratch + (int64_t)blockIdx.x * a.gslot_bytes : nullptr;
+        for (;;) {
+            cta_sync();
+            if (threadIdx.x == 0) big_item = (int64_t)atomicAdd(a.ticket + 1, 1ull);
+            cta_sync();
+            const int64_t wk = big_item;
+            if (wk >= n_work) {
+                if (a.hybrid) break;
+                return;
+            }
+            const int64_t net = a.big_pos[a.big_beg + wk];
             const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
             const int nn = (int)(n1 - n0);
-            const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - F.sink0[n0];
-            const NetLay blay = net_layout(nn, ns, L, LD);
-            char *base = blay.bytes <= a.big_smem ? nets : a.gscratch + (int64_t)blockIdx.x * a.gslot_bytes;
-            const NetCtx c{net_buf(base, blay), L, LD, nn};
-            const int pdrv = F.net_pdrv[net];
-            if (flow) {
-                if (threadIdx.x == 0) while (ld_acquire(a.wait + net) > 0) __nanosleep(100);
-                cta_sync();
-                __threadfence();
-            }
-            gather_nodes(c.nb, F, n0, nn, threadIdx.x, blockDim.x);
-            cta_sync();
-            gather_state(c.nb, G, sh, nn, LD, threadIdx.x, blockDim.x);
-            if (threadIdx.x == 0) {
-                int hi = 0;
-                while (hi < nn - 1 && c.nb.height[hi] == 0) ++hi;
-                sh.lo = 0;
-                sh.hi = hi;
-            }
-            cta_sync();
-            leaves_dp(c, sh, G, sh.hi, threadIdx.x, blockDim.x);
-            for (;;) {
-                cta_sync();
-                if (threadIdx.x == 0) {
-                    int lo = sh.hi, hi = lo;
-                    if (lo < nn) {
-                        const int h = c.nb.height[lo];
-                        while (hi < nn && c.nb.height[hi] == h) ++hi;
-                    }
-                    sh.lo = lo;
-                    sh.hi = hi;
-                }
-                cta_sync();
-                const int lo = sh.lo, hi = sh.hi;
-                if (lo >= nn) break;
-                for (int i = lo + warp; i < hi; i += ASSIGN_WARPS) node_dp(c, wb, sh, G, i, i == nn - 1, pdrv, lane);
-            }
-            // Alg. 4, level-parallel from the root (root entry = driver pin layer, R13)
-            if (threadIdx.x == 0) {
-                c.nb.lay[nn - 1] = (uint8_t)pdrv;
-                S.froot[net] = *c.nb.froot;
-                sh.lo = nn;
-            }
-            for (;;) {
-                cta_sync();
-                if (threadIdx.x == 0) {
-                    const int hi = sh.lo;
-                    int lo = hi;
-                    if (hi > 0) {
-                        const int h = c.nb.height[hi - 1];
-                        while (lo > 0 && c.nb.height[lo - 1] == h) --lo;
-                    }
-                    sh.hi = hi;
-                    sh.lo = lo;
-                }
-                cta_sync();
-                const int lo = sh.lo, hi = sh.hi;
-                if (hi <= 0) break;
-                for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) backtrack_node(c, sh, i);
-            }
-            cta_sync();
-            for (int i = threadIdx.x; i < nn; i += blockDim.x) {
-                S.lay[n0 + i] = c.nb.lay[i];
-                S.sb[n0 + i] = c.nb.sb[i];
-                S.st[n0 + i] = c.nb.st[i];
-                if (a.commit) commit_node(G, c.nb.xy[i], c.nb.edir[i], c.nb.len[i], c.nb.lay[i], c.nb.sb[i], c.nb.st[i]);
-            }
-            if (flow) {
-                __threadfence();
-                cta_sync();
-                for (int64_t e = a.succ_off[net] + threadIdx.x; e < a.succ_off[net + 1]; e += blockDim.x)
-                    atomicSub(a.wait + a.succ[e], 1);
-            }
-            continue;
+            const int q_base = F.sink0[n0];
+            const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - q_base;
+            const NetLay lay = net_layout(nn, ns, L, LD);
+            char *base = lay.bytes <= ASSIGN_WARPS * slay.bytes ? dyn : gmine;
+            const NetCtx c{net_buf(base, lay), L, LD, nn};
+            run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, threadIdx.x, blockDim.x);
         }
+    }
 
-        // ========================= small nets: one warp each =========================
-        if (warp >= cnt) continue;
-        const int64_t net = net_first + warp;
+    // ---------------- small nets: one warp per net ----------------
+    char *mine = dyn + warp * slay.bytes;
+    const int64_t n_work = a.small_end - a.small_beg;
+    for (;;) {
+        unsigned long long tk = 0;
+        if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
+        tk = __shfl_sync(FULL_MASK, tk, 0);
+        if ((int64_t)tk >= n_work) return;
+        const int64_t net = a.small_pos[a.small_beg + (int64_t)tk];
         const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
         const int nn = (int)(n1 - n0);
-        const NetCtx c{net_buf(nets + warp * slay.bytes, slay), L, LD, nn};
-        const int pdrv = F.net_pdrv[net];
-        if (flow) {
-            while (ld_acquire(a.wait + net) > 0) __nanosleep(64);
-            __syncwarp();
-        }
-        gather_nodes(c.nb, F, n0, nn, lane, 32);
+        const int q_base = F.sink0[n0];
+        const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - q_base;
+        const NetCtx c{net_buf(mine, slay), L, LD, nn};
+        run_net<false>(c, w, sh, G, F, S, a, net, n0, q_base, ns, lane, 32);
         __syncwarp();
-        gather_state(c.nb, G, sh, nn, LD, lane, 32);
-        __syncwarp();
-        int nleaf = 0;
-        while (nleaf < nn - 1 && c.nb.height[nleaf] == 0) ++nleaf;
-        leaves_dp(c, sh, G, nleaf, lane, 32);
-        __syncwarp();
-        for (int i = nleaf; i < nn; ++i) node_dp(c, wb, sh, G, i, i == nn - 1, pdrv, lane);
-        if (lane == 0) {
-            S.froot[net] = *c.nb.froot;
-            c.nb.lay[nn - 1] = (uint8_t)pdrv;
-        }
-        __syncwarp();
-        int hi = nn;
-        while (hi > 0) {
-            const int h = c.nb.height[hi - 1];
-            int lo = hi - 1;
-            while (lo > 0 && c.nb.height[lo - 1] == h) --lo;
-            for (int i = lo + lane; i < hi; i += 32) backtrack_node(c, sh, i);
-            __syncwarp();
-            hi = lo;
-        }
-        for (int i = lane; i < nn; i += 32) {
-            S.lay[n0 + i] = c.nb.lay[i];
-            S.sb[n0 + i] = c.nb.sb[i];
-            S.st[n0 + i] = c.nb.st[i];
-            if (a.commit) commit_node(G, c.nb.xy[i], c.nb.edir[i], c.nb.len[i], c.nb.lay[i], c.nb.sb[i], c.nb.st[i]);
-        }
-        if (flow) {
-            __threadfence();
-            __syncwarp();
-            for (int64_t e = a.succ_off[net] + lane; e < a.succ_off[net + 1]; e += 32) atomicSub(a.wait + a.succ[e], 1);
-        }
     }
 }
 
 }  // namespace
 
 size_t assign_smem_bytes(int L, int LD, int NS, int NP) {
-    return (size_t)ASSIGN_WARPS * (warp_layout(L, LD).bytes + net_layout(NS, NP, L, LD).bytes);
+    return (size_t)ASSIGN_WARPS * (net_layout(NS, NP, L, LD).bytes + SCR_BYTES);
 }
 
 size_t assign_net_bytes(int nodes, int sinks, int L, int LD) { return (size_t)net_layout(nodes, sinks, L, LD).bytes; }
+
+int assign_nets_per_cta() { return ASSIGN_WARPS; }
+
+size_t assign_cta_net_bytes(int L, int LD, int NS, int NP) {
+    return (size_t)ASSIGN_WARPS * net_layout(NS, NP, L, LD).bytes;
+}
 
 cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm) {
     const size_t smem = assign_smem_bytes(L, LD, NS, NP);
@@ -649,7 +786,7 @@ cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int
 
 cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           cudaStream_t s) {
-    if (a.item_end <= a.item_beg || grid <= 0) return cudaSuccess;
+    if ((a.small_end <= a.small_beg && a.big_end <= a.big_beg) || grid <= 0) return cudaSuccess;
     const size_t smem = assign_smem_bytes(G.L, a.LD, a.NS, a.NP);
     if (a.wait) {
         // dataflow mode: every CTA must be co-resident (nets wait on each other)

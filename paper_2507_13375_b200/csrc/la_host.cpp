@@ -82,24 +82,27 @@ struct la_ctx {
     std::vector<uint8_t> h_edir;
     std::vector<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
-    std::vector<int64_t> batch_item0;         // [n_batches+1] first work item of each batch
-    int64_t n_items = 0;
     int32_t LD = 0;                           // layer slots per direction
     int32_t NS = NS_DEFAULT, NP = NP_DEFAULT; // small-path capacities of k_assign
     int32_t grid = 0;                         // resident k_assign CTAs (persistent grid)
-    int64_t big_smem = 0;                     // shared-memory bytes a big net may use
-    int32_t schedule = LA_SCHED_DATAFLOW;
+    int32_t schedule = LA_SCHED_BATCH;        // measured faster on B200; dataflow on request
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
-    std::vector<uint64_t> h_items;
     bool fuse_commit = true;
-    // work items and the dataflow DAG (device)
-    uint64_t *d_items = nullptr;
+    int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
+    std::vector<int64_t> batch_big0, batch_small0;   // [n_batches+1] per-batch ranges of the role lists
+    int32_t *d_big_pos = nullptr, *d_small_pos = nullptr;           // batch order
+    int32_t *d_flow_big_pos = nullptr, *d_flow_small_pos = nullptr; // dataflow priority order
+    int32_t n_big_ctas = 0;
+    bool hybrid = true;                       // batch-mode launches: all CTAs take big nets first
+    bool tracing = false;
+    // tickets and the dataflow DAG (device)
     unsigned long long *d_ticket = nullptr;   // [n_batches + 1]: [0] dataflow, [1 + b] batch b
     int64_t *d_succ_off = nullptr;
     int32_t *d_succ = nullptr, *d_indeg = nullptr, *d_wait = nullptr;
     char *d_gscratch = nullptr;
     int64_t gslot_bytes = 0;
     std::vector<int32_t> batch_of_net;        // input order
+    std::vector<int32_t> h_big_pos, h_small_pos;
     DevForest F{};
     DevScratch S{};
     std::vector<void *> dev_allocs;           // forest + scratch
@@ -123,7 +126,7 @@ struct la_ctx {
     ~la_ctx() {
         for (void *p : dev_allocs) cudaFree(p);
         void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab,
-                      d_items, d_ticket, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
+                      d_ticket, d_trace, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
         for (void *p : gp) if (p) cudaFree(p);
         if (comm) ncclCommDestroy(comm);
         for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -736,7 +739,16 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         int64_t i = net - ch.beg;
         return ch.sink_off[i + 1] - ch.sink_off[i];
     };
-    // nets whose whole DP state fits a warp's shared memory take the warp path
+    // nets whose whole DP state fits a group's shared-memory slot (SLOT_BYTES) stay
+    // on chip; the slot's node capacity NS follows from the layer count
+    ctx->LD = std::max(ctx->LH, ctx->LV);
+    {
+        int64_t budget = SLOT_BYTES;
+        if (const char *e = getenv("GAPLA_SLOT_BYTES")) budget = std::max(512, atoi(e));
+        int ns = 1;
+        while (assign_net_bytes(ns + 1, ctx->NP, ctx->L, ctx->LD) <= (size_t)budget) ns++;
+        ctx->NS = ns;
+    }
     if (const char *e = getenv("GAPLA_NS")) ctx->NS = std::max(1, std::min(1024, atoi(e)));   // tuning knobs
     if (const char *e = getenv("GAPLA_NP")) ctx->NP = std::max(1, std::min(4096, atoi(e)));
     auto is_big = [&](int64_t net) { return nnodes_of(net) > ctx->NS || nsinks_of(net) > ctx->NP; };
@@ -819,30 +831,28 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                                  return nnodes_of(a) > nnodes_of(c);
                              });
     }
-    // work items: per batch, each big net alone, then runs of up to
-    // ASSIGN_WARPS small nets; the largest big net sizes the global big-net slot
-    std::vector<uint64_t> items;
-    ctx->batch_item0.assign(1, 0);
+    // role lists: big nets (CTA path) and small nets (group path), both in
+    // forest = topological order; per batch the big nets are its leading positions
     int64_t max_big_nodes = 0, max_big_sinks = 0;
+    std::vector<int32_t> big_pos, small_pos;
+    big_pos.reserve(N / 16 + 1);
+    small_pos.reserve(N);
+    ctx->batch_big0.assign(1, 0);
+    ctx->batch_small0.assign(1, 0);
     for (int32_t b = 0; b < nb; b++) {
-        int64_t k = ctx->batch_net0[b];
-        const int64_t kend = ctx->batch_net0[b + 1];
-        while (k < kend) {
-            if (is_big(pos_net[k])) {
-                max_big_nodes = std::max(max_big_nodes, nnodes_of(pos_net[k]));
-                max_big_sinks = std::max(max_big_sinks, nsinks_of(pos_net[k]));
-                items.push_back((uint64_t)k | (1ull << 32) | (1ull << 40));
-                k++;
-                continue;
+        for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++) {
+            const int64_t net = pos_net[p];
+            if (is_big(net)) {
+                big_pos.push_back((int32_t)p);
+                max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
+                max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
+            } else {
+                small_pos.push_back((int32_t)p);
             }
-            int64_t c = 0;
-            while (k + c < kend && c < ASSIGN_WARPS && !is_big(pos_net[k + c])) c++;
-            items.push_back((uint64_t)k | ((uint64_t)c << 32));
-            k += c;
         }
-        ctx->batch_item0.push_back((int64_t)items.size());
+        ctx->batch_big0.push_back((int64_t)big_pos.size());
+        ctx->batch_small0.push_back((int64_t)small_pos.size());
     }
-    ctx->n_items = (int64_t)items.size();
     // dataflow DAG in forest order
     {
         std::vector<int64_t> rank_of_net(N), rank_of_pos(N);
@@ -852,6 +862,35 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                                              ctx->stream, &ctx->stats.launches);
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "dependency DAG"); }
         ctx->stats.h2d_bytes += 8 * N;
+    }
+    // dataflow priority: nets are taken in descending weighted bottom level
+    // (longest chain of dependent work still ahead of the net; weight ~ its latency), ties
+    // by position.  Bottom levels strictly decrease along DAG edges, so the order is
+    // topological; critical chains start first instead of waiting for their batch.
+    std::vector<int32_t> flow_big, flow_small;
+    {
+        std::vector<int64_t> off(N + 1, 0);
+        if (N) CK(cudaMemcpyAsync(off.data(), ctx->d_succ_off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        std::vector<int32_t> succ((size_t)std::max<int64_t>(off[N], 1));
+        if (off[N]) CK(cudaMemcpyAsync(succ.data(), ctx->d_succ, sizeof(int32_t) * off[N], cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->stats.d2h_bytes += 8 * (N + 1) + 4 * off[N];
+        std::vector<int64_t> bl(N);
+        for (int64_t p = N - 1; p >= 0; p--) {
+            const int64_t net = pos_net[p];
+            const int64_t nn = nnodes_of(net);
+            int64_t m = 0;
+            for (int64_t e = off[p]; e < off[p + 1]; e++) m = std::max(m, bl[succ[e]]);   // succ positions > p
+            bl[p] = m + 8 + (is_big(net) ? nn / 4 : nn);
+        }
+        auto by_prio = [&](int32_t a, int32_t c) { return bl[a] != bl[c] ? bl[a] > bl[c] : a < c; };
+        flow_big = big_pos;
+        flow_small = small_pos;
+        std::sort(flow_big.begin(), flow_big.end(), by_prio);
+        std::sort(flow_small.begin(), flow_small.end(), by_prio);
     }
     // offsets in final order
     std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
@@ -921,7 +960,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     chunks.clear();
     chunks.shrink_to_fit();
 
-    ctx->LD = std::max(ctx->LH, ctx->LV);
 
     // ---- upload forest, allocate scratch
     DevForest &F = ctx->F;
@@ -948,28 +986,37 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
     TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
     if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
-    // persistent k_assign grid, work items, tickets, dataflow counters, big-net slots
+    // persistent k_assign grid, tickets, dataflow counters, big-net slots
     {
         int per_sm = 0, n_sm = 0;
         CK(assign_resident_ctas(ctx->L, ctx->LD, ctx->NS, ctx->NP, &per_sm, &n_sm));
         if (per_sm < 1) return set_err(LA_ECUDA, "k_assign does not fit on an SM");
         ctx->grid = per_sm * n_sm;
-        TRY(dev_upload(ctx, &ctx->d_items, items.data(), items.size()));
-        ctx->h_items = items;
-        ctx->dev_allocs.pop_back();   // owned by the ctx field, freed in ~la_ctx
-        CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned long long) * (nb + 1)));
-        CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * (nb + 1), ctx->stream));
+        CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned long long) * 2 * (nb + 1)));
+        CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
+        ctx->h_big_pos = big_pos;
+        ctx->h_small_pos = small_pos;
+        big_pos.push_back(0);     // never empty on the device
+        small_pos.push_back(0);
+        TRY(dev_upload(ctx, &ctx->d_big_pos, big_pos.data(), big_pos.size()));
+        TRY(dev_upload(ctx, &ctx->d_small_pos, small_pos.data(), small_pos.size()));
+        flow_big.push_back(0);
+        flow_small.push_back(0);
+        TRY(dev_upload(ctx, &ctx->d_flow_big_pos, flow_big.data(), flow_big.size()));
+        TRY(dev_upload(ctx, &ctx->d_flow_small_pos, flow_small.data(), flow_small.size()));
+        // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
+        ctx->n_big_ctas = big_pos.empty() ? 0 : n_sm;
+        if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
+        if (!big_pos.empty()) ctx->n_big_ctas = std::max(1, std::min(ctx->n_big_ctas, ctx->grid - 1));
+        if (const char *e = getenv("GAPLA_HYBRID")) ctx->hybrid = atoi(e) != 0;
         CK(cudaMalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
         if (N) CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
-        // a big net runs out of the CTA's four small-net buffers when it fits there
-        size_t small = (size_t)ASSIGN_WARPS * assign_net_bytes(ctx->NS, ctx->NP, ctx->L, ctx->LD);
-        if (const char *e = getenv("GAPLA_BIG_SMEM")) small = std::min<size_t>(small, (size_t)atoll(e));
-        ctx->big_smem = (int64_t)small;
+        // a big net keeps its DP state in its CTA's shared memory, or in a per-CTA global slot
         const size_t need = assign_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD);
         ctx->gslot_bytes = 0;
-        if (max_big_nodes > 0 && need > small) {
+        if (max_big_nodes > 0 && need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP)) {
             ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
-            CK(cudaMalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));
+            CK(cudaMalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));   // hybrid: any CTA
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
@@ -1008,25 +1055,49 @@ static la_status check_ready(la_ctx *ctx) {
     return LA_OK;
 }
 
-// This rank's share of batch k: a contiguous range of the batch's work items.
-static void rank_items(const la_ctx *ctx, int32_t batch, int64_t *i0, int64_t *i1) {
-    const int64_t b0 = ctx->batch_item0[batch], b1 = ctx->batch_item0[batch + 1];
+// This rank's share of batch k: contiguous ranges of the batch's big and small
+// nets (role-list indices; their forest positions are contiguous as well).
+struct RankShare { int64_t big_beg, big_end, small_beg, small_end; };
+static RankShare rank_share(const la_ctx *ctx, int32_t batch) {
+    RankShare r;
     int64_t s0, s1;
-    la_shard_range(b1 - b0, ctx->world, ctx->rank, &s0, &s1);
-    *i0 = b0 + s0;
-    *i1 = b0 + s1;
+    const int64_t g0 = ctx->batch_big0[batch], g1 = ctx->batch_big0[batch + 1];
+    la_shard_range(g1 - g0, ctx->world, ctx->rank, &s0, &s1);
+    r.big_beg = g0 + s0;
+    r.big_end = g0 + s1;
+    const int64_t m0 = ctx->batch_small0[batch], m1 = ctx->batch_small0[batch + 1];
+    la_shard_range(m1 - m0, ctx->world, ctx->rank, &s0, &s1);
+    r.small_beg = m0 + s0;
+    r.small_end = m0 + s1;
+    return r;
+}
+
+// Grid of one launch: the big-role CTAs it needs, then the small-role CTAs.
+static int launch_grid(const la_ctx *ctx, AssignLaunch &al) {
+    const int64_t nbig = al.big_end - al.big_beg, nsmall = al.small_end - al.small_beg;
+    const int npc = assign_nets_per_cta();
+    if (!al.wait && ctx->hybrid) {   // batch mode: every CTA takes the batch's big nets first
+        al.hybrid = 1;
+        al.n_big_ctas = 0;
+        return (int)std::min<int64_t>(ctx->grid, std::max<int64_t>(nbig, (nsmall + npc - 1) / npc));
+    }
+    al.hybrid = 0;
+    al.n_big_ctas = (int32_t)std::min<int64_t>(ctx->n_big_ctas, nbig);
+    const int64_t small_ctas = std::min<int64_t>(ctx->grid - ctx->n_big_ctas, (nsmall + npc - 1) / npc);
+    return al.n_big_ctas + (int)small_ctas;
 }
 
 static AssignLaunch assign_launch(const la_ctx *ctx) {
     AssignLaunch al{};
-    al.items = ctx->d_items;
+    al.big_pos = ctx->d_big_pos;
+    al.small_pos = ctx->d_small_pos;
     al.gscratch = ctx->d_gscratch;
     al.gslot_bytes = ctx->gslot_bytes;
     al.NS = ctx->NS;
     al.NP = ctx->NP;
-    al.big_smem = ctx->big_smem;
     al.LD = ctx->LD;
     al.commit = (ctx->world == 1 && ctx->fuse_commit) ? 1 : 0;
+    al.trace = ctx->tracing ? ctx->d_trace : nullptr;
     return al;
 }
 
@@ -1040,9 +1111,10 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
     AssignLaunch al = assign_launch(ctx);
-    rank_items(ctx, batch, &al.item_beg, &al.item_end);
-    al.ticket = ctx->d_ticket + 1 + batch;
-    const int grid = (int)std::min<int64_t>(ctx->grid, al.item_end - al.item_beg);
+    const RankShare r = rank_share(ctx, batch);
+    al.big_beg = r.big_beg; al.big_end = r.big_end; al.small_beg = r.small_beg; al.small_end = r.small_end;
+    al.ticket = ctx->d_ticket + 2 * (1 + batch);
+    const int grid = launch_grid(ctx, al);
     int pi = prof_begin(ctx, K_ASSIGN);
     CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
     prof_end(ctx, pi);
@@ -1059,16 +1131,17 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
     if (ctx->world > 1) {
         // reconcile: every rank contributes its shard's packed decisions (others 0) -> sum
-        int64_t i0, i1;
-        rank_items(ctx, batch, &i0, &i1);
-        const int64_t e0 = i0 < i1 ? (int64_t)(ctx->h_items[i0] & 0xffffffffull) : b0;
-        const int64_t e1 = i0 < i1 ? (int64_t)(ctx->h_items[i1 - 1] & 0xffffffffull) +
-                                         (int64_t)((ctx->h_items[i1 - 1] >> 32) & 0xff)
-                                   : b0;
-        const int64_t m0 = ctx->h_net_node0[e0], m1 = ctx->h_net_node0[e1];
+        const RankShare r = rank_share(ctx, batch);
         int pr = prof_begin(ctx, K_RECONCILE);
         CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
-        CK(launch_pack_decisions(ctx->S, m0, m1, ctx->stream));
+        // the shard's big nets and small nets are two contiguous position ranges
+        const int64_t ranges[2][2] = {{r.big_beg, r.big_end}, {r.small_beg, r.small_end}};
+        for (int k = 0; k < 2; k++) {
+            if (ranges[k][1] <= ranges[k][0]) continue;
+            const int64_t p0 = k == 0 ? ctx->h_big_pos[ranges[k][0]] : ctx->h_small_pos[ranges[k][0]];
+            const int64_t p1 = (k == 0 ? ctx->h_big_pos[ranges[k][1] - 1] : ctx->h_small_pos[ranges[k][1] - 1]) + 1;
+            CK(launch_pack_decisions(ctx->S, ctx->h_net_node0[p0], ctx->h_net_node0[p1], ctx->stream));
+        }
         NK(ncclAllReduce(ctx->S.dec + n0, ctx->S.dec + n0, (size_t)(n1 - n0), ncclUint32, ncclSum, ctx->comm,
                          ctx->stream));
         NK(ncclAllReduce(ctx->S.froot + b0, ctx->S.froot + b0, (size_t)(b1 - b0), ncclFloat64, ncclSum, ctx->comm,
@@ -1095,13 +1168,17 @@ la_status la_assign_all(la_ctx *ctx) {
         ctx->next_batch == 0 && !ctx->flow_dirty) {
         // one persistent launch over every work item, nets ordered by the dependency DAG
         AssignLaunch al = assign_launch(ctx);
-        al.item_beg = 0;
-        al.item_end = ctx->n_items;
+        al.big_pos = ctx->d_flow_big_pos;
+        al.small_pos = ctx->d_flow_small_pos;
+        al.big_beg = 0;
+        al.big_end = (int64_t)ctx->h_big_pos.size();
+        al.small_beg = 0;
+        al.small_end = (int64_t)ctx->h_small_pos.size();
         al.ticket = ctx->d_ticket;
         al.wait = ctx->d_wait;
         al.succ_off = ctx->d_succ_off;
         al.succ = ctx->d_succ;
-        const int grid = (int)std::min<int64_t>(ctx->grid, ctx->n_items);
+        const int grid = launch_grid(ctx, al);
         int pi = prof_begin(ctx, K_ASSIGN);
         CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
         prof_end(ctx, pi);
@@ -1255,7 +1332,7 @@ la_status la_reset(la_ctx *ctx) {
     CK(cudaMemcpyAsync(ctx->d_wV, ctx->d_wV0, bV, cudaMemcpyDeviceToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->d_via, ctx->d_via0, bVia, cudaMemcpyDeviceToDevice, ctx->stream));
     const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
-    CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * (nb + 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
     if (ctx->n_nets)
         CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * ctx->n_nets, cudaMemcpyDeviceToDevice,
                            ctx->stream));
@@ -1296,6 +1373,28 @@ la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset) {
     ctx->spans.clear();
     *out = ctx->acc;
     if (reset) ctx->acc = la_profile{};
+    return LA_OK;
+}
+
+la_status la_set_tracing(la_ctx *ctx, int32_t enable) {
+    TRY(check_ready(ctx));
+    if (enable && !ctx->d_trace) {
+        CK(cudaMalloc(&ctx->d_trace, sizeof(int64_t) * 5 * std::max<int64_t>(ctx->n_nets, 1)));
+        CK(cudaMemsetAsync(ctx->d_trace, 0, sizeof(int64_t) * 5 * std::max<int64_t>(ctx->n_nets, 1), ctx->stream));
+    }
+    ctx->tracing = enable != 0;
+    return LA_OK;
+}
+
+la_status la_get_trace(la_ctx *ctx, int64_t *out) {
+    TRY(check_ready(ctx));
+    if (!out) return set_err(LA_EINVAL, "null argument");
+    if (!ctx->d_trace) return set_err(LA_ESTATE, "tracing was never enabled");
+    std::vector<int64_t> t((size_t)5 * ctx->n_nets);
+    CK(cudaMemcpyAsync(t.data(), ctx->d_trace, sizeof(int64_t) * t.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int64_t p = 0; p < ctx->n_nets; p++)
+        for (int k = 0; k < 5; k++) out[ctx->h_net_id[p] * 5 + k] = t[p * 5 + k];
     return LA_OK;
 }
 

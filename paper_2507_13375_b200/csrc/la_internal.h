@@ -60,11 +60,12 @@ struct DevForest {
     const uint8_t *net_pdrv;                  // driver pin layer
 };
 
-// Default capacities of the warp-per-net (small) path of k_assign: a net whose LA
-// tree has at most NS nodes and at most NP sinks keeps all its DP state in its
-// warp's shared memory; larger nets take the CTA-per-net (big) path.
-constexpr int NS_DEFAULT = 32;
-constexpr int NP_DEFAULT = 64;
+// Default capacities of k_assign's shared-memory net slot: a net whose LA tree has
+// at most NS nodes and at most NP sinks is "small" and keeps all its DP state in
+// its warp's slot; a larger ("big") net is run by a whole CTA.
+constexpr int NS_DEFAULT = 28;              // replaced at load time by the SLOT_BYTES fit
+constexpr int NP_DEFAULT = 48;
+constexpr int SLOT_BYTES = 9216;            // shared memory per warp's net slot (4 warps per CTA, 4 CTAs per SM)
 constexpr int ASSIGN_WARPS = 4;
 
 struct DevScratch {
@@ -80,24 +81,31 @@ cudaError_t launch_pack_state(const DevGrid &G, const int32_t *wcap, const int32
                               const int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
 cudaError_t launch_unpack_demand(const DevGrid &G, const int32_t *wcap, const int32_t *vcap, int32_t *wdem,
                                  int32_t *vdem, const int64_t *wire_off, cudaStream_t s);
-// One k_assign launch.  Items (batch-major): bits 0-31 first net, 32-39 net
-// count, bit 40 big (the CTA runs one net).  wait == nullptr: batch mode.
+// One k_assign launch.  Nets are named by forest position through two lists in
+// topological (forest) order: big nets (more than NS nodes or NP sinks), run by
+// the first n_big_ctas CTAs, one whole CTA per net, and small nets, run by the
+// other CTAs, one 8-lane group per net.  wait == nullptr: batch mode.
 struct AssignLaunch {
-    const uint64_t *items;
-    int64_t item_beg, item_end;               // items of this launch
-    unsigned long long *ticket;               // zeroed before the launch
+    const int32_t *big_pos, *small_pos;       // forest positions
+    int64_t big_beg, big_end;                 // this launch's range of big_pos
+    int64_t small_beg, small_end;             // this launch's range of small_pos
+    int32_t n_big_ctas;                       // CTAs [0, n_big_ctas) take big nets
+    int32_t hybrid;                           // batch mode: every CTA takes big nets first, then small
+    unsigned long long *ticket;               // [0] small, [1] big; zeroed before the launch
     int32_t *wait;                            // dataflow mode: unfinished predecessors per net
     const int64_t *succ_off;                  // [n_nets+1] successor CSR (forest order)
     const int32_t *succ;
-    char *gscratch;                           // big nets that do not fit shared memory:
-    int64_t gslot_bytes;                      //   one slot per CTA
-    int32_t NS, NP;                           // small-path capacities
-    int64_t big_smem;                         // bytes of shared memory a big net may use (else gscratch)
+    char *gscratch;                           // big nets that do not fit a CTA's shared memory:
+    int64_t gslot_bytes;                      //   one global slot per big CTA
+    int32_t NS, NP;                           // shared-memory slot capacities of a small net
     int32_t LD;                               // max(#H layers, #V layers): layer slots per direction
     int32_t commit;                           // fuse the demand commit (K8) into the kernel
+    int64_t *trace;                           // diagnostics: [n_nets][5] per-net timestamps, or nullptr
 };
 size_t assign_smem_bytes(int L, int LD, int NS, int NP);
 size_t assign_net_bytes(int nodes, int sinks, int L, int LD);
+int assign_nets_per_cta();
+size_t assign_cta_net_bytes(int L, int LD, int NS, int NP);   // shared memory a big net may use
 cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm);
 cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           cudaStream_t s);

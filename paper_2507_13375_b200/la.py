@@ -81,6 +81,8 @@ def _load():
         "la_commit_demand": ([c_void_p, c_i32], c_i32),
         "la_assign_all": ([c_void_p], c_i32),
         "la_set_schedule": ([c_void_p, c_i32], c_i32),
+        "la_set_tracing": ([c_void_p, c_i32], c_i32),
+        "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
         "la_get_demand": ([c_void_p, P(c_i32), P(c_i32)], c_i32),
@@ -106,7 +108,7 @@ _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
-           "la_set_schedule")
+           "la_set_schedule", "la_set_tracing", "la_get_trace")
 
 
 def _check(st):
@@ -173,6 +175,16 @@ LA_SCHED_DATAFLOW, LA_SCHED_BATCH = 0, 1
 
 def la_set_schedule(ctx, schedule: int):
     _check(_lib.la_set_schedule(ctx, int(schedule)))
+
+
+def la_set_tracing(ctx, enable: bool):
+    _check(_lib.la_set_tracing(ctx, 1 if enable else 0))
+
+
+def la_get_trace(ctx, n_nets: int):
+    out = np.zeros((n_nets, 5), np.int64)
+    _check(_lib.la_get_trace(ctx, out.ctypes.data_as(P(c_i64))))
+    return out
 
 
 def la_reset(ctx):

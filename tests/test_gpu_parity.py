@@ -115,11 +115,13 @@ def test_dataflow_equals_batch_schedule(la, cfg, n):
         assert np.array_equal(a[k], b[k]), k
 
 
-def test_dense_conflicts_deep_dag(la):
+@pytest.mark.parametrize("sched", ["dataflow", "batch"])
+def test_dense_conflicts_deep_dag(la, sched):
     """20K nets on a 24x24 grid: long conflict chains (hundreds of batches), so the
-    dataflow schedule's waits and releases are exercised on every net."""
+    dataflow schedule's waits and releases are exercised on every net, and the
+    batch schedule launches hundreds of mostly tiny batches."""
     d = synth.generate(20_000, 24, 24, 6, seed=77, pin_max=16, rdrv_mode=1, name="dense")
-    got = run_gpu(la, d)
+    got = run_gpu(la, d, schedule=la.LA_SCHED_DATAFLOW if sched == "dataflow" else la.LA_SCHED_BATCH)
     ref = oracle.run(d)
     assert got["n_batches"] > 200
     assert_parity(got, ref, bitwise_fp=True)
