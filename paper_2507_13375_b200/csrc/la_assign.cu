@@ -686,7 +686,7 @@ __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Share
 }
 
 // ------------------------------------------------------------------ kernel --
-__global__ void __launch_bounds__(ASSIGN_WARPS * 32, 4) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
+__global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
     __shared__ int64_t big_item;
     extern __shared__ __align__(16) char dyn[];
