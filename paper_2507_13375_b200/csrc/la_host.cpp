@@ -47,6 +47,20 @@ const int OPP[4] = {DIR_W, DIR_E, DIR_S, DIR_N};
 
 }  // namespace
 
+namespace gapla {
+// Host staging vectors without the serial zero-fill of value-initialisation.
+template <class T>
+struct default_init_alloc : std::allocator<T> {
+    template <class U> struct rebind { using other = default_init_alloc<U>; };
+    using std::allocator<T>::allocator;
+    template <class U> void construct(U *p) { ::new ((void *)p) U; }
+    template <class U, class... A> void construct(U *p, A &&...a) { ::new ((void *)p) U(std::forward<A>(a)...); }
+};
+template <class T> using hvec = std::vector<T, default_init_alloc<T>>;
+
+}  // namespace gapla
+using gapla::hvec;
+
 struct la_ctx {
     int device = 0, rank = 0, world = 1;
     cudaStream_t stream = nullptr;
@@ -77,9 +91,9 @@ struct la_ctx {
 
     // forest (host copies needed for outputs)
     int64_t n_nets = 0, n_pins = 0, n_nodes = 0, n_sinks = 0;
-    std::vector<uint32_t> h_xy;
-    std::vector<int32_t> h_len;
-    std::vector<uint8_t> h_edir;
+    hvec<uint32_t> h_xy;
+    hvec<int32_t> h_len;
+    hvec<uint8_t> h_edir;
     std::vector<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
     int32_t LD = 0;                           // layer slots per direction
@@ -199,6 +213,47 @@ la_status dev_alloc(la_ctx *ctx, T **dst, size_t n) {
         la_status s_ = (x);             \
         if (s_ != LA_OK) return s_;     \
     } while (0)
+
+// Run f(i) for i in [0, n) on up to nthr threads (contiguous blocks).
+template <class F>
+void par_for(int64_t n, unsigned nthr, F f) {
+    if (n <= 0) return;
+    nthr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nthr, n / 2048 + 1));
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nthr; t++)
+        th.emplace_back([&, t] { for (int64_t i = n * t / nthr; i < n * (t + 1) / nthr; i++) f(i); });
+    for (int64_t i = 0; i < n / nthr; i++) f(i);
+    for (auto &x : th) x.join();
+}
+
+// Sort v by cmp on nthr threads: sorted blocks, then pairwise merges in parallel.
+template <class T, class C>
+void par_sort(std::vector<T> &v, C cmp, unsigned nthr) {
+    const int64_t n = (int64_t)v.size();
+    unsigned k = 1;
+    while (k * 2 <= nthr && n / (k * 2) >= 65536) k *= 2;
+    if (k == 1) { std::sort(v.begin(), v.end(), cmp); return; }
+    std::vector<int64_t> b(k + 1);
+    for (unsigned i = 0; i <= k; i++) b[i] = n * i / k;
+    {
+        std::vector<std::thread> th;
+        for (unsigned i = 0; i < k; i++) th.emplace_back([&, i] { std::sort(v.begin() + b[i], v.begin() + b[i + 1], cmp); });
+        for (auto &x : th) x.join();
+    }
+    std::vector<T> tmp(n);
+    std::vector<T> *src = &v, *dst = &tmp;
+    for (unsigned w = 1; w < k; w *= 2) {
+        std::vector<std::thread> th;
+        for (unsigned i = 0; i < k; i += 2 * w)
+            th.emplace_back([&, i, w] {
+                const int64_t a = b[i], m = b[std::min(k, i + w)], e = b[std::min(k, i + 2 * w)];
+                std::merge(src->begin() + a, src->begin() + m, src->begin() + m, src->begin() + e, dst->begin() + a, cmp);
+            });
+        for (auto &x : th) x.join();
+        std::swap(src, dst);
+    }
+    if (src != &v) v.swap(*src);
+}
 
 bool ok_nonneg(const double *a, int n) {
     for (int i = 0; i < n; i++)
@@ -673,6 +728,14 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (n->n_nets >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "too many nets");
     CK(cudaSetDevice(ctx->device));
     auto t0 = std::chrono::steady_clock::now();
+    const bool verbose = getenv("GAPLA_VERBOSE") != nullptr;   // phase times of la_load_nets to stderr
+    auto tph = t0;
+    auto phase = [&](const char *what) {
+        if (!verbose) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[gapla load] %-28s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tph).count());
+        tph = t;
+    };
     const int64_t N = n->n_nets;
     ctx->n_nets = N;
     ctx->n_pins = N > 0 ? n->pin_ptr[N] : 0;
@@ -725,20 +788,19 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     for (auto &ch : chunks)
         if (ch.err_net >= 0) return set_err(LA_EINVAL, ch.err);
 
-    // per-net index: chunk and local position
+    // per-net index: chunk and local position; flat per-net node and sink counts
     std::vector<int32_t> chunk_of(N);
     for (int64_t c = 0; c < nchunks; c++)
         for (int64_t i = chunks[c].beg; i < chunks[c].end; i++) chunk_of[i] = (int32_t)c;
-    auto nnodes_of = [&](int64_t net) {
+    std::vector<int32_t> nn_of(N), ns_of(N);
+    par_for(N, nthr, [&](int64_t net) {
         const Chunk &ch = chunks[chunk_of[net]];
-        int64_t i = net - ch.beg;
-        return ch.node_off[i + 1] - ch.node_off[i];
-    };
-    auto nsinks_of = [&](int64_t net) {
-        const Chunk &ch = chunks[chunk_of[net]];
-        int64_t i = net - ch.beg;
-        return ch.sink_off[i + 1] - ch.sink_off[i];
-    };
+        const int64_t i = net - ch.beg;
+        nn_of[net] = (int32_t)std::min<int64_t>(ch.node_off[i + 1] - ch.node_off[i], INT32_MAX);
+        ns_of[net] = (int32_t)std::min<int64_t>(ch.sink_off[i + 1] - ch.sink_off[i], INT32_MAX);
+    });
+    auto nnodes_of = [&](int64_t net) { return (int64_t)nn_of[net]; };
+    auto nsinks_of = [&](int64_t net) { return (int64_t)ns_of[net]; };
     // nets whose whole DP state fits a group's shared-memory slot (SLOT_BYTES) stay
     // on chip; the slot's node capacity NS follows from the layer count
     ctx->LD = std::max(ctx->LH, ctx->LV);
@@ -756,12 +818,14 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (nnodes_of(net) >= 65535 || nsinks_of(net) >= 65535)
             return set_err(LA_EINVAL, "net " + std::to_string(net) + ": more than 65534 LA-tree nodes or sinks");
 
+    phase("tree build");
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
     for (int64_t i = 0; i < N; i++) by_rank[i] = i;
-    if (n->order_key)
-        std::stable_sort(by_rank.begin(), by_rank.end(),
-                         [&](int64_t a, int64_t b) { return n->order_key[a] < n->order_key[b]; });
+    if (n->order_key) {
+        const int64_t *ok = n->order_key;
+        par_sort(by_rank, [ok](int64_t a, int64_t b) { return ok[a] != ok[b] ? ok[a] < ok[b] : a < b; }, nthr);
+    }
     std::vector<int64_t> fp_pos(N + 1, 0);
     for (int64_t r = 0; r < N; r++) {
         int64_t net = by_rank[r];
@@ -796,6 +860,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     while (((uint64_t)1 << elem_bits) < (uint64_t)3 * ctx->X * ctx->Y) elem_bits++;
     auto t1 = std::chrono::steady_clock::now();
 
+    phase("priority order + keys");
     // ---- GPU conflict-free batching (K1/K2)
     std::vector<int32_t> batch_of_rank;
     int32_t nb = 0;
@@ -810,6 +875,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     ctx->batch_of_net.assign(N, 0);
     for (int64_t r = 0; r < N; r++) ctx->batch_of_net[by_rank[r]] = batch_of_rank[r];
 
+    phase("GPU batching");
     // ---- batch-major net order: by batch, then node count descending, then rank
     std::vector<int64_t> pos_net(N);   // final position -> input net
     {
@@ -822,15 +888,32 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             int64_t net = by_rank[r];
             pos_net[cur[ctx->batch_of_net[net]]++] = net;
         }
-        // big nets (CTA path) first, then by node count descending: the longest nets start first
-        for (int32_t b = 0; b < nb; b++)
-            std::stable_sort(pos_net.begin() + ctx->batch_net0[b], pos_net.begin() + ctx->batch_net0[b + 1],
-                             [&](int64_t a, int64_t c) {
-                                 const bool ba = is_big(a), bc = is_big(c);
-                                 if (ba != bc) return ba;
-                                 return nnodes_of(a) > nnodes_of(c);
-                             });
+        // big nets (CTA path) first, then by node count descending, then rank: the longest nets
+        // start first.  Key per position: !big | (65535 - nodes) | offset in the batch (rank order).
+        std::atomic<int32_t> nxt{0};
+        auto sorter = [&]() {
+            std::vector<uint64_t> kk;
+            for (;;) {
+                const int32_t b = nxt.fetch_add(1);
+                if (b >= nb) break;
+                const int64_t p0 = ctx->batch_net0[b], p1 = ctx->batch_net0[b + 1];
+                kk.resize(p1 - p0);
+                for (int64_t p = p0; p < p1; p++) {
+                    const int64_t net = pos_net[p];
+                    kk[p - p0] = ((uint64_t)(is_big(net) ? 0 : 1) << 63) | ((uint64_t)(65535 - nn_of[net]) << 40) |
+                                 (uint64_t)(p - p0);
+                }
+                std::sort(kk.begin(), kk.end());
+                std::vector<int64_t> tmp(pos_net.begin() + p0, pos_net.begin() + p1);
+                for (int64_t q = 0; q < p1 - p0; q++) pos_net[p0 + q] = tmp[kk[q] & ((1ull << 40) - 1)];
+            }
+        };
+        std::vector<std::thread> th;
+        for (unsigned i = 1; i < nthr; i++) th.emplace_back(sorter);
+        sorter();
+        for (auto &t : th) t.join();
     }
+    phase("batch-major order");
     // role lists: big nets (CTA path) and small nets (group path), both in
     // forest = topological order; per batch the big nets are its leading positions
     int64_t max_big_nodes = 0, max_big_sinks = 0;
@@ -853,6 +936,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->batch_big0.push_back((int64_t)big_pos.size());
         ctx->batch_small0.push_back((int64_t)small_pos.size());
     }
+    phase("role lists");
     // dataflow DAG in forest order
     {
         std::vector<int64_t> rank_of_net(N), rank_of_pos(N);
@@ -863,59 +947,31 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "dependency DAG"); }
         ctx->stats.h2d_bytes += 8 * N;
     }
-    // dataflow priority: nets are taken in descending weighted bottom level
-    // (longest chain of dependent work still ahead of the net; weight ~ its latency), ties
-    // by position.  Bottom levels strictly decrease along DAG edges, so the order is
-    // topological; critical chains start first instead of waiting for their batch.
-    std::vector<int32_t> flow_big, flow_small;
-    {
-        std::vector<int64_t> off(N + 1, 0);
-        if (N) CK(cudaMemcpyAsync(off.data(), ctx->d_succ_off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost,
-                                  ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        std::vector<int32_t> succ((size_t)std::max<int64_t>(off[N], 1));
-        if (off[N]) CK(cudaMemcpyAsync(succ.data(), ctx->d_succ, sizeof(int32_t) * off[N], cudaMemcpyDeviceToHost,
-                                       ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        ctx->stats.d2h_bytes += 8 * (N + 1) + 4 * off[N];
-        std::vector<int64_t> bl(N);
-        for (int64_t p = N - 1; p >= 0; p--) {
-            const int64_t net = pos_net[p];
-            const int64_t nn = nnodes_of(net);
-            int64_t m = 0;
-            for (int64_t e = off[p]; e < off[p + 1]; e++) m = std::max(m, bl[succ[e]]);   // succ positions > p
-            bl[p] = m + 8 + (is_big(net) ? nn / 4 : nn);
-        }
-        auto by_prio = [&](int32_t a, int32_t c) { return bl[a] != bl[c] ? bl[a] > bl[c] : a < c; };
-        flow_big = big_pos;
-        flow_small = small_pos;
-        std::sort(flow_big.begin(), flow_big.end(), by_prio);
-        std::sort(flow_small.begin(), flow_small.end(), by_prio);
-    }
+    phase("DAG to positions");
     // offsets in final order
     std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
     int64_t max_nodes = 0;
     for (int64_t p = 0; p < N; p++) {
-        int64_t net = pos_net[p];
-        const Chunk &ch = chunks[chunk_of[net]];
-        int64_t i = net - ch.beg;
-        int64_t nn = ch.node_off[i + 1] - ch.node_off[i];
+        const int64_t net = pos_net[p];
+        const int64_t nn = nn_of[net];
         node0[p + 1] = node0[p] + nn;
-        sink0g[p + 1] = sink0g[p] + (ch.sink_off[i + 1] - ch.sink_off[i]);
+        sink0g[p + 1] = sink0g[p] + ns_of[net];
         max_nodes = std::max(max_nodes, nn);
     }
     const int64_t NN = node0[N], NS = sink0g[N];
     ctx->n_nodes = NN;
     ctx->n_sinks = NS;
+    phase("offsets");
     // host staging in device layout
-    std::vector<uint32_t> xy(NN);
-    std::vector<int32_t> kid(NN * 4), len(NN), sink0(NN);
-    std::vector<uint8_t> edir(NN), nkid(NN), nl(NN), nh(NN), pdrv(N);
-    std::vector<uint16_t> nsink(NN), height(NN);
-    std::vector<double> wd(NN), ur(NN);
-    std::vector<uint8_t> p_layer(NS);
-    std::vector<double> p_cap(NS), p_w(NS);
-    std::vector<int64_t> p_orig(NS), net_id(N);
+    hvec<uint32_t> xy(NN);
+    hvec<int32_t> kid(NN * 4), len(NN), sink0(NN);
+    hvec<uint8_t> edir(NN), nkid(NN), nl(NN), nh(NN), pdrv(N);
+    hvec<uint16_t> nsink(NN), height(NN);
+    hvec<double> wd(NN), ur(NN);
+    hvec<uint8_t> p_layer(NS);
+    hvec<double> p_cap(NS), p_w(NS);
+    hvec<int64_t> p_orig(NS);
+    std::vector<int64_t> net_id(N);
     {
         std::atomic<int64_t> nx{0};
         auto lay = [&]() {
@@ -961,6 +1017,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     chunks.shrink_to_fit();
 
 
+    phase("forest staging");
     // ---- upload forest, allocate scratch
     DevForest &F = ctx->F;
     F.n_nets = N; F.n_nodes = NN; F.n_sinks = NS;
@@ -986,6 +1043,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
     TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
     if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
+    phase("forest upload");
     // persistent k_assign grid, tickets, dataflow counters, big-net slots
     {
         int per_sm = 0, n_sm = 0;
@@ -1000,10 +1058,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         small_pos.push_back(0);
         TRY(dev_upload(ctx, &ctx->d_big_pos, big_pos.data(), big_pos.size()));
         TRY(dev_upload(ctx, &ctx->d_small_pos, small_pos.data(), small_pos.size()));
-        flow_big.push_back(0);
-        flow_small.push_back(0);
-        TRY(dev_upload(ctx, &ctx->d_flow_big_pos, flow_big.data(), flow_big.size()));
-        TRY(dev_upload(ctx, &ctx->d_flow_small_pos, flow_small.data(), flow_small.size()));
         // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
         ctx->n_big_ctas = big_pos.empty() ? 0 : n_sm;
         if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
@@ -1026,6 +1080,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     ctx->h_edir.swap(edir);
     ctx->h_net_node0.swap(node0);
     ctx->h_net_id.swap(net_id);
+    phase("grid/tickets/slots");
     auto t3 = std::chrono::steady_clock::now();
 
     la_stats &stt = ctx->stats;
@@ -1161,12 +1216,50 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     return LA_OK;
 }
 
+// Dataflow priority lists, built on the first dataflow run: nets are taken
+// in descending weighted bottom level (longest chain of dependent work still ahead of the
+// net; weight ~ its latency), ties by position.  Bottom levels strictly decrease along DAG
+// edges, so the order is topological; critical chains start first.
+static la_status build_flow_lists(la_ctx *ctx) {
+    if (ctx->d_flow_big_pos) return LA_OK;
+    const int64_t N = ctx->n_nets;
+    std::vector<int64_t> off(N + 1, 0);
+    if (N) CK(cudaMemcpyAsync(off.data(), ctx->d_succ_off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<int32_t> succ((size_t)std::max<int64_t>(off[N], 1));
+    if (off[N])
+        CK(cudaMemcpyAsync(succ.data(), ctx->d_succ, sizeof(int32_t) * off[N], cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint8_t> big(N, 0);
+    for (int32_t p : ctx->h_big_pos) big[p] = 1;
+    std::vector<int64_t> bl(N);
+    for (int64_t p = N - 1; p >= 0; p--) {
+        const int64_t nn = ctx->h_net_node0[p + 1] - ctx->h_net_node0[p];
+        int64_t m = 0;
+        for (int64_t e = off[p]; e < off[p + 1]; e++) m = std::max(m, bl[succ[e]]);   // succ positions > p
+        bl[p] = m + 8 + (big[p] ? nn / 4 : nn);
+    }
+    auto by_prio = [&](int32_t a, int32_t c) { return bl[a] != bl[c] ? bl[a] > bl[c] : a < c; };
+    std::vector<int32_t> fb = ctx->h_big_pos, fs = ctx->h_small_pos;
+    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    par_sort(fb, by_prio, nthr);
+    par_sort(fs, by_prio, nthr);
+    fb.push_back(0);     // never empty on the device
+    fs.push_back(0);
+    TRY(dev_upload(ctx, &ctx->d_flow_big_pos, fb.data(), fb.size()));
+    TRY(dev_upload(ctx, &ctx->d_flow_small_pos, fs.data(), fs.size()));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LA_OK;
+}
+
 la_status la_assign_all(la_ctx *ctx) {
     TRY(check_ready(ctx));
     const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
     if (ctx->world == 1 && ctx->fuse_commit && ctx->schedule == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
         ctx->next_batch == 0 && !ctx->flow_dirty) {
-        // one persistent launch over every work item, nets ordered by the dependency DAG
+        // one persistent launch over every net, in bottom-level priority order
+        TRY(build_flow_lists(ctx));
         AssignLaunch al = assign_launch(ctx);
         al.big_pos = ctx->d_flow_big_pos;
         al.small_pos = ctx->d_flow_small_pos;
@@ -1241,22 +1334,34 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     if (N) CK(cudaMemcpyAsync(froot.data(), ctx->S.froot, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->stats.d2h_bytes += 3 * NN + 8 * N;
-    // per input net: counts
+    // per input net: counts (threads over positions)
+    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     std::vector<int64_t> nw(N + 1, 0), nv(N + 1, 0);
     std::vector<int64_t> pos_of(N);
-    int64_t vcuts = 0;
-    for (int64_t p = 0; p < N; p++) {
-        int64_t net = ctx->h_net_id[p];
-        pos_of[net] = p;
-        int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
-        nw[net + 1] = (b - a) - 1;
-        int64_t v = 0;
-        for (int64_t k = a; k < b; k++) {
-            if (st[k] > sb[k]) v++;
-            vcuts += st[k] - sb[k];
-        }
-        nv[net + 1] = v;
+    std::vector<int64_t> vc_part(nthr + 1, 0);
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nthr; t++)
+            th.emplace_back([&, t] {
+                int64_t vc = 0;
+                for (int64_t p = N * t / nthr; p < N * (t + 1) / nthr; p++) {
+                    const int64_t net = ctx->h_net_id[p];
+                    pos_of[net] = p;
+                    const int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
+                    nw[net + 1] = (b - a) - 1;
+                    int64_t v = 0;
+                    for (int64_t k = a; k < b; k++) {
+                        if (st[k] > sb[k]) v++;
+                        vc += st[k] - sb[k];
+                    }
+                    nv[net + 1] = v;
+                }
+                vc_part[t] = vc;
+            });
+        for (auto &x : th) x.join();
     }
+    int64_t vcuts = 0;
+    for (unsigned t = 0; t < nthr; t++) vcuts += vc_part[t];
     ctx->stats.via_cuts = vcuts;
     for (int64_t i = 0; i < N; i++) { nw[i + 1] += nw[i]; nv[i + 1] += nv[i]; }
     if (n_wires) *n_wires = nw[N];
@@ -1264,35 +1369,41 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     if (wire_ptr) std::memcpy(wire_ptr, nw.data(), sizeof(int64_t) * (N + 1));
     if (via_ptr) std::memcpy(via_ptr, nv.data(), sizeof(int64_t) * (N + 1));
     if (net_cost)
-        for (int64_t i = 0; i < N; i++) net_cost[i] = froot[pos_of[i]];
+        par_for(N, nthr, [&](int64_t i) { net_cost[i] = froot[pos_of[i]]; });
     if (wires || vias) {
-        std::vector<std::array<int32_t, 5>> W;
-        std::vector<std::array<int32_t, 4>> V;
-        for (int64_t net = 0; net < N; net++) {
-            int64_t p = pos_of[net];
-            int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
-            W.clear();
-            V.clear();
-            for (int64_t k = a; k < b; k++) {
-                int x = ctx->h_xy[k] & 0xffff, y = ctx->h_xy[k] >> 16;
-                if (ctx->h_edir[k] != NO_DIR) {
-                    int ln = ctx->h_len[k];
-                    int qx = x, qy = y;   // parent GCell
-                    switch (ctx->h_edir[k]) {
-                        case DIR_E: qx = x - ln; break;
-                        case DIR_W: qx = x + ln; break;
-                        case DIR_N: qy = y - ln; break;
-                        default: qy = y + ln; break;
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nthr; t++)
+            th.emplace_back([&, t] {
+                std::vector<std::array<int32_t, 5>> W;
+                std::vector<std::array<int32_t, 4>> V;
+                for (int64_t net = N * t / nthr; net < N * (t + 1) / nthr; net++) {
+                    const int64_t p = pos_of[net];
+                    const int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
+                    W.clear();
+                    V.clear();
+                    for (int64_t k = a; k < b; k++) {
+                        const int x = ctx->h_xy[k] & 0xffff, y = ctx->h_xy[k] >> 16;
+                        if (ctx->h_edir[k] != NO_DIR) {
+                            const int ln = ctx->h_len[k];
+                            int qx = x, qy = y;   // parent GCell
+                            switch (ctx->h_edir[k]) {
+                                case DIR_E: qx = x - ln; break;
+                                case DIR_W: qx = x + ln; break;
+                                case DIR_N: qy = y - ln; break;
+                                default: qy = y + ln; break;
+                            }
+                            W.push_back({std::min(x, qx), std::min(y, qy), std::max(x, qx), std::max(y, qy),
+                                         (int32_t)lay[k]});
+                        }
+                        if (st[k] > sb[k]) V.push_back({x, y, (int32_t)sb[k], (int32_t)st[k]});
                     }
-                    W.push_back({std::min(x, qx), std::min(y, qy), std::max(x, qx), std::max(y, qy), (int32_t)lay[k]});
+                    std::sort(W.begin(), W.end());
+                    std::sort(V.begin(), V.end());
+                    if (wires) std::memcpy(wires + 5 * nw[net], W.data(), 20 * W.size());
+                    if (vias) std::memcpy(vias + 4 * nv[net], V.data(), 16 * V.size());
                 }
-                if (st[k] > sb[k]) V.push_back({x, y, (int32_t)sb[k], (int32_t)st[k]});
-            }
-            std::sort(W.begin(), W.end());
-            std::sort(V.begin(), V.end());
-            if (wires) std::memcpy(wires + 5 * nw[net], W.data(), 20 * W.size());
-            if (vias) std::memcpy(vias + 4 * nv[net], V.data(), 16 * V.size());
-        }
+            });
+        for (auto &x : th) x.join();
     }
     return LA_OK;
 }
