@@ -297,10 +297,13 @@ struct Builder {
     std::vector<uint64_t> pcells;
     // preorder tree
     std::vector<int32_t> px, py, ppar, plen, pedir, pheight, pnl, pnh;
-    std::vector<std::vector<int32_t>> pkids;
-    std::vector<std::vector<int64_t>> psinks;
-    std::vector<double> w, ur;
-    std::vector<int32_t> order, finalid;
+    std::vector<std::array<int32_t, 4>> pkids;     // children per preorder node (E, W, N, S order)
+    std::vector<uint8_t> pnk;                       // number of children
+    std::vector<int32_t> sink_cnt, sink_beg;        // sinks per node: CSR over sink_list
+    std::vector<int64_t> sink_list, pin_node;       // input pin indices, grouped by node in input order
+    std::vector<double> w, ur, pwq;                 // pwq: Eq. (4) weight per pin of the net
+    std::vector<int32_t> order, finalid, pre, vof;
+    std::vector<uint8_t> seen;
 
     int64_t vfind(uint64_t g) const {
         auto it = std::lower_bound(vs.begin(), vs.end(), g);
@@ -387,7 +390,7 @@ struct Builder {
         }
         // connectivity from the driver
         {
-            std::vector<uint8_t> seen(nv, 0);
+            seen.assign(nv, 0);
             bfs.clear();
             int64_t r0 = vfind(g_drv);
             bfs.push_back((int32_t)r0);
@@ -416,20 +419,20 @@ struct Builder {
             return !(m == ((1 << DIR_E) | (1 << DIR_W)) || m == ((1 << DIR_N) | (1 << DIR_S)));
         };
         // preorder DFS from the root, children E, W, N, S
-        px.clear(); py.clear(); ppar.clear(); plen.clear(); pedir.clear(); pkids.clear(); psinks.clear();
+        px.clear(); py.clear(); ppar.clear(); plen.clear(); pedir.clear(); pkids.clear(); pnk.clear();
         vnode.assign(nv, -1);
         auto add = [&](int x, int y, int par, int ln, int ed, int64_t vi) {
             px.push_back(x); py.push_back(y); ppar.push_back(par); plen.push_back(ln); pedir.push_back(ed);
-            pkids.emplace_back(); psinks.emplace_back();
+            pkids.push_back({-1, -1, -1, -1}); pnk.push_back(0);
             vnode[vi] = (int32_t)px.size() - 1;
             return (int32_t)px.size() - 1;
         };
-        std::vector<int32_t> pre;
+        pre.clear();
         {
             int64_t rv = vfind(g_drv);
             add((int)(g_drv % X), (int)(g_drv / X), -1, 0, -1, rv);
             stack.assign(1, 0);
-            std::vector<int32_t> vof(1, (int32_t)rv);
+            vof.assign(1, (int32_t)rv);
             while (!stack.empty()) {
                 int32_t n = stack.back();
                 stack.pop_back();
@@ -447,7 +450,7 @@ struct Builder {
                     }
                     int32_t k = add(cx, cy, n, ln, d, vi);
                     vof.push_back((int32_t)vi);
-                    pkids[n].push_back(k);
+                    pkids[n][pnk[n]++] = k;
                     kids[nk++] = k;
                 }
                 for (int i = nk - 1; i >= 0; i--) stack.push_back(kids[i]);
@@ -457,12 +460,24 @@ struct Builder {
         // pins: nl/nh over all pins (driver included); sinks in input order
         pnl.assign(nn, 255);
         pnh.assign(nn, -1);
+        sink_cnt.assign(nn + 1, 0);
+        pin_node.resize(p1 - p0);
+        pwq.resize(p1 - p0);
         for (int64_t p = p0; p < p1; p++) {
             int32_t n = vnode[vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p])];
+            pin_node[p - p0] = n;
             pnl[n] = std::min<int32_t>(pnl[n], nd->pin_layer[p]);
             pnh[n] = std::max<int32_t>(pnh[n], nd->pin_layer[p]);
-            if (p != p0) psinks[n].push_back(p);
+            if (p != p0) {
+                sink_cnt[n + 1]++;
+                pwq[p - p0] = pin_weight(nd->pin_slack[p]);
+            }
         }
+        sink_beg.assign(nn + 1, 0);
+        for (size_t n = 0; n < nn; n++) sink_beg[n + 1] = sink_beg[n] + sink_cnt[n + 1];
+        sink_list.resize(sink_beg[nn]);
+        for (size_t n = 0; n < nn; n++) sink_cnt[n] = sink_beg[n];     // fill cursors
+        for (int64_t p = p0 + 1; p < p1; p++) sink_list[sink_cnt[pin_node[p - p0]]++] = p;   // input order per node
         // heights; subtree max sink weight (Eq. 5, reading R3); 0 without sinks (R39)
         pheight.assign(nn, 0);
         w.assign(nn, 0.0);
@@ -470,8 +485,8 @@ struct Builder {
             int32_t n = *it;
             int h = 0;
             double m = 0.0;
-            for (int64_t q : psinks[n]) m = std::max(m, pin_weight(nd->pin_slack[q]));
-            for (int32_t k : pkids[n]) { h = std::max(h, pheight[k] + 1); m = std::max(m, w[k]); }
+            for (int32_t q = sink_beg[n]; q < sink_beg[n + 1]; q++) m = std::max(m, pwq[sink_list[q] - p0]);
+            for (int k = 0; k < pnk[n]; k++) { h = std::max(h, pheight[pkids[n][k]] + 1); m = std::max(m, w[pkids[n][k]]); }
             pheight[n] = h;
             w[n] = m;
         }
@@ -491,22 +506,23 @@ struct Builder {
         for (size_t i = 0; i < nn; i++) {
             int32_t n = order[i];
             out.xy[i] = (uint32_t)px[n] | ((uint32_t)py[n] << 16);
-            for (size_t k = 0; k < pkids[n].size(); k++) out.kid[i * 4 + k] = finalid[pkids[n][k]];
+            for (int k = 0; k < pnk[n]; k++) out.kid[i * 4 + k] = finalid[pkids[n][k]];
             out.len[i] = plen[n];
             out.edir[i] = ppar[n] < 0 ? NO_DIR : (uint8_t)pedir[n];
-            out.nkid[i] = (uint8_t)pkids[n].size();
+            out.nkid[i] = pnk[n];
             out.nl[i] = (uint8_t)pnl[n];
             out.nh[i] = (uint8_t)(pnh[n] < 0 ? 255 : pnh[n]);
             out.wd[i] = ctx->W_D * w[n];
             out.ur[i] = ur[n];
             out.height[i] = (uint16_t)std::min(pheight[n], 65535);
             out.sink0[i] = (int32_t)out.p_layer.size();
-            out.nsink[i] = (uint16_t)psinks[n].size();
-            for (int64_t q : psinks[n]) {
+            out.nsink[i] = (uint16_t)(sink_beg[n + 1] - sink_beg[n]);
+            for (int32_t qi = sink_beg[n]; qi < sink_beg[n + 1]; qi++) {
+                const int64_t q = sink_list[qi];
                 out.p_layer.push_back(nd->pin_layer[q]);
                 out.p_cap.push_back(nd->pin_cap[q]);
                 // pin-via delay weight: w^d_{n->par} for a non-root node (Alg. 3 l.6), W_D * w_q at the root (R13)
-                out.p_w.push_back(ppar[n] < 0 ? ctx->W_D * pin_weight(nd->pin_slack[q]) : ctx->W_D * w[n]);
+                out.p_w.push_back(ppar[n] < 0 ? ctx->W_D * pwq[q - p0] : ctx->W_D * w[n]);
                 out.p_orig.push_back(q);
             }
         }
