@@ -112,8 +112,12 @@ __global__ void k_unpack_dec(DevScratch S, int64_t node_beg, int64_t node_end) {
 
 // ------------------------------------------------------------------ K6 + K7 --
 // Canonical fast Elmore form (DESIGN §3 O9), one thread per net.
-__global__ void k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg, int64_t net_end) {
+constexpr int ELMORE_THREADS = 128;
+
+__global__ void __launch_bounds__(ELMORE_THREADS) k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg,
+                                                          int64_t net_end) {
     __shared__ TechTab T;
+    __shared__ double Tks[MAXL][ELMORE_THREADS];   // T(n, k) of the current node, one column per thread
     stage_tab(T, G.tab);
     __syncthreads();
     const int64_t net = net_beg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -146,10 +150,11 @@ __global__ void k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg, 
     S.net_cap[nid] = S.Cd[n1 - 1];
     S.net_rc[nid] = S.rcv[n1 - 1];
     // top-down: via stacks (C>= / C<= over the branches attached at each layer) and pi wires
-    double Tk[MAXL];
+    double *Tk = &Tks[0][threadIdx.x];               // Tk[k * ELMORE_THREADS]: no local-memory array
+#define TK(k) Tk[(k) * ELMORE_THREADS]
     for (int64_t n = n1 - 1; n >= n0; --n) {
         const int ln = S.lay[n], b = S.sb[n], t = S.st[n];
-        Tk[ln] = (n == n1 - 1) ? 0.0 : S.Tin[n];
+        TK(ln) = (n == n1 - 1) ? 0.0 : S.Tin[n];
         const int q0 = F.sink0[n], qn = F.nsink[n], nk = F.nkid[n];
         for (int k = ln; k < t; ++k) {
             const int j = k + 1;
@@ -160,7 +165,7 @@ __global__ void k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg, 
                 const int ls = S.lay[s];
                 if (ls >= j) acc = acc + (T.c[ls] * (double)F.len[s] + S.Cd[s]);
             }
-            Tk[k + 1] = Tk[k] + T.vr[k] * acc;
+            TK(k + 1) = TK(k) + T.vr[k] * acc;
         }
         for (int k = ln; k > b; --k) {
             const int j = k - 1;
@@ -171,16 +176,17 @@ __global__ void k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg, 
                 const int ls = S.lay[s];
                 if (ls <= j) acc = acc + (T.c[ls] * (double)F.len[s] + S.Cd[s]);
             }
-            Tk[k - 1] = Tk[k] + T.vr[k - 1] * acc;
+            TK(k - 1) = TK(k) + T.vr[k - 1] * acc;
         }
-        for (int q = q0; q < q0 + qn; ++q) S.sink_delay[F.p_orig[q]] = Tk[F.p_layer[q]];
+        for (int q = q0; q < q0 + qn; ++q) S.sink_delay[F.p_orig[q]] = TK(F.p_layer[q]);
         for (int i = 0; i < nk; ++i) {
             const int64_t s = F.kid[n * 4 + i];
             const int ls = S.lay[s], len = F.len[s];
             const double Cw = T.c[ls] * (double)len, Rw = T.r[ls] * (double)len;
-            S.Tin[s] = Tk[ls] + Rw * (0.5 * Cw + S.Cd[s]);
+            S.Tin[s] = TK(ls) + Rw * (0.5 * Cw + S.Cd[s]);
         }
     }
+#undef TK
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -231,7 +237,7 @@ cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch
                           int64_t net_end, cudaStream_t s) {
     int64_t n = net_end - net_beg;
     if (n <= 0) return cudaSuccess;
-    k_elmore<<<nblk(n, 128), 128, 0, s>>>(G, F, S, net_beg, net_end);
+    k_elmore<<<nblk(n, ELMORE_THREADS), ELMORE_THREADS, 0, s>>>(G, F, S, net_beg, net_end);
     return cudaGetLastError();
 }
 
