@@ -116,11 +116,9 @@ __device__ __forceinline__ NetBuf net_buf(char *b, const NetLay &w) {
 struct WarpScr {
     double Vt[MAXL * MAXL];               // V(b, t) of the current node, [b][t]
     double cpt[MAXE * MAXKIDS * MAXE];    // cost'(l_e; s_k, slot s), [e][k][s]
-    double bestG[MAXE];                   // per entry: best G' so far
+    double bestG[MAXE];                   // per entry: best G'
     uint32_t bestK[MAXE];                 // per entry: (t - b) << 4 | b, bit 8 = none
-    int32_t off[MAXE + 1];                // task offsets per entry
-    uint32_t mT[MAXE], mB[MAXE];          // candidate tops above t0 / bottoms below b0
-    uint8_t el[MAXE], eb0[MAXE], et0[MAXE], enT[MAXE];
+    uint8_t el[MAXE];                     // per entry: its layer
 };
 constexpr int SCR_BYTES = (int)((sizeof(WarpScr) + 15) & ~(size_t)15);
 
@@ -369,88 +367,69 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
         }
         w.cpt[(e * MAXKIDS + k) * MAXE + s] = cp;
     }
-    // (3) entries: span bounds, candidate sets, task counts (warp prefix sum)
-    int cnt = 0;
-    if (lane < nE) {
-        const int l = root ? pdrv : sh.lay_of[dt][lane];
-        w.el[lane] = (uint8_t)l;
-        if (root || sh.routable[l]) {                  // illegal entry layers keep A = +inf (R15)
-            const int nl = nd.nl, nh = nd.nh;
-            const bool pins = nl != 255;
-            const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
-            const uint32_t mT = legal_any & ~((2u << t0) - 1u);
-            const uint32_t mB = legal_any & ((1u << b0) - 1u);
-            const int nT = 1 + __popc(mT), nB = 1 + __popc(mB);
-            cnt = nk == 0 ? 1 : (nk == 1 ? nT + nB - 1 : nT * nB);
-            w.eb0[lane] = (uint8_t)b0;
-            w.et0[lane] = (uint8_t)t0;
-            w.enT[lane] = (uint8_t)nT;
-            w.mT[lane] = mT;
-            w.mB[lane] = mB;
-        }
-        w.bestG[lane] = dinf();
-        w.bestK[lane] = 0x1ffu;
-    }
-    int inc = cnt;
-#pragma unroll
-    for (int o = 1; o < MAXE; o <<= 1) {
-        const int x = __shfl_up_sync(FULL_MASK, inc, o);
-        if (lane >= o) inc += x;
-    }
-    if (lane < nE) w.off[lane + 1] = inc;
-    if (lane == 0) w.off[0] = 0;
-    const int total = __shfl_sync(FULL_MASK, inc, nE - 1);
     __syncwarp();
-    // (4) candidate tasks, 32 per round, segmented argmin per entry
-    for (int base = 0; base < total; base += 32) {
-        const int idx = base + lane;
-        double Gp = dinf();
-        uint32_t key = 0x1ffu;
-        int seg_end = 0, e = 0;
-        if (idx < total) {
-            while (e + 1 < nE && w.off[e + 1] <= idx) ++e;
-            seg_end = min(w.off[e + 1] - base, 32);
-            const int cI = idx - w.off[e];
-            const int b0 = w.eb0[e], t0 = w.et0[e], nT = w.enT[e];
-            int b = b0, t = t0;
-            if (nk == 1) {
-                if (cI < nT) t = cI == 0 ? t0 : nth_bit(w.mT[e], cI);
-                else b = nth_bit(w.mB[e], cI - nT + 1);
-            } else if (nk >= 2) {
-                const int bi = cI / nT, ti = cI - bi * nT;
-                if (bi) b = nth_bit(w.mB[e], bi);
-                if (ti) t = nth_bit(w.mT[e], ti);
-            }
-            double g = w.Vt[b * MAXL + t];
-            bool feas = true;
+    // (3) lanes over (entry e, span bottom b): 8-lane segments, one per entry, lane s8 takes
+    //     the bottoms b = B[s8], B[s8 + 8], ...; each sweeps the candidate tops t upward with
+    //     the running son minima (strict <: the lowest layer keeps ties), then a butterfly
+    //     argmin by the key (G', t-b, b) (R21) leaves the entry's best span in its segment
+    const int nl = nd.nl, nh = nd.nh;
+    const bool pins = nl != 255;
+    const int s8 = lane & 7;
+    for (int e0 = 0; e0 < nE; e0 += 4) {
+        const int e = e0 + (lane >> 3);
+        const int l = root ? pdrv : sh.lay_of[dt][e < nE ? e : 0];
+        const bool eok = e < nE && (root || sh.routable[l]);
+        const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+        const uint32_t mB = legal_any & ((1u << b0) - 1u);
+        const int nB = 1 + __popc(mB);
+        double Gb = dinf();
+        uint32_t kb = 0x1ffu;
+        for (int bi = s8; eok && bi < nB; bi += 8) {
+            const int b = bi == 0 ? b0 : nth_bit(mB, bi);
+            double m[MAXKIDS];
 #pragma unroll
             for (int k = 0; k < MAXKIDS; ++k) {
-                if (k < nk) {
-                    double mv;
-                    feas = feas && window_argmin(w, sh, e, k, kdt[k], b, t, &mv) >= 0;
-                    g = g + mv;
-                }
+                m[k] = dinf();
+                if (k < nk) window_argmin(w, sh, e, k, kdt[k], b, t0, &m[k]);
             }
-            if (feas) {
-                Gp = g;
-                key = (uint32_t)(((t - b) << 4) | b);
-            }
-        }
-        // segmented argmin over the lanes of one entry (contiguous lanes)
+            auto evaluate = [&](int t) {
+                double g = w.Vt[b * MAXL + t];
+                bool feas = true;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double oG = __shfl_down_sync(FULL_MASK, Gp, o);
-            const uint32_t ok = __shfl_down_sync(FULL_MASK, key, o);
-            if (lane + o < seg_end && (oG < Gp || (oG == Gp && ok < key))) { Gp = oG; key = ok; }
-        }
-        if (idx < total && (lane == 0 || idx == w.off[e])) {    // head of entry e's segment in this round
-            if (Gp < w.bestG[e] || (Gp == w.bestG[e] && key < w.bestK[e])) {
-                w.bestG[e] = Gp;
-                w.bestK[e] = key;
+                for (int k = 0; k < MAXKIDS; ++k)
+                    if (k < nk) {
+                        feas = feas && m[k] < dinf();
+                        g = g + m[k];
+                    }
+                const uint32_t key = (uint32_t)(((t - b) << 4) | b);
+                if (feas && (g < Gb || (g == Gb && key < kb))) { Gb = g; kb = key; }
+            };
+            evaluate(t0);
+            for (int t = t0 + 1; t < L; ++t) {
+                if (!((legal_any >> t) & 1)) continue;
+                const int dtt = sh.dir[t], st = sh.lidx[t];
+#pragma unroll
+                for (int k = 0; k < MAXKIDS; ++k)
+                    if (k < nk && kdt[k] == dtt) {
+                        const double cp = w.cpt[(e * MAXKIDS + k) * MAXE + st];
+                        if (cp < m[k]) m[k] = cp;
+                    }
+                evaluate(t);
             }
         }
-        __syncwarp();
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const double oG = __shfl_xor_sync(FULL_MASK, Gb, o, 8);
+            const uint32_t ok = __shfl_xor_sync(FULL_MASK, kb, o, 8);
+            if (oG < Gb || (oG == Gb && ok < kb)) { Gb = oG; kb = ok; }
+        }
+        if (s8 == 0 && e < nE) {
+            w.el[e] = (uint8_t)l;
+            w.bestG[e] = Gb;
+            w.bestK[e] = kb;
+        }
     }
+    __syncwarp();
     // (5) entry lanes: winner's son layers, G (cost, not cost'), K; finish
     if (lane < nE && (root || sh.routable[w.el[lane]])) {
         const int e = lane, l = w.el[e];

@@ -142,3 +142,75 @@ if os.environ.get("DIAG_NCU"):
     A.sync()
     torch.cuda.profiler.stop()
     A.close()
+
+if os.environ.get("DIAG_TAIL"):
+    import numpy as np
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    A.reset()
+    la.la_set_tracing(A.ctx, True)
+    A.assign_all()
+    A.sync()
+    t = la.la_get_trace(A.ctx, d.n_nets)
+    bo = A.batches()
+    nbat = int(bo.max()) + 1
+    span = tail = 0.0
+    gaps = 0.0
+    prev_end = None
+    for b in range(nbat):
+        m = bo == b
+        s0, e = t[m, 0].min(), t[m, 3].max()
+        e90 = np.percentile(t[m, 3], 90)
+        span += (e - s0) / 1e3
+        tail += (e - e90) / 1e3
+        if prev_end is not None:
+            gaps += (s0 - prev_end) / 1e3
+        prev_end = e
+    print(f"  batches {nbat}: sum of spans {span:.0f} us, of which after the 90th-percentile finish {tail:.0f} us; "
+          f"gaps between batches {gaps:.0f} us", flush=True)
+    A.close()
+
+if os.environ.get("DIAG_PHASES"):
+    import numpy as np
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    A.reset()
+    la.la_set_tracing(A.ctx, True)
+    A.assign_all()
+    A.sync()
+    t = la.la_get_trace(A.ctx, d.n_nets).astype(np.float64)
+    sol = A.solution()
+    nw = np.diff(sol["wire_ptr"])
+    ph = {"gather": t[:, 1] - t[:, 0], "leaves": t[:, 2] - t[:, 1], "nodes": t[:, 4] - t[:, 2],
+          "backtrack+commit": t[:, 3] - t[:, 4]}
+    tot = t[:, 3] - t[:, 0]
+    print("  mean us per net: " + "  ".join(f"{k} {v.mean() / 1e3:.2f}" for k, v in ph.items()) +
+          f"  total {tot.mean() / 1e3:.2f}", flush=True)
+    for lo, hi in ((0, 2), (2, 4), (4, 8), (8, 16), (16, 10000)):
+        m = (nw >= lo) & (nw < hi)
+        print(f"    wires [{lo},{hi}) {m.mean():.3f}: " + "  ".join(f"{k} {v[m].mean() / 1e3:.2f}" for k, v in ph.items()),
+              flush=True)
+    A.close()
+
+if os.environ.get("DIAG_NODEKIND"):
+    import numpy as np
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    A.reset()
+    la.la_set_tracing(A.ctx, True)
+    A.assign_all()
+    A.sync()
+    t = la.la_get_trace(A.ctx, d.n_nets).astype(np.float64)
+    sol = A.solution()
+    nw = np.diff(sol["wire_ptr"])
+    tot = t[:, 3] - t[:, 0]
+    print(f"  mean us per net: total {tot.mean() / 1e3:.2f}  one-son nodes {t[:, 1].mean() / 1e3:.2f}  "
+          f"other internal nodes {t[:, 4].mean() / 1e3:.2f}", flush=True)
+    for lo, hi in ((0, 2), (2, 4), (4, 8), (8, 16), (16, 10000)):
+        m = (nw >= lo) & (nw < hi)
+        print(f"    wires [{lo},{hi}): total {tot[m].mean() / 1e3:.2f} one-son {t[m, 1].mean() / 1e3:.2f} "
+              f"other {t[m, 4].mean() / 1e3:.2f}", flush=True)
+    A.close()
