@@ -706,11 +706,9 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
                 if (a.hybrid) break;
                 return;
             }
-            const int64_t net = a.big_pos[a.big_beg + wk];
-            const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
-            const int nn = (int)(n1 - n0);
-            const int q_base = F.sink0[n0];
-            const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - q_base;
+            const int4 rec = a.big_pos[a.big_beg + wk];
+            const int64_t net = rec.x, n0 = (uint32_t)rec.y;
+            const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
             const NetLay lay = net_layout(nn, ns, L, LD);
             char *base = lay.bytes <= ASSIGN_WARPS * slay.bytes ? dyn : gmine;
             const NetCtx c{net_buf(base, lay), L, LD, nn};
@@ -719,21 +717,24 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
     }
 
     // ---------------- small nets: one warp per net ----------------
+    // The ticket of the next net is taken before the current one runs, so its atomic
+    // round trip overlaps the DP.
     char *mine = dyn + warp * slay.bytes;
     const int64_t n_work = a.small_end - a.small_beg;
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
+    tk = __shfl_sync(FULL_MASK, tk, 0);
     for (;;) {
-        unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
-        tk = __shfl_sync(FULL_MASK, tk, 0);
         if ((int64_t)tk >= n_work) return;
-        const int64_t net = a.small_pos[a.small_beg + (int64_t)tk];
-        const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
-        const int nn = (int)(n1 - n0);
-        const int q_base = F.sink0[n0];
-        const int ns = F.sink0[n1 - 1] + F.nsink[n1 - 1] - q_base;
+        const int4 rec = a.small_pos[a.small_beg + (int64_t)tk];
+        unsigned long long tk_next = 0;
+        if (lane == 0) tk_next = atomicAdd(a.ticket, 1ull);
+        const int64_t net = rec.x, n0 = (uint32_t)rec.y;
+        const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
         const NetCtx c{net_buf(mine, slay), L, LD, nn};
         run_net<false>(c, w, sh, G, F, S, a, net, n0, q_base, ns, lane, 32);
         __syncwarp();
+        tk = __shfl_sync(FULL_MASK, tk_next, 0);
     }
 }
 

@@ -104,8 +104,11 @@ struct la_ctx {
     bool fuse_commit = true;
     int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
     std::vector<int64_t> batch_big0, batch_small0;   // [n_batches+1] per-batch ranges of the role lists
-    int32_t *d_big_pos = nullptr, *d_small_pos = nullptr;           // batch order
-    int32_t *d_flow_big_pos = nullptr, *d_flow_small_pos = nullptr; // dataflow priority order
+    // role lists as packed per-net records (position, node0, nodes | sinks << 16, sink0): one
+    // 16-byte load per net instead of a chain of dependent loads in k_assign
+    int4 *d_big_pos = nullptr, *d_small_pos = nullptr;               // batch order
+    int4 *d_flow_big_pos = nullptr, *d_flow_small_pos = nullptr;     // dataflow priority order
+    std::vector<int64_t> h_net_sink0;                                // [n_nets+1] first sink per position
     int32_t n_big_ctas = 0;
     bool hybrid = true;                       // batch-mode launches: all CTAs take big nets first
     bool tracing = false;
@@ -731,6 +734,8 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     return LA_OK;
 }
 
+static std::vector<int4> pack_nets(const la_ctx *ctx, const std::vector<int32_t> &pos);
+
 la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (!ctx || !n) return set_err(LA_EINVAL, "null argument");
     if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
@@ -1070,10 +1075,11 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
         ctx->h_big_pos = big_pos;
         ctx->h_small_pos = small_pos;
-        big_pos.push_back(0);     // never empty on the device
-        small_pos.push_back(0);
-        TRY(dev_upload(ctx, &ctx->d_big_pos, big_pos.data(), big_pos.size()));
-        TRY(dev_upload(ctx, &ctx->d_small_pos, small_pos.data(), small_pos.size()));
+        ctx->h_net_node0.assign(node0.begin(), node0.end());
+        ctx->h_net_sink0.assign(sink0g.begin(), sink0g.end());
+        const std::vector<int4> ib = pack_nets(ctx, big_pos), is = pack_nets(ctx, small_pos);
+        TRY(dev_upload(ctx, &ctx->d_big_pos, ib.data(), ib.size()));
+        TRY(dev_upload(ctx, &ctx->d_small_pos, is.data(), is.size()));
         // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
         ctx->n_big_ctas = big_pos.empty() ? 0 : n_sm;
         if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
@@ -1232,6 +1238,18 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     return LA_OK;
 }
 
+// Packed k_assign records of the nets at forest positions `pos` (+ one dummy: never empty).
+static std::vector<int4> pack_nets(const la_ctx *ctx, const std::vector<int32_t> &pos) {
+    std::vector<int4> v(pos.size() + 1, int4{0, 0, 0, 0});
+    for (size_t i = 0; i < pos.size(); i++) {
+        const int64_t p = pos[i];
+        const int64_t n0 = ctx->h_net_node0[p], nn = ctx->h_net_node0[p + 1] - n0;
+        const int64_t q0 = ctx->h_net_sink0[p], ns = ctx->h_net_sink0[p + 1] - q0;
+        v[i] = int4{(int)p, (int)n0, (int)(nn | (ns << 16)), (int)q0};
+    }
+    return v;
+}
+
 // Dataflow priority lists, built on the first dataflow run: nets are taken
 // in descending weighted bottom level (longest chain of dependent work still ahead of the
 // net; weight ~ its latency), ties by position.  Bottom levels strictly decrease along DAG
@@ -1261,10 +1279,9 @@ static la_status build_flow_lists(la_ctx *ctx) {
     const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     par_sort(fb, by_prio, nthr);
     par_sort(fs, by_prio, nthr);
-    fb.push_back(0);     // never empty on the device
-    fs.push_back(0);
-    TRY(dev_upload(ctx, &ctx->d_flow_big_pos, fb.data(), fb.size()));
-    TRY(dev_upload(ctx, &ctx->d_flow_small_pos, fs.data(), fs.size()));
+    const std::vector<int4> ib = pack_nets(ctx, fb), is = pack_nets(ctx, fs);
+    TRY(dev_upload(ctx, &ctx->d_flow_big_pos, ib.data(), ib.size()));
+    TRY(dev_upload(ctx, &ctx->d_flow_small_pos, is.data(), is.size()));
     CK(cudaStreamSynchronize(ctx->stream));
     return LA_OK;
 }

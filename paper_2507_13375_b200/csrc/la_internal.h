@@ -89,7 +89,7 @@ cudaError_t launch_unpack_demand(const DevGrid &G, const int32_t *wcap, const in
 // the first n_big_ctas CTAs, one whole CTA per net, and small nets, run by the
 // other CTAs, one 8-lane group per net.  wait == nullptr: batch mode.
 struct AssignLaunch {
-    const int32_t *big_pos, *small_pos;       // forest positions
+    const int4 *big_pos, *small_pos;          // per net: {forest position, first node, nodes | sinks << 16, first sink}
     int64_t big_beg, big_end;                 // this launch's range of big_pos
     int64_t small_beg, small_end;             // this launch's range of small_pos
     int32_t n_big_ctas;                       // CTAs [0, n_big_ctas) take big nets
