@@ -245,6 +245,16 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
     prof = A.profile(reset=True)
     A.profiling(False)
+    # evaluator (outside the step): Eq. (3)/(2) overflow, wirelength, via cuts
+    ev_res, ev_ms = None, None
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            A.profiling(True)
+            A.profile(reset=True)
+        ev_res = A.eval_overflow()
+    pe = A.profile(reset=True)
+    A.profiling(False)
+    ev_ms = pe["eval_ms"] / max(args.steps, 1)
     launches = (A.stats()["launches"] - launches0) // args.steps
     sol = A.solution()
     via_cuts = int((sol["vias"][:, 3] - sol["vias"][:, 2]).sum()) if len(sol["vias"]) else 0
@@ -272,7 +282,16 @@ def run_ours(args, rank, world, local_rank):
                  "kernel_ms_per_step": {"k_assign": a_ms, "k_commit": prof["commit_ms"] / args.steps,
                                         "k_elmore": prof["elmore_ms"] / args.steps,
                                         "reconcile": prof["reconcile_ms"] / args.steps}}
+    # algorithmic bytes: every packed wire / via word once (4 B) + per node lay, sb, st, edir (u8) and len (i32)
+    ev_bytes = 4 * (int(sum(d.wire_layer_sizes())) + d.X * d.Y * (d.L - 1)) + 8 * st["n_nodes"]
     A.close()
+    evaluator = {"kernel": "k_eval_plane x3 + k_eval_nodes (NEXT #3: Eq. (3)/(2) overflow, wirelength, via cuts)",
+                 "bound": "hbm", "ms": ev_ms, "alg_bytes": ev_bytes,
+                 "achieved": ev_bytes / (ev_ms / 1000.0) / 1e9 if ev_ms else None, "peak": hbm, "unit": "GB/s",
+                 "frac": (ev_bytes / (ev_ms / 1000.0) / 1e9 / hbm) if ev_ms else None,
+                 "tof_wire": ev_res["tof_wire"], "legacy_wire": ev_res["legacy_wire"],
+                 "via_cuts": ev_res["via_cuts"], "wire_cap_fF": ev_res["wire_cap"],
+                 "out_of_domain": ev_res["out_of_domain"]}
 
     # e2e: the public API from host buffers: init_grid + load_nets + all batches + Elmore + solution to host
     e2e = None
@@ -321,7 +340,7 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"dp{world}: nets of every conflict-free batch sharded over {world} GPU(s)",
                        "l2": f"inputs > L2: {(4 * (st['via_state_words'] + st['wire_state_words']) + 50 * st['n_nodes']) / 1e9:.2f} GB touched per step",
                        "setup_s": setup_s, "load_ms": st0["load_ms"], "batching_ms": st0["batch_ms"]},
-            "roofline": roof, "roofline_step": roof_step,
+            "roofline": roof, "roofline_step": roof_step, "evaluator": evaluator,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(out), flush=True)

@@ -125,7 +125,33 @@ typedef struct {
 typedef struct {
     int64_t assign_launches, commit_launches, elmore_launches, reconcile_calls;
     double assign_ms, commit_ms, elmore_ms, reconcile_ms;
+    int64_t eval_launches;
+    double eval_ms;
 } la_profile;
+
+/* Evaluation of a 3D solution (la_eval_overflow).
+ * Overflow of a GCell edge e on layer l with demand d and capacity c:
+ *   Eq. (3) (PAPER §II-E l.178-182): of = ofw(l) * e^{s (d - c)}, s = s_pos (0.5) if
+ *   c > 0 else s_zero (1.5), summed over every wire edge of every layer: tof_wire
+ *   (the paper's "total overflow of all the GCell edges", l.169);
+ *   Eq. (2) (l.175-177): of = max{0, d - c}: legacy_wire (exact integer).
+ * The via-cut grid of reading R11 is evaluated the same way with ofw of the
+ * cut's lower layer (R36): tof_via, legacy_via.  Exactness: every element is
+ * binned by (layer, c == 0, d - c) with integer counts on the GPU; the host
+ * then sums count * ofw(l) * exp(s * (d - c)) per layer in a fixed order, so the
+ * result is deterministic and within a few ulps times the element count of the
+ * exactly rounded sum (DESIGN §5 "k_eval").  d - c outside [delta_lo, delta_hi]
+ * is clamped (reading R20) and counted in out_of_domain.  wirelength[l] = unit
+ * wire edges the solution assigns to layer l, via_cuts = sum over via stacks of
+ * (t - b), wire_cap = sum_l c[l] * wirelength[l] (fF; the power term of R27). */
+typedef struct {
+    double tof_wire, tof_via;
+    int64_t legacy_wire, legacy_via;
+    int64_t wirelength[16];
+    int64_t via_cuts;
+    double wire_cap;
+    int64_t out_of_domain;
+} la_eval;
 
 /* Create a context: validate the grid, allocate the packed device demand
  * planes, build the Eq. (3) marginal tables and the via-R table, set up NCCL
@@ -207,6 +233,12 @@ la_status la_set_profiling(la_ctx *ctx, int32_t enable);
 /* Accumulated per-kernel device times since the last reset (synchronises).
  * reset != 0 clears the accumulators after reading. */
 la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset);
+
+/* Overflow, via count and wire capacitance of the current solution and demand
+ * (la_eval above; k_eval_plane / k_eval_nodes).  Requires every batch committed
+ * (LA_ESTATE otherwise).  Synchronises.  Collective when world > 1 (every rank
+ * holds the full demand and evaluates it; results are identical). */
+la_status la_eval_overflow(la_ctx *ctx, la_eval *out);
 
 /* Diagnostics: enable (1) / disable (0) per-net timestamps in k_assign (device
  * %globaltimer, ns).  While enabled every k_assign launch records, for each net

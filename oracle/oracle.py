@@ -189,3 +189,52 @@ def tree(d, net: int):
     if rc != 0:
         raise OracleError(err.value.decode())
     return out[: cnt.value]
+
+
+def evaluate(d, wire_dem, via_dem, wires, vias) -> dict:
+    """Evaluation of a 3D solution by the plain definitions.
+
+    PAPER §II-E Eq. (3) (l.178-182): a GCell edge on layer l with demand d and capacity c
+    overflows by ofw(l) * e^{s (d - c)}, s = 0.5 (s_pos) if c > 0 else 1.5 (s_zero); tof_wire
+    is the sum over every wire edge of every layer (l.169 "total overflow of all the GCell
+    edges").  Eq. (2) (l.175-177): max{0, d - c}, summed: legacy_wire.  The via-cut grid of
+    reading R11 is evaluated the same way with ofw of the cut's lower layer (R36).  Sums of
+    floating-point terms are exactly rounded (math.fsum), so the library's binned sum is
+    compared against the correctly rounded total.  wirelength[l] = unit wire edges on layer l,
+    via_cuts = sum of (t - b) over via stacks, wire_cap = sum over wires of c[l] * length.
+    Grids are in API layout (wire edges per layer, by lower endpoint, row-major; via cuts
+    [k][y][x]); wires [n][5] (x1, y1, x2, y2, l); vias [n][4] (x, y, b, t).
+    """
+    import math
+    wd = np.asarray(wire_dem, np.int64)
+    vd = np.asarray(via_dem, np.int64)
+    wc = np.asarray(d.wire_cap, np.int64)
+    vc = np.asarray(d.via_cap, np.int64)
+    sizes = d.wire_layer_sizes()
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    X, Y = d.X, d.Y
+
+    def terms(dem, cap, ofw_l):
+        delta = (dem - cap).astype(np.float64)
+        s = np.where(cap > 0, d.s_pos, d.s_zero)
+        return [ofw_l * math.exp(sv * dv) for sv, dv in zip(s.tolist(), delta.tolist())]
+
+    tw, lw = [], 0
+    for l in range(d.L):
+        a, b = offs[l], offs[l + 1]
+        tw.extend(terms(wd[a:b], wc[a:b], float(d.ofw[l])))
+        lw += int(np.maximum(wd[a:b] - wc[a:b], 0).sum())
+    tv, lv = [], 0
+    n_cut = X * Y
+    for k in range(d.L - 1):
+        a, b = k * n_cut, (k + 1) * n_cut
+        tv.extend(terms(vd[a:b], vc[a:b], float(d.ofw[k])))
+        lv += int(np.maximum(vd[a:b] - vc[a:b], 0).sum())
+    wires = np.asarray(wires, np.int64).reshape(-1, 5)
+    vias = np.asarray(vias, np.int64).reshape(-1, 4)
+    length = np.abs(wires[:, 2] - wires[:, 0]) + np.abs(wires[:, 3] - wires[:, 1])
+    wl = [int(length[wires[:, 4] == l].sum()) for l in range(16)]
+    wire_cap = math.fsum(float(d.c[l]) * float(n) for l, n in zip(wires[:, 4].tolist(), length.tolist()))
+    return {"tof_wire": math.fsum(tw), "tof_via": math.fsum(tv), "legacy_wire": lw, "legacy_via": lv,
+            "wirelength": wl, "via_cuts": int((vias[:, 3] - vias[:, 2]).sum()), "wire_cap": wire_cap,
+            "n_wire_terms": len(tw), "n_via_terms": len(tv)}

@@ -103,6 +103,8 @@ struct la_ctx {
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
     int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
+    unsigned long long *d_eval = nullptr;     // la_eval_overflow buffers (lazy)
+    int8_t *d_eval_lay = nullptr;             // [3][MAXL] slot -> layer for the H, V and via planes
     std::vector<int64_t> batch_big0, batch_small0;   // [n_batches+1] per-batch ranges of the role lists
     // role lists as packed per-net records (position, node0, nodes | sinks << 16, sink0): one
     // 16-byte load per net instead of a chain of dependent loads in k_assign
@@ -143,7 +145,7 @@ struct la_ctx {
     ~la_ctx() {
         for (void *p : dev_allocs) cudaFree(p);
         void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab,
-                      d_ticket, d_trace, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
+                      d_ticket, d_trace, d_eval, d_eval_lay, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
         for (void *p : gp) if (p) cudaFree(p);
         if (comm) ncclCommDestroy(comm);
         for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -192,7 +194,7 @@ la_status dev_upload(la_ctx *ctx, T **dst, const T *src, size_t n) {
     return LA_OK;
 }
 
-enum { K_ASSIGN = 0, K_COMMIT = 1, K_ELMORE = 2, K_RECONCILE = 3 };
+enum { K_ASSIGN = 0, K_COMMIT = 1, K_ELMORE = 2, K_RECONCILE = 3, K_EVAL = 4 };
 
 // Profiling brackets: record a CUDA event before / after a launch on the context stream.
 int prof_begin(la_ctx *ctx, int kind) {
@@ -1509,6 +1511,7 @@ la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset) {
             case K_ASSIGN: ctx->acc.assign_ms += ms; ctx->acc.assign_launches++; break;
             case K_COMMIT: ctx->acc.commit_ms += ms; ctx->acc.commit_launches++; break;
             case K_ELMORE: ctx->acc.elmore_ms += ms; ctx->acc.elmore_launches++; break;
+            case K_EVAL: ctx->acc.eval_ms += ms; ctx->acc.eval_launches++; break;
             default: ctx->acc.reconcile_ms += ms; ctx->acc.reconcile_calls++; break;
         }
         ctx->ev_pool.push_back(sp.a);
@@ -1517,6 +1520,70 @@ la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset) {
     ctx->spans.clear();
     *out = ctx->acc;
     if (reset) ctx->acc = la_profile{};
+    return LA_OK;
+}
+
+la_status la_eval_overflow(la_ctx *ctx, la_eval *out) {
+    TRY(require_done(ctx));
+    if (!out) return set_err(LA_EINVAL, "null argument");
+    const int L = ctx->L, dlo = ctx->G.delta_lo, dhi = ctx->G.delta_hi, nbins = dhi - dlo + 1;
+    const size_t nh = (size_t)MAXL * 2 * nbins;
+    const size_t nwords = 2 * nh + 2 * MAXL + 1 + MAXL + 1;   // hist w, hist v, legacy w, legacy v, oob, wl, vcuts
+    if (!ctx->d_eval) {
+        CK(cudaMalloc(&ctx->d_eval, sizeof(unsigned long long) * nwords));
+        int8_t lay[3][MAXL] = {};
+        for (int l = 0; l < L; l++) lay[ctx->dir[l]][ctx->G.lidx[l]] = (int8_t)l;
+        for (int k = 0; k < L - 1; k++) lay[2][k] = (int8_t)k;            // via cut k: ofw of its lower layer (R36)
+        CK(cudaMalloc(&ctx->d_eval_lay, sizeof(lay)));
+        CK(cudaMemcpyAsync(ctx->d_eval_lay, lay, sizeof(lay), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    unsigned long long *b = ctx->d_eval;
+    CK(cudaMemsetAsync(b, 0, sizeof(unsigned long long) * nwords, ctx->stream));
+    EvalDev Ew{b, b + 2 * nh, b + 2 * nh + 2 * MAXL, b + 2 * nh + 2 * MAXL + 1, b + 2 * nh + 3 * MAXL + 1};
+    EvalDev Ev = Ew;
+    Ev.hist = b + nh;
+    Ev.legacy = b + 2 * nh + MAXL;
+    const int64_t nH = (int64_t)(ctx->X - 1) * ctx->Y * ctx->LH, nV = (int64_t)ctx->X * (ctx->Y - 1) * ctx->LV;
+    int pe = prof_begin(ctx, K_EVAL);
+    CK(launch_eval_plane(ctx->d_wH, nH, ctx->LH, ctx->d_eval_lay, Ew, dlo, dhi, ctx->stream));
+    CK(launch_eval_plane(ctx->d_wV, nV, ctx->LV, ctx->d_eval_lay + MAXL, Ew, dlo, dhi, ctx->stream));
+    CK(launch_eval_plane(ctx->d_via, ctx->n_via_api, L - 1, ctx->d_eval_lay + 2 * MAXL, Ev, dlo, dhi, ctx->stream));
+    CK(launch_eval_nodes(ctx->F, ctx->S, Ew, ctx->stream));
+    prof_end(ctx, pe);
+    ctx->stats.launches += 4;
+    std::vector<unsigned long long> h(nwords);
+    CK(cudaMemcpyAsync(h.data(), b, sizeof(unsigned long long) * nwords, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.d2h_bytes += (int64_t)(8 * nwords);
+    // Eq. (3): per layer, bins in a fixed order (c > 0 then c == 0, d - c ascending), then layers ascending
+    auto tof = [&](const unsigned long long *hist, int nlay) {
+        double t = 0.0;
+        for (int l = 0; l < nlay; l++) {
+            double acc = 0.0;
+            for (int f = 0; f < 2; f++) {
+                const double sl = f ? ctx->s_zero : ctx->s_pos;
+                for (int i = 0; i < nbins; i++) {
+                    const unsigned long long c = hist[((size_t)l * 2 + f) * nbins + i];
+                    if (c) acc = acc + (double)c * std::exp(sl * (double)(dlo + i));
+                }
+            }
+            t = t + ctx->ofw[l] * acc;
+        }
+        return t;
+    };
+    la_eval r{};
+    r.tof_wire = tof(h.data(), L);
+    r.tof_via = tof(h.data() + nh, L - 1);
+    for (int l = 0; l < MAXL; l++) {
+        r.legacy_wire += (int64_t)h[2 * nh + l];
+        r.legacy_via += (int64_t)h[2 * nh + MAXL + l];
+        r.wirelength[l] = (int64_t)h[2 * nh + 2 * MAXL + 1 + l];
+    }
+    r.out_of_domain = (int64_t)h[2 * nh + 2 * MAXL];
+    r.via_cuts = (int64_t)h[2 * nh + 3 * MAXL + 1];
+    r.wire_cap = 0.0;
+    for (int l = 0; l < L; l++) r.wire_cap = r.wire_cap + ctx->c[l] * (double)r.wirelength[l];
+    *out = r;
     return LA_OK;
 }
 

@@ -119,6 +119,20 @@ cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64
 cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
                           int64_t net_end, cudaStream_t s);
 
+// Evaluator (la_kernels.cu): histogram of (layer, c == 0, clamp(d - c)) over one packed
+// plane with `slots` layers per element group (slot -> layer via layer_of), exact
+// legacy sum of max(0, d - c) per layer, and the out-of-domain count.
+struct EvalDev {
+    unsigned long long *hist;                 // [MAXL][2][nbins], nbins = delta_hi - delta_lo + 1
+    unsigned long long *legacy;               // [MAXL]
+    unsigned long long *oob;                  // [1]
+    unsigned long long *wl;                   // [MAXL] unit wire edges per layer (k_eval_nodes)
+    unsigned long long *vcuts;                // [1]
+};
+cudaError_t launch_eval_plane(const int32_t *words, int64_t n, int slots, const int8_t *layer_of_slot, EvalDev E,
+                              int delta_lo, int delta_hi, cudaStream_t s);
+cudaError_t launch_eval_nodes(const DevForest &F, const DevScratch &S, EvalDev E, cudaStream_t s);
+
 // GPU conflict-free batching (la_batch.cu): keys = (element << 32) | rank,
 // returns batch id per rank (host vector) and the number of batches.  The
 // predecessor DAG (successor CSR over ranks, in-degrees) stays on the device in

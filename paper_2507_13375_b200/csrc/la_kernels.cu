@@ -13,6 +13,8 @@
 // reductions are min/argmin only, with a total-order key.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "la_device.cuh"
 #include "la_internal.h"
 
@@ -241,4 +243,118 @@ cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch
     return cudaGetLastError();
 }
 
+}  // namespace gapla
+
+// ------------------------------------------------------------------ evaluator
+// k_eval_plane (PAPER Eq. (2)/(3) l.174-182): one pass over a packed
+// demand plane (the element of slot s of group i is words[i * slots + s]).  Every word gives
+// d - c (w >> 1) and the zero-capacity flag (w & 1); counts per (layer, flag, d - c) go to a
+// shared-memory window of d - c (warp-aggregated with __match_any_sync), the rest straight
+// to the global bins; max(0, d - c) is summed exactly per layer.  HBM-bound: 4 B per element,
+// read once with 16-byte loads; grid = a multiple of the SM count.
+namespace gapla {
+namespace {
+constexpr int EV_LO = -64, EV_W = 128;             // shared window of d - c
+constexpr int EV_THREADS = 512;
+
+__device__ __forceinline__ void eval_word(int32_t w, int slot, uint32_t (*sh)[2][EV_W], unsigned long long *shleg,
+                                          const int8_t *layer_of, EvalDev &E, int dlo, int dhi, int nbins) {
+    const int d = w >> 1, f = w & 1;
+    if (d > 0) atomicAdd(&shleg[slot], (unsigned long long)d);
+    if (d >= EV_LO && d < EV_LO + EV_W) {
+        const unsigned key = ((unsigned)slot << 8) | ((unsigned)f << 7) | (unsigned)(d - EV_LO);
+        const unsigned peers = __match_any_sync(__activemask(), key);
+        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&sh[slot][f][d - EV_LO], __popc(peers));
+    } else {
+        const int dc = min(max(d, dlo), dhi);
+        if (dc != d) atomicAdd(E.oob, 1ull);
+        atomicAdd(&E.hist[((int)layer_of[slot] * 2 + f) * nbins + (dc - dlo)], 1ull);
+    }
+}
+
+__global__ void __launch_bounds__(EV_THREADS) k_eval_plane(const int32_t *__restrict__ words, int64_t n, int slots,
+                                                           const int8_t *__restrict__ layer_of, EvalDev E, int dlo,
+                                                           int dhi) {
+    __shared__ uint32_t sh[MAXL][2][EV_W];
+    __shared__ unsigned long long shleg[MAXL];
+    for (int i = threadIdx.x; i < MAXL * 2 * EV_W; i += blockDim.x) (&sh[0][0][0])[i] = 0;
+    if (threadIdx.x < MAXL) shleg[threadIdx.x] = 0;
+    __syncthreads();
+    const int nbins = dhi - dlo + 1;
+    const int64_t n4 = n / 4;
+    const int4 *w4 = reinterpret_cast<const int4 *>(words);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int slot = (int)((4 * i0) % slots);                  // slot of word 4i, advanced without 64-bit modulo
+    const int step = (int)((4 * stride) % slots);
+    for (int64_t i = i0; i < n4; i += stride) {
+        const int4 v = __ldcs(w4 + i);
+        int s1 = slot + 1, s2 = slot + 2, s3 = slot + 3;
+        s1 -= s1 >= slots ? slots : 0;
+        s2 = s2 >= slots ? s2 - slots : s2;
+        s2 -= s2 >= slots ? slots : 0;
+        s3 = s3 % slots;
+        eval_word(v.x, slot, sh, shleg, layer_of, E, dlo, dhi, nbins);
+        eval_word(v.y, s1, sh, shleg, layer_of, E, dlo, dhi, nbins);
+        eval_word(v.z, s2, sh, shleg, layer_of, E, dlo, dhi, nbins);
+        eval_word(v.w, s3, sh, shleg, layer_of, E, dlo, dhi, nbins);
+        slot += step;
+        slot -= slot >= slots ? slots : 0;
+    }
+    for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += stride)
+        eval_word(words[e], (int)(e % slots), sh, shleg, layer_of, E, dlo, dhi, nbins);
+    __syncthreads();
+    for (int i = threadIdx.x; i < slots * 2 * EV_W; i += blockDim.x) {
+        const int s = i / (2 * EV_W), f = (i / EV_W) & 1, b = i % EV_W;
+        const uint32_t c = sh[s][f][b];
+        const int d = EV_LO + b;
+        if (c) atomicAdd(&E.hist[((int)layer_of[s] * 2 + f) * nbins + (min(max(d, dlo), dhi) - dlo)], (unsigned long long)c);
+        if (c && (d < dlo || d > dhi)) atomicAdd(E.oob, (unsigned long long)c);
+    }
+    if (threadIdx.x < slots && shleg[threadIdx.x]) atomicAdd(&E.legacy[layer_of[threadIdx.x]], shleg[threadIdx.x]);
+}
+
+// k_eval_nodes: unit wire edges per layer (len of every parent run on its layer) and via cuts.
+__global__ void __launch_bounds__(256) k_eval_nodes(DevForest F, DevScratch S, EvalDev E) {
+    __shared__ unsigned long long wl[MAXL];
+    __shared__ unsigned long long vc;
+    if (threadIdx.x < MAXL) wl[threadIdx.x] = 0;
+    if (threadIdx.x == 0) vc = 0;
+    __syncthreads();
+    unsigned long long myv = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.n_nodes; i += stride) {
+        const int l = S.lay[i];
+        if (F.edir[i] != NO_DIR) atomicAdd(&wl[l], (unsigned long long)F.len[i]);
+        myv += (unsigned)(S.st[i] - S.sb[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) myv += __shfl_xor_sync(FULL_MASK, myv, o);
+    if ((threadIdx.x & 31) == 0 && myv) atomicAdd(&vc, myv);
+    __syncthreads();
+    if (threadIdx.x < MAXL && wl[threadIdx.x]) atomicAdd(&E.wl[threadIdx.x], wl[threadIdx.x]);
+    if (threadIdx.x == 0 && vc) atomicAdd(E.vcuts, vc);
+}
+}  // namespace
+
+static int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+cudaError_t launch_eval_plane(const int32_t *words, int64_t n, int slots, const int8_t *layer_of_slot, EvalDev E,
+                              int delta_lo, int delta_hi, cudaStream_t s) {
+    if (n <= 0 || slots <= 0) return cudaSuccess;
+    const int64_t want = (n / 4 + EV_THREADS - 1) / EV_THREADS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 4));
+    k_eval_plane<<<grid, EV_THREADS, 0, s>>>(words, n, slots, layer_of_slot, E, delta_lo, delta_hi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_nodes(const DevForest &F, const DevScratch &S, EvalDev E, cudaStream_t s) {
+    if (F.n_nodes <= 0) return cudaSuccess;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((F.n_nodes + 255) / 256, (int64_t)sm_count() * 8));
+    k_eval_nodes<<<grid, 256, 0, s>>>(F, S, E);
+    return cudaGetLastError();
+}
 }  // namespace gapla

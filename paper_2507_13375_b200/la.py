@@ -49,6 +49,16 @@ class la_net_desc(ctypes.Structure):
                 ("wns", c_f64)]
 
 
+class la_eval(ctypes.Structure):
+    _fields_ = [("tof_wire", c_f64), ("tof_via", c_f64), ("legacy_wire", c_i64), ("legacy_via", c_i64),
+                ("wirelength", c_i64 * 16), ("via_cuts", c_i64), ("wire_cap", c_f64), ("out_of_domain", c_i64)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["wirelength"] = list(self.wirelength)
+        return d
+
+
 class la_stats(ctypes.Structure):
     _fields_ = [("n_nets", c_i64), ("n_pins", c_i64), ("n_nodes", c_i64), ("n_sinks", c_i64),
                 ("wirelength", c_i64), ("footprint", c_i64), ("n_batches", c_i32), ("max_height", c_i32),
@@ -63,7 +73,7 @@ class la_stats(ctypes.Structure):
 class la_profile(ctypes.Structure):
     _fields_ = [("assign_launches", c_i64), ("commit_launches", c_i64), ("elmore_launches", c_i64),
                 ("reconcile_calls", c_i64), ("assign_ms", c_f64), ("commit_ms", c_f64), ("elmore_ms", c_f64),
-                ("reconcile_ms", c_f64)]
+                ("reconcile_ms", c_f64), ("eval_launches", c_i64), ("eval_ms", c_f64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -82,6 +92,7 @@ def _load():
         "la_assign_all": ([c_void_p], c_i32),
         "la_set_schedule": ([c_void_p, c_i32], c_i32),
         "la_set_tracing": ([c_void_p, c_i32], c_i32),
+        "la_eval_overflow": ([c_void_p, P(la_eval)], c_i32),
         "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
@@ -108,7 +119,7 @@ _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
-           "la_set_schedule", "la_set_tracing", "la_get_trace")
+           "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow")
 
 
 def _check(st):
@@ -175,6 +186,12 @@ LA_SCHED_DATAFLOW, LA_SCHED_BATCH = 0, 1
 
 def la_set_schedule(ctx, schedule: int):
     _check(_lib.la_set_schedule(ctx, int(schedule)))
+
+
+def la_eval_overflow(ctx) -> dict:
+    out = la_eval()
+    _check(_lib.la_eval_overflow(ctx, ctypes.byref(out)))
+    return out.as_dict()
 
 
 def la_set_tracing(ctx, enable: bool):
@@ -312,6 +329,10 @@ class LayerAssigner:
         nr = np.zeros(d.n_nets, np.float64)
         la_eval_timing(self.ctx, sd, nc, nr)
         return dict(sink_delay=sd, net_cap=nc, net_rc=nr)
+
+    def eval_overflow(self):
+        """la_eval_overflow: Eq. (3)/(2) total overflow, wirelength per layer, via cuts, wire C."""
+        return la_eval_overflow(self.ctx)
 
     def solution(self):
         return la_get_solution(self.ctx, self.d.n_nets)

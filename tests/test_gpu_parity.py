@@ -271,3 +271,25 @@ def test_config5_full_scale_properties(la):
         p0 = int(d.pin_ptr[net])
         np.testing.assert_allclose(got["sink_delay"][p0:p0 + len(pins)], delays, rtol=1e-9, atol=1e-15)
         np.testing.assert_allclose([got["net_cap"][net], got["net_rc"][net]], [ncap, nrc], rtol=1e-9)
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, None)])
+def test_evaluator_parity(la, cfg, n):
+    """la_eval_overflow (NEXT #3) vs oracle.evaluate on the oracle's own solution and demand:
+    integers (Eq. (2) totals, wirelength per layer, via cuts) exact; the Eq. (3) totals and
+    wire C within 1e-12 of the correctly rounded sums (the library bins elements exactly and
+    sums count * ofw * e^{s(d-c)} per layer: a few roundings per bin, DESIGN §5 k_eval)."""
+    d = synth.make_config(cfg, n_nets=n)
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.assign_all()
+    ev = A.eval_overflow()
+    A.close()
+    ref = oracle.run(d)
+    ex = oracle.evaluate(d, ref["wire_dem"], ref["via_dem"], ref["wires"], ref["vias"])
+    assert ev["out_of_domain"] == 0
+    for k in ("legacy_wire", "legacy_via", "via_cuts"):
+        assert ev[k] == ex[k], k
+    assert ev["wirelength"] == ex["wirelength"]
+    for k in ("tof_wire", "tof_via", "wire_cap"):
+        assert abs(ev[k] - ex[k]) <= 1e-12 * abs(ex[k]), (k, ev[k], ex[k])

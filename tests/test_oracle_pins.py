@@ -331,3 +331,35 @@ def test_tie_break_span_key():
     r = oracle.run(d)
     assert int(r["wires"][0][4]) == 0
     assert [tuple(int(t) for t in v) for v in r["vias"]] == [(0, 0, 0, 1), (4, 0, 0, 1)]
+
+
+def test_evaluator_closed_forms():
+    """oracle.evaluate (NEXT #3) against Eq. (3)/(2) closed forms: an edge with d = c
+    contributes ofw(l) (e^0); c = 0, d = 2 contributes ofw(l) e^3 and d = c - 4 (c > 0)
+    ofw(l) e^-2 (golden values, tests/golden/closed_forms.json); Eq. (2)
+    counts only the positive excess.  Wirelength, via cuts and wire C by hand."""
+    g = golden("closed_forms.json")["eq3"]
+    d = synth.empty_design(3, 3, 2, cap_wire=5, cap_via=4)
+    sizes = d.wire_layer_sizes()              # layer 0 (H): 2*3 edges, layer 1 (V): 3*2 edges
+    assert list(sizes) == [6, 6]
+    wcap = d.wire_cap.copy()
+    wdem = wcap.copy()                        # every edge d = c ...
+    wcap[0], wdem[0] = 0, 2                   # ... but edge 0 of layer 0: c = 0, d = 2
+    wdem[7] = wcap[7] - 4                     # and edge 1 of layer 1: d = c - 4
+    d.wire_cap = wcap
+    vcap = d.via_cap.copy()
+    vdem = vcap.copy()
+    vdem[4] = vcap[4] + 3                     # one via cut 3 over capacity
+    d.via_cap = vcap
+    wires = [(0, 0, 2, 0, 0), (1, 0, 1, 2, 1)]   # 2 unit edges on layer 0, 2 on layer 1
+    vias = [(0, 0, 0, 1), (1, 2, 0, 1)]
+    ev = oracle.evaluate(d, wdem, vdem, wires, vias)
+    ofw0, ofw1 = float(d.ofw[0]), float(d.ofw[1])
+    want_w = ofw0 * (5 + g["state_c0_d2"]) + ofw1 * (5 + g["state_d_eq_c_minus_4_cpos"])
+    assert abs(ev["tof_wire"] - want_w) <= 1e-12 * want_w
+    want_v = ofw0 * (8 + np.e ** 1.5)        # 8 cuts at d = c, one at d = c + 3 (c > 0: s = 0.5 -> e^1.5)
+    assert abs(ev["tof_via"] - want_v) <= 1e-12 * want_v
+    assert ev["legacy_wire"] == 2 and ev["legacy_via"] == 3
+    assert ev["wirelength"][:2] == [2, 2] and sum(ev["wirelength"]) == 4
+    assert ev["via_cuts"] == 2
+    assert abs(ev["wire_cap"] - (2 * d.c[0] + 2 * d.c[1])) <= 1e-15
