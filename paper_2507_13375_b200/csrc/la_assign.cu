@@ -231,7 +231,7 @@ __device__ __forceinline__ int window_argmin(const WarpScr &w, const Shared &sh,
 // segmented scans -- upward from b0 (strict <: the lower layer keeps ties) and
 // downward from t0 (the lower layer wins ties) -- and a butterfly argmin by the
 // key (G', t-b, b) picks each entry's span.
-__device__ __forceinline__ void node_dp_1son(const NetCtx &c, const WarpScr &w, const Shared &sh, const DevGrid &G,
+__device__ __forceinline__ void node_dp_1son(const NetCtx &c, WarpScr &w, const Shared &sh, const DevGrid &G,
                                              int i, bool root, int pdrv, int dt, int nE, int kk, int dk, int lane) {
     const NetBuf &nb = c.nb;
     const NodeRec &nd = nb.nd[i];
@@ -292,16 +292,26 @@ __device__ __forceinline__ void node_dp_1son(const NetCtx &c, const WarpScr &w, 
             const int oj = __shfl_xor_sync(FULL_MASK, jm, o, 8);
             if (oG < Gp || (oG == Gp && ok < key)) { Gp = oG; key = ok; jm = oj; }
         }
-        if (eok && s == 0) {
+        if (s == 0 && e < nE) {
+            w.el[e] = (uint8_t)l;
+            w.bestK[e] = eok ? (key | ((uint32_t)(jm & 0xf) << 12)) : 0x1ffu;
+        }
+    }
+    __syncwarp();
+    // entry lanes finish in parallel: G (cost, not cost'), K = capb (O6)
+    if (lane < nE) {
+        const int e = lane, l = w.el[e];
+        const uint32_t key = w.bestK[e];
+        if (root || sh.routable[l]) {
             const int slot = root ? 0 : e;
             if (key & 0x100u) {
                 if (root) *nb.froot = dinf();
                 else nb.sl[i * LD + slot].A = dinf();
             } else {
-                const int b = key & 0xf, t = b + (int)(key >> 4);
+                const int b = key & 0xf, t = b + (int)((key >> 4) & 0xf), jm = (int)(key >> 12);
                 const SlotRec &rr = nb.sl[kk * LD + sh.lidx[jm]];
                 const double Bv = wdk * rr.C;
-                const double Gv = w.Vt[b * MAXL + t] + (rr.A + Bv * sh.T.VR[l * MAXL + jm]);   // G: cost, not cost'
+                const double Gv = w.Vt[b * MAXL + t] + (rr.A + Bv * sh.T.VR[l * MAXL + jm]);
                 finish_layer(c, sh, G, i, root, l, slot, Gv, 0.0 + rr.C, b, t, (uint32_t)jm);
             }
         }
