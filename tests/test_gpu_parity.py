@@ -293,3 +293,19 @@ def test_evaluator_parity(la, cfg, n):
     assert ev["wirelength"] == ex["wirelength"]
     for k in ("tof_wire", "tof_via", "wire_cap"):
         assert abs(ev[k] - ex[k]) <= 1e-12 * abs(ex[k]), (k, ev[k], ex[k])
+
+
+@pytest.mark.parametrize("variant", ["no_lookahead", "no_timing", "heavy_timing"])
+def test_ablation_variants(la, variant):
+    """the 'w/o ahead' ablation (Table IV: ur = 0, i.e.
+    r_avg = 0 and r_drv = 0, so cost' = cost) and the W_D sweep ends are input switches of the
+    same hot path: parity with the oracle under each."""
+    d = synth.generate(n_nets=20_000, X=96, Y=96, L=10, seed=97, pin_max=63, rdrv_mode=1)
+    if variant == "no_lookahead":
+        d.r_avg = 0.0
+        d.r_drv = np.zeros_like(d.r_drv)
+    elif variant == "no_timing":
+        d.W_D = 0.0
+    else:
+        d.W_D = 1e4
+    assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
