@@ -194,6 +194,18 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch);
  * (DESIGN §2).  Both are bit-identical to sequential assignment. */
 la_status la_assign_all(la_ctx *ctx);
 
+/* Paper-style snapshot batches (PAPER §III-A l.224-226 "nets in a
+ * subset are assigned in parallel", Alg. 1 l.257-260, Alg. 2 l.345; reading R31).  Call
+ * before la_load_nets.  batch_of[n_nets] (>= 0, input net order) replaces the conflict-free
+ * batching: batches run in ascending id, every net of a batch reads the demand at the
+ * start of its batch, and the batch's commits are applied after it (k_commit), so results
+ * are deterministic but may differ from sequential assignment when nets of one batch
+ * share GCell edges (the paper's "minimal quality degradation").  batch_of == NULL restores
+ * conflict-free batching.  Forces LA_SCHED_BATCH.  Errors: LA_ESTATE after la_load_nets,
+ * LA_EINVAL for a negative count; a negative id or a count that differs from the net
+ * descriptor's is reported by la_load_nets (LA_EINVAL). */
+la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t n_nets);
+
 /* Schedule used by la_assign_all on one rank; LA_SCHED_BATCH is the default. */
 enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an unknown value */

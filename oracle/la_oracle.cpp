@@ -89,6 +89,11 @@ struct OOut {
     double elapsed_s;             // DP + backtrack + commit + Elmore of the nets run
     int64_t nets_run;
     char err[256];
+    // SURVEY §8(f) NEXT #1 (paper-style batches, PAPER §III-A l.224-226, reading R31): when
+    // non-NULL, snap_batch[net] is the net's batch; batches run in ascending id, every net of a
+    // batch reads the demand at the start of its batch, and the batch's commits are applied
+    // after all its nets (integer adds: their order does not matter).  NULL: sequential.
+    const int32_t *snap_batch;
 };
 
 }  // extern "C"
@@ -576,6 +581,16 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     if (nets->order_key)
         std::stable_sort(order.begin(), order.end(),
                          [&](int64_t a, int64_t b) { return nets->order_key[a] < nets->order_key[b]; });
+    const int32_t *snap = out->snap_batch;
+    if (snap)   // batches in ascending id; inside a batch the order is immaterial (snapshot reads)
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return snap[a] < snap[b]; });
+    std::vector<int64_t> pend_w, pend_v;   // snapshot mode: commits deferred to the end of the batch
+    auto flush = [&]() {
+        for (int64_t i : pend_w) C.wdem[i] += 1;
+        for (int64_t i : pend_v) C.vdem[i] += 1;
+        pend_w.clear();
+        pend_v.clear();
+    };
     int64_t nrun = (out->max_nets_to_run > 0 && out->max_nets_to_run < NN) ? out->max_nets_to_run : NN;
 
     // batch recurrence: footprint = unit edges U node GCells; element spaces disjoint
@@ -593,6 +608,7 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     NetState st;
     for (int64_t oi = 0; oi < nrun; oi++) {
         int64_t net = order[oi];
+        if (snap && oi > 0 && snap[net] != snap[order[oi - 1]]) flush();
         NetView nv{nets->pin_ptr[net], nets->pin_ptr[net + 1], nets->seg_ptr[net], nets->seg_ptr[net + 1]};
         if (nv.p1 <= nv.p0) { std::snprintf(out->err, 256, "net %lld: no pins", (long long)net); return -1; }
         for (int64_t p = nv.p0; p < nv.p1; p++)
@@ -650,10 +666,14 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
                         case DIR_N: idx = wire_index(C, j, x, y - len + i); break;
                         default:    idx = wire_index(C, j, x, y + i); break;
                     }
-                    C.wdem[idx] += 1;
+                    if (snap) pend_w.push_back(idx);
+                    else C.wdem[idx] += 1;
                 }
             }
-            for (int k = st.sb[n]; k < st.st[n]; k++) C.vdem[via_index(C, k, T.x[n], T.y[n])] += 1;
+            for (int k = st.sb[n]; k < st.st[n]; k++) {
+                if (snap) pend_v.push_back(via_index(C, k, T.x[n], T.y[n]));
+                else C.vdem[via_index(C, k, T.x[n], T.y[n])] += 1;
+            }
         }
         // O9 Elmore
         double ncap = 0, nrc = 0;
@@ -692,6 +712,7 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
             out->batch_of[net] = b;
         }
     }
+    flush();
     out->elapsed_s = elapsed;
     out->nets_run = nrun;
     if (out->wire_ptr) {

@@ -51,7 +51,7 @@ class OOut(ctypes.Structure):
                 ("via_ptr", P(c_i64)), ("vias", P(c_i32)), ("wire_dem", P(c_i32)), ("via_dem", P(c_i32)),
                 ("sink_delay", P(c_f64)), ("net_cap", P(c_f64)), ("net_rc", P(c_f64)),
                 ("batch_of", P(c_i32)), ("n_nodes", P(c_i32)), ("elapsed_s", c_f64), ("nets_run", c_i64),
-                ("err", ctypes.c_char * 256)]
+                ("err", ctypes.c_char * 256), ("snap_batch", P(c_i32))]
 
 
 _lib = None
@@ -113,10 +113,11 @@ def _nets(d, keep):
 
 
 def run(d, solution: bool = True, grids: bool = True, timing: bool = True, batches: bool = True,
-        max_nets: int = 0) -> dict:
+        max_nets: int = 0, snap_batch=None) -> dict:
     """Sequential oracle over design ``d`` (gen.synth.Design).  Returns numpy arrays:
     net_cost, wire_ptr/wires, via_ptr/vias, wire_dem, via_dem, sink_delay, net_cap,
-    net_rc, batch_of, n_nodes, elapsed_s, nets_run."""
+    net_rc, batch_of, n_nodes, elapsed_s, nets_run.  ``snap_batch`` (int32 per net):
+    paper-style snapshot batches (NEXT #1, reading R31) instead of sequential commits."""
     lib = _load()
     keep = []
     g = _grid(d, keep)
@@ -137,6 +138,10 @@ def run(d, solution: bool = True, grids: bool = True, timing: bool = True, batch
     o.max_wires = res["wires"].shape[0] if solution else 0
     o.max_vias = res["vias"].shape[0] if solution else 0
     o.max_nets_to_run = max_nets
+    if snap_batch is not None:
+        snap_batch = np.ascontiguousarray(snap_batch, np.int32)
+        keep.append(snap_batch)
+        o.snap_batch = _ptr(snap_batch, c_i32)
     for k, ct in (("net_cost", c_f64), ("wire_ptr", c_i64), ("wires", c_i32), ("via_ptr", c_i64), ("vias", c_i32),
                   ("wire_dem", c_i32), ("via_dem", c_i32), ("sink_delay", c_f64), ("net_cap", c_f64),
                   ("net_rc", c_f64), ("batch_of", c_i32), ("n_nodes", c_i32)):

@@ -112,6 +112,7 @@ struct la_ctx {
     int4 *d_flow_big_pos = nullptr, *d_flow_small_pos = nullptr;     // dataflow priority order
     std::vector<int64_t> h_net_sink0;                                // [n_nets+1] first sink per position
     int32_t n_big_ctas = 0;
+    std::vector<int32_t> snap_batch;          // la_set_snapshot_batches (input order); empty: conflict-free
     bool hybrid = true;                       // batch-mode launches: all CTAs take big nets first
     bool tracing = false;
     // tickets and the dataflow DAG (device)
@@ -888,7 +889,18 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     std::vector<int32_t> batch_of_rank;
     int32_t nb = 0;
     DagDev dag;
-    {
+    const bool snapshot = !ctx->snap_batch.empty();
+    if (snapshot) {
+        // paper-style batches (NEXT #1, R31): the caller's ids, no conflict DAG
+        if ((int64_t)ctx->snap_batch.size() != N) return set_err(LA_EINVAL, "snapshot batches: wrong net count");
+        batch_of_rank.resize(N);
+        for (int64_t r = 0; r < N; r++) {
+            const int32_t b = ctx->snap_batch[by_rank[r]];
+            if (b < 0) return set_err(LA_EINVAL, "snapshot batches: negative batch id");
+            batch_of_rank[r] = b;
+            nb = std::max(nb, b + 1);
+        }
+    } else {
         cudaError_t e = gpu_conflict_batches(keys.data(), n_fp, elem_bits, N, batch_of_rank, nb, ctx->stream,
                                              &ctx->stats.launches, &dag);
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "conflict-free batching"); }
@@ -960,8 +972,17 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->batch_small0.push_back((int64_t)small_pos.size());
     }
     phase("role lists");
-    // dataflow DAG in forest order
-    {
+    // dataflow DAG in forest order (snapshot batches: none -- every net has 0 predecessors)
+    if (snapshot) {
+        std::vector<int64_t> zoff(N + 1, 0);
+        TRY(dev_upload(ctx, &ctx->d_succ_off, zoff.data(), N + 1));
+        TRY(dev_alloc(ctx, &ctx->d_succ, 1));
+        TRY(dev_alloc(ctx, &ctx->d_indeg, std::max<int64_t>(N, 1)));
+        CK(cudaMemsetAsync(ctx->d_indeg, 0, sizeof(int32_t) * std::max<int64_t>(N, 1), ctx->stream));
+        for (int i = 0; i < 3; i++) ctx->dev_allocs.pop_back();   // owned by the ctx fields, freed in ~la_ctx
+        ctx->fuse_commit = false;                                  // commits after the whole batch (snapshot)
+        ctx->schedule = LA_SCHED_BATCH;
+    } else {
         std::vector<int64_t> rank_of_net(N), rank_of_pos(N);
         for (int64_t r = 0; r < N; r++) rank_of_net[by_rank[r]] = r;
         for (int64_t p = 0; p < N; p++) rank_of_pos[p] = rank_of_net[pos_net[p]];
@@ -1325,7 +1346,21 @@ la_status la_assign_all(la_ctx *ctx) {
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule) {
     if (!ctx) return set_err(LA_EINVAL, "null context");
     if (schedule != LA_SCHED_DATAFLOW && schedule != LA_SCHED_BATCH) return set_err(LA_EINVAL, "unknown schedule");
+    if (!ctx->snap_batch.empty() && schedule == LA_SCHED_DATAFLOW)
+        return set_err(LA_EINVAL, "snapshot batches run batch by batch (no dataflow schedule)");
     ctx->schedule = schedule;
+    return LA_OK;
+}
+
+la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t n_nets) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (ctx->loaded) return set_err(LA_ESTATE, "snapshot batches must be set before la_load_nets");
+    if (!batch_of) {
+        ctx->snap_batch.clear();
+        return LA_OK;
+    }
+    if (n_nets < 0) return set_err(LA_EINVAL, "negative net count");
+    ctx->snap_batch.assign(batch_of, batch_of + n_nets);
     return LA_OK;
 }
 

@@ -93,6 +93,7 @@ def _load():
         "la_set_schedule": ([c_void_p, c_i32], c_i32),
         "la_set_tracing": ([c_void_p, c_i32], c_i32),
         "la_eval_overflow": ([c_void_p, P(la_eval)], c_i32),
+        "la_set_snapshot_batches": ([c_void_p, P(c_i32), c_i64], c_i32),
         "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
@@ -119,7 +120,7 @@ _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
-           "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow")
+           "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches")
 
 
 def _check(st):
@@ -192,6 +193,14 @@ def la_eval_overflow(ctx) -> dict:
     out = la_eval()
     _check(_lib.la_eval_overflow(ctx, ctypes.byref(out)))
     return out.as_dict()
+
+
+def la_set_snapshot_batches(ctx, batch_of):
+    if batch_of is None:
+        _check(_lib.la_set_snapshot_batches(ctx, None, 0))
+        return
+    b = np.ascontiguousarray(batch_of, np.int32)
+    _check(_lib.la_set_snapshot_batches(ctx, b.ctypes.data_as(P(c_i32)), b.shape[0]))
 
 
 def la_set_tracing(ctx, enable: bool):
@@ -306,7 +315,10 @@ class LayerAssigner:
         n.wns = d.wns
         return n
 
-    def load(self, d=None) -> int:
+    def load(self, d=None, snapshot_batches=None) -> int:
+        """la_load_nets; ``snapshot_batches`` (int32 per net): paper-style batches (NEXT #1)."""
+        if snapshot_batches is not None:
+            la_set_snapshot_batches(self.ctx, snapshot_batches)
         self.n_batches = la_load_nets(self.ctx, self.net_desc(d))
         return self.n_batches
 

@@ -309,3 +309,32 @@ def test_ablation_variants(la, variant):
     else:
         d.W_D = 1e4
     assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
+
+
+@pytest.mark.parametrize("kind", ["random20", "all_in_one", "conflict_free", "size_cap"])
+def test_snapshot_batches_parity(la, kind):
+    """Paper-style snapshot batches (NEXT #1, la_set_snapshot_batches): GPU == oracle snapshot
+    mode, bit for bit, for arbitrary partitions -- including one batch of everything (every
+    net reads the initial demand) and the conflict-free batches (== sequential)."""
+    d = synth.make_config(2, n_nets=30_000)
+    rng = np.random.default_rng(5)
+    rank = np.argsort(np.argsort(d.order_key, kind="stable"), kind="stable")
+    if kind == "random20":
+        sb = rng.integers(0, 20, d.n_nets).astype(np.int32)
+    elif kind == "all_in_one":
+        sb = np.zeros(d.n_nets, np.int32)
+    elif kind == "conflict_free":
+        sb = oracle.run(d, solution=False, grids=False, timing=False)["batch_of"]
+    else:
+        sb = (rank // 4096).astype(np.int32)            # priority order cut into batches of 4096
+    A = la.LayerAssigner(d, device=0)
+    nb = A.load(snapshot_batches=sb)
+    assert nb == int(sb.max()) + 1
+    got = A.run()
+    A.close()
+    ref = oracle.run(d, snap_batch=sb)
+    ref["batch_of"] = sb
+    assert_parity(got, ref, bitwise_fp=True)
+    if kind == "conflict_free":
+        seq = oracle.run(d)
+        assert np.array_equal(seq["wires"], ref["wires"]) and np.array_equal(seq["wire_dem"], ref["wire_dem"])

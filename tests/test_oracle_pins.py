@@ -363,3 +363,30 @@ def test_evaluator_closed_forms():
     assert ev["wirelength"][:2] == [2, 2] and sum(ev["wirelength"]) == 4
     assert ev["via_cuts"] == 2
     assert abs(ev["wire_cap"] - (2 * d.c[0] + 2 * d.c[1])) <= 1e-15
+
+
+def test_snapshot_batches_reduce_to_known_schedules():
+    """Oracle snapshot batches (NEXT #1, reading R31) pinned by the two schedules it must reduce
+    to: one net per batch is sequential assignment; a batch of nets that pairwise share no
+    footprint element (the conflict-free recurrence) is sequential too; and
+    one batch of everything gives every net the initial demand, i.e. the solution of running
+    each net alone on the initial grid."""
+    d = tiny_pool(81, 6, n=120, X=8, Y=8, pin_max=5)
+    seq = oracle.run(d)
+    one_each = oracle.run(d, snap_batch=np.argsort(np.argsort(d.order_key, kind="stable"), kind="stable"))
+    for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost"):
+        assert np.array_equal(one_each[k], seq[k]), k
+    cf = oracle.run(d, snap_batch=seq["batch_of"])
+    for k in ("wires", "vias", "wire_dem", "via_dem", "net_cost"):
+        assert np.array_equal(cf[k], seq[k]), k
+    allin = oracle.run(d, snap_batch=np.zeros(d.n_nets, np.int32))
+    wires, vias = [], []
+    for j in range(d.n_nets):
+        r = oracle.run(single_net(d, j))
+        wires.append(r["wires"])
+        vias.append(r["vias"])
+        assert r["net_cost"][0] == allin["net_cost"][j]
+    assert np.array_equal(np.concatenate(wires), allin["wires"])
+    assert np.array_equal(np.concatenate(vias) if vias else allin["vias"], allin["vias"])
+    wd, vd = rebuild_demand(d, allin["wires"], allin["vias"])
+    assert np.array_equal(wd, allin["wire_dem"]) and np.array_equal(vd, allin["via_dem"])
