@@ -221,3 +221,20 @@ def with_nets(d: Design, nets) -> Design:
     d.seg_xy = np.array(sxy, np.int32).reshape(-1, 4)
     d.r_drv = np.array(rd, np.float64); d.order_key = np.array(ok, np.int64)
     return d
+
+
+def criticality(d: Design, seed: int = 7) -> np.ndarray:
+    """Synthetic net criticality (number of critical paths through a net), the STA
+    output Alg. 1 line 2 would give: nets whose worst sink slack is below 0.7 WNS get a count
+    that grows as the slack approaches WNS (a few up to ~12), the rest 0-1.  Input
+    generation only (no method arithmetic)."""
+    rng = np.random.default_rng(seed)
+    n = d.n_nets
+    slack = np.full(n, np.inf)
+    sinks = np.ones(d.n_pins, bool)
+    sinks[d.pin_ptr[:-1]] = False
+    idx = np.repeat(np.arange(n), np.diff(d.pin_ptr))
+    np.minimum.at(slack, idx[sinks], d.pin_slack[sinks])
+    ratio = np.where(np.isfinite(slack), slack / d.wns, 0.0)
+    base = np.where(ratio > 0.7, 12.0 * (ratio - 0.7) / 0.3, 0.0)
+    return np.floor(base * rng.uniform(0.5, 1.5, n) + rng.uniform(0, 1.5, n)).astype(np.int32)

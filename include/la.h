@@ -206,6 +206,27 @@ la_status la_assign_all(la_ctx *ctx);
  * descriptor's is reported by la_load_nets (LA_EINVAL). */
 la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t n_nets);
 
+/* Alg. 1 lines 3-10 (PAPER §III-A l.213-262): critical-net-analysis
+ * based ordering and batching, given what Alg. 1 lines 1-2 (STA) produce.  Inputs: the net
+ * descriptor (its pin slacks and wns), criticality[n_nets] = number of critical paths through
+ * each net (l.208), alpha (semi-critical ratio, 0.7, l.216-218) and th (3, l.215).  Steps:
+ *   Divide (l.3): critical nets N_c: criticality > th; semi-critical N_s: the rest with net
+ *     slack (minimum over the net's sink slacks, l.217) < alpha * wns; non-critical N_n.
+ *   PartitionAndSort(N_c) (l.4, l.228): bands [C, C], [C/2, C), [C/4, C/2), ... of
+ *     criticality (C = the maximum); inside a band criticality descending, net slack
+ *     ascending, net index.
+ *   PartitionAndSort(N_s) (l.5, l.229, reading R33): bands slack == wns, then
+ *     (f_{k-1} wns, f_k wns] with f_k = 1 - 0.01 k^2 (1, 0.99, 0.96, 0.91, ...; reading R42)
+ *     down to alpha * wns; inside a band net slack ascending, net index.
+ *   Sort(N_n) (l.6, l.230 "congestion-driven"; reading R43): 2D wirelength ascending, index.
+ *   GetBatches (l.7-9, reading R31): every band (and N_n) cut in its order into batches of
+ *     at most max_batch nets; Concat (l.10): N_c's, then N_s's, then N_n's.
+ * Output: batch_of[n_nets] (input order), *n_batches; feed them to la_set_snapshot_batches.
+ * Host code, multithreaded sorts; no context needed.  Errors: LA_EINVAL on NULL arrays,
+ * alpha <= 0, max_batch < 1 or a negative criticality. */
+la_status la_paper_batches(const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
+                           int64_t max_batch, int32_t *batch_of, int32_t *n_batches);
+
 /* Schedule used by la_assign_all on one rank; LA_SCHED_BATCH is the default. */
 enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an unknown value */

@@ -243,3 +243,64 @@ def evaluate(d, wire_dem, via_dem, wires, vias) -> dict:
     return {"tof_wire": math.fsum(tw), "tof_via": math.fsum(tv), "legacy_wire": lw, "legacy_via": lv,
             "wirelength": wl, "via_cuts": int((vias[:, 3] - vias[:, 2]).sum()), "wire_cap": wire_cap,
             "n_wire_terms": len(tw), "n_via_terms": len(tv)}
+
+
+def paper_batches(pin_ptr, pin_slack, seg_ptr, seg_xy, wns, criticality, alpha=0.7, th=3, max_batch=1 << 20):
+    """Alg. 1 lines 3-10 (PAPER §III-A l.213-262) written out step by step
+    in plain Python; readings R31 (GetBatches = size cap), R33 (slack bands (f_{k-1} WNS, f_k WNS]),
+    R42 (f_k = 1 - 0.01 k^2: 1, 0.99, 0.96, ...), R43 (non-critical: 2D wirelength ascending).
+    Returns (batch id per net, number of batches)."""
+    n = len(pin_ptr) - 1
+    net_slack, wl = [], []
+    for j in range(n):
+        sinks = [float(pin_slack[p]) for p in range(int(pin_ptr[j]) + 1, int(pin_ptr[j + 1]))]
+        net_slack.append(min(sinks) if sinks else float("inf"))      # l.217: minimum over its pins
+        w = 0
+        for s in range(int(seg_ptr[j]), int(seg_ptr[j + 1])):
+            x1, y1, x2, y2 = (int(v) for v in seg_xy[s])
+            w += abs(x2 - x1) + abs(y2 - y1)
+        wl.append(w)
+    # line 3: Divide
+    Nc = [j for j in range(n) if criticality[j] > th]
+    Ns = [j for j in range(n) if criticality[j] <= th and wns < 0 and net_slack[j] < alpha * wns]
+    Nn = [j for j in range(n) if j not in set(Nc) | set(Ns)]
+    # line 4: PartitionAndSort(N_c): [C, C], [C/2, C), [C/4, C/2), ...
+    subsets = []
+    if Nc:
+        C = max(criticality[j] for j in Nc)
+        bands = {}
+        for j in Nc:
+            c = criticality[j]
+            k = 0
+            if c < C:
+                k = 1
+                while c < C / 2 ** k:
+                    k += 1
+            bands.setdefault(k, []).append(j)
+        for k in sorted(bands):
+            subsets.append(sorted(bands[k], key=lambda j: (-criticality[j], net_slack[j], j)))
+    # line 5: PartitionAndSort(N_s): slack == WNS, then (f_{k-1} WNS, f_k WNS]
+    if Ns:
+        bands = {}
+        for j in Ns:
+            s = net_slack[j]
+            k = 0
+            if not s <= wns:
+                k = 1
+                while k < 10 and not s <= (1.0 - 0.01 * k * k) * wns:
+                    k += 1
+            bands.setdefault(k, []).append(j)
+        for k in sorted(bands):
+            subsets.append(sorted(bands[k], key=lambda j: (net_slack[j], j)))
+    # line 6: Sort(N_n)
+    if Nn:
+        subsets.append(sorted(Nn, key=lambda j: (wl[j], j)))
+    # lines 7-10: GetBatches per subset, Concat
+    batch = [0] * n
+    nb = 0
+    for sub in subsets:
+        for i in range(0, len(sub), max_batch):
+            for j in sub[i:i + max_batch]:
+                batch[j] = nb
+            nb += 1
+    return np.array(batch, np.int32), nb

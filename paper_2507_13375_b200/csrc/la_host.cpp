@@ -1343,6 +1343,85 @@ la_status la_assign_all(la_ctx *ctx) {
     return LA_OK;
 }
 
+la_status la_paper_batches(const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
+                           int64_t max_batch, int32_t *batch_of, int32_t *n_batches) {
+    if (!n || !criticality || !batch_of || !n_batches) return set_err(LA_EINVAL, "null argument");
+    if (!(alpha > 0.0) || max_batch < 1) return set_err(LA_EINVAL, "alpha must be > 0 and max_batch >= 1");
+    const int64_t N = n->n_nets;
+    if (N > 0 && (!n->pin_ptr || !n->pin_slack || !n->seg_ptr)) return set_err(LA_EINVAL, "bad net descriptor");
+    const double wns = n->wns;
+    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<double> slack(N);
+    std::vector<int64_t> wl(N);
+    par_for(N, nthr, [&](int64_t j) {
+        double m = std::numeric_limits<double>::infinity();
+        for (int64_t p = n->pin_ptr[j] + 1; p < n->pin_ptr[j + 1]; p++) m = std::min(m, n->pin_slack[p]);   // sinks
+        slack[j] = m;
+        int64_t w = 0;
+        for (int64_t s = n->seg_ptr[j]; s < n->seg_ptr[j + 1]; s++) {
+            const int32_t *q = n->seg_xy + 4 * s;
+            w += std::abs(q[2] - q[0]) + std::abs(q[3] - q[1]);
+        }
+        wl[j] = w;
+    });
+    for (int64_t j = 0; j < N; j++)
+        if (criticality[j] < 0) return set_err(LA_EINVAL, "negative criticality");
+    // Divide (l.3): band key per net; (class, band) sorts the subsets in Concat order
+    int32_t C = 0;
+    for (int64_t j = 0; j < N; j++) if (criticality[j] > th) C = std::max(C, criticality[j]);
+    struct Item { int32_t cls, band; int64_t key1; double key2; int64_t idx; };
+    std::vector<Item> it(N);
+    par_for(N, nthr, [&](int64_t j) {
+        Item &x = it[j];
+        x.idx = j;
+        if (criticality[j] > th) {                               // N_c: bands [C/2^k, C/2^(k-1)), [C, C] first
+            x.cls = 0;
+            int b = 0;
+            if (criticality[j] < C) {
+                b = 1;
+                while ((double)criticality[j] < (double)C / std::ldexp(1.0, b)) b++;
+            }
+            x.band = b;
+            x.key1 = -(int64_t)criticality[j];
+            x.key2 = slack[j];
+        } else if (wns < 0.0 && slack[j] < alpha * wns) {       // N_s: bands of net slack (R33, R42)
+            x.cls = 1;
+            int b = 0;
+            if (!(slack[j] <= wns)) {
+                b = 1;
+                while (b < 10 && !(slack[j] <= (1.0 - 0.01 * b * b) * wns)) b++;
+            }
+            x.band = b;
+            x.key1 = 0;
+            x.key2 = slack[j];
+        } else {                                                 // N_n: congestion-driven (R43)
+            x.cls = 2;
+            x.band = 0;
+            x.key1 = wl[j];
+            x.key2 = 0.0;
+        }
+    });
+    par_sort(it, [](const Item &a, const Item &b) {
+        if (a.cls != b.cls) return a.cls < b.cls;
+        if (a.band != b.band) return a.band < b.band;
+        if (a.key1 != b.key1) return a.key1 < b.key1;
+        if (a.key2 != b.key2) return a.key2 < b.key2;
+        return a.idx < b.idx;
+    }, nthr);
+    // GetBatches (l.7-9) + Concat (l.10)
+    int32_t nb = 0;
+    int64_t in_batch = 0;
+    for (int64_t i = 0; i < N; i++) {
+        const bool new_subset = i > 0 && (it[i].cls != it[i - 1].cls || it[i].band != it[i - 1].band);
+        if (i == 0) nb = 1;
+        else if (new_subset || in_batch == max_batch) { nb++; in_batch = 0; }
+        batch_of[it[i].idx] = nb - 1;
+        in_batch++;
+    }
+    *n_batches = nb;
+    return LA_OK;
+}
+
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule) {
     if (!ctx) return set_err(LA_EINVAL, "null context");
     if (schedule != LA_SCHED_DATAFLOW && schedule != LA_SCHED_BATCH) return set_err(LA_EINVAL, "unknown schedule");

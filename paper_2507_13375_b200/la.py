@@ -94,6 +94,7 @@ def _load():
         "la_set_tracing": ([c_void_p, c_i32], c_i32),
         "la_eval_overflow": ([c_void_p, P(la_eval)], c_i32),
         "la_set_snapshot_batches": ([c_void_p, P(c_i32), c_i64], c_i32),
+        "la_paper_batches": ([P(la_net_desc), P(c_i32), c_f64, c_i32, c_i64, P(c_i32), P(c_i32)], c_i32),
         "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
@@ -120,7 +121,8 @@ _lib = _load()
 EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand", "la_assign_all", "la_eval_timing",
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
-           "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches")
+           "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches",
+           "la_paper_batches")
 
 
 def _check(st):
@@ -201,6 +203,39 @@ def la_set_snapshot_batches(ctx, batch_of):
         return
     b = np.ascontiguousarray(batch_of, np.int32)
     _check(_lib.la_set_snapshot_batches(ctx, b.ctypes.data_as(P(c_i32)), b.shape[0]))
+
+
+def net_desc_of(d, keep) -> la_net_desc:
+    """la_net_desc over the arrays of design ``d`` (converted copies are appended to ``keep``)."""
+    def arr(a, dt):
+        x = np.ascontiguousarray(a, dtype=dt)
+        keep.append(x)
+        return x
+
+    n = la_net_desc()
+    n.n_nets = d.n_nets
+    n.pin_ptr = _p(arr(d.pin_ptr, np.int64), c_i64)
+    n.pin_x, n.pin_y = _p(arr(d.pin_x, np.int32), c_i32), _p(arr(d.pin_y, np.int32), c_i32)
+    n.pin_layer = _p(arr(d.pin_layer, np.uint8), c_u8)
+    n.pin_cap, n.pin_slack = _p(arr(d.pin_cap, np.float64), c_f64), _p(arr(d.pin_slack, np.float64), c_f64)
+    n.seg_ptr = _p(arr(d.seg_ptr, np.int64), c_i64)
+    n.seg_xy = _p(arr(np.asarray(d.seg_xy).reshape(-1), np.int32), c_i32)
+    n.r_drv = _p(arr(d.r_drv, np.float64), c_f64)
+    n.order_key = _p(arr(d.order_key, np.int64), c_i64)
+    n.wns = d.wns
+    return n
+
+
+def la_paper_batches(d, criticality, alpha: float = 0.7, th: int = 3, max_batch: int = 1 << 20):
+    """Alg. 1 lines 3-10 (include/la.h): batch id per net (input order) and the batch count."""
+    keep = []
+    desc = net_desc_of(d, keep)
+    crit = np.ascontiguousarray(criticality, np.int32)
+    out = np.zeros(d.n_nets, np.int32)
+    nb = c_i32(0)
+    _check(_lib.la_paper_batches(ctypes.byref(desc), crit.ctypes.data_as(P(c_i32)), float(alpha), int(th),
+                                 int(max_batch), out.ctypes.data_as(P(c_i32)), ctypes.byref(nb)))
+    return out, int(nb.value)
 
 
 def la_set_tracing(ctx, enable: bool):
@@ -294,26 +329,7 @@ class LayerAssigner:
         self.n_batches = None
 
     def net_desc(self, d=None) -> la_net_desc:
-        d = d or self.d
-        k = self._keep
-
-        def arr(a, dt):
-            x = np.ascontiguousarray(a, dtype=dt)
-            k.append(x)
-            return x
-
-        n = la_net_desc()
-        n.n_nets = d.n_nets
-        n.pin_ptr = _p(arr(d.pin_ptr, np.int64), c_i64)
-        n.pin_x, n.pin_y = _p(arr(d.pin_x, np.int32), c_i32), _p(arr(d.pin_y, np.int32), c_i32)
-        n.pin_layer = _p(arr(d.pin_layer, np.uint8), c_u8)
-        n.pin_cap, n.pin_slack = _p(arr(d.pin_cap, np.float64), c_f64), _p(arr(d.pin_slack, np.float64), c_f64)
-        n.seg_ptr = _p(arr(d.seg_ptr, np.int64), c_i64)
-        n.seg_xy = _p(arr(np.asarray(d.seg_xy).reshape(-1), np.int32), c_i32)
-        n.r_drv = _p(arr(d.r_drv, np.float64), c_f64)
-        n.order_key = _p(arr(d.order_key, np.int64), c_i64)
-        n.wns = d.wns
-        return n
+        return net_desc_of(d or self.d, self._keep)
 
     def load(self, d=None, snapshot_batches=None) -> int:
         """la_load_nets; ``snapshot_batches`` (int32 per net): paper-style batches (NEXT #1)."""

@@ -390,3 +390,37 @@ def test_snapshot_batches_reduce_to_known_schedules():
     assert np.array_equal(np.concatenate(vias) if vias else allin["vias"], allin["vias"])
     wd, vd = rebuild_demand(d, allin["wires"], allin["vias"])
     assert np.array_equal(wd, allin["wire_dem"]) and np.array_equal(vd, allin["via_dem"])
+
+
+def test_paper_batches_by_hand():
+    """Alg. 1 lines 3-10 (oracle.paper_batches) on eight hand-made nets, WNS = -100, alpha 0.7,
+    th 3: criticality 8, 8, 5, 4 are critical (bands [8, 8] then [4, 8)); net slacks -98 and -80
+    are semi-critical (< -70), in slack bands (-99, -96] and (-84, -75]; -60 and +10 are not,
+    and go by 2D wirelength."""
+    # nets: (criticality, sink slack, wirelength)
+    spec = [(8, -90, 3), (8, -95, 1), (5, -50, 2), (4, -99, 5), (0, -98, 2), (1, -80, 4), (0, 10, 7), (2, -60, 1)]
+    pin_ptr, slacks, seg_ptr, segs = [0], [], [0], []
+    for c, s, w in spec:
+        slacks += [0.0, float(s)]
+        pin_ptr.append(len(slacks))
+        segs.append((0, 0, w, 0))
+        seg_ptr.append(len(segs))
+    crit = [c for c, _, _ in spec]
+    b, nb = oracle.paper_batches(pin_ptr, slacks, seg_ptr, segs, -100.0, crit, 0.7, 3, max_batch=1)
+    # order: [8,8] band by slack: net1 (-95), net0 (-90); [4,8): net2 (5), net3 (4); semi: net4 (-98, band 1),
+    # net5 (-80, band 5); non-critical by wirelength: net7 (1), net6 (7)
+    assert nb == 8
+    assert list(b) == [1, 0, 2, 3, 4, 5, 7, 6]
+    b2, nb2 = oracle.paper_batches(pin_ptr, slacks, seg_ptr, segs, -100.0, crit, 0.7, 3, max_batch=100)
+    assert nb2 == 5 and list(b2) == [0, 0, 1, 1, 2, 3, 4, 4]
+
+
+def test_paper_batches_library_equals_oracle():
+    """The library's host Alg. 1 (la_paper_batches, no GPU needed) == the plain oracle."""
+    from paper_2507_13375_b200 import la
+    d = synth.make_config(1)
+    for seed, mb in ((1, 50), (2, 1000)):
+        crit = synth.criticality(d, seed)
+        got, nb = la.la_paper_batches(d, crit, 0.7, 3, mb)
+        ref, nbr = oracle.paper_batches(d.pin_ptr, d.pin_slack, d.seg_ptr, d.seg_xy, d.wns, crit, 0.7, 3, mb)
+        assert nb == nbr and np.array_equal(got, ref)
