@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    ap.add_argument("--batching", choices=["conflict-free", "paper"], default="conflict-free",
+                    help="conflict-free batches (exact sequential semantics, default) or the paper's Alg. 1 "
+                         "snapshot batches (NEXT #1/#2, synthetic criticality)")
+    ap.add_argument("--max-batch", type=int, default=1 << 18, help="Alg. 1 GetBatches size cap (paper batching)")
     ap.add_argument("--ncu-pass", action="store_true",
                     help="setup + 1 warm step, then ONE step between cudaProfilerStart/Stop (for ncu)")
     return ap.parse_args()
@@ -199,9 +203,12 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    snap = None
+    if args.batching == "paper":
+        snap, _ = la.la_paper_batches(d, synth.criticality(d), 0.7, 3, args.max_batch)
     t_setup = time.perf_counter()
     A = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=nid, stream=stream.cuda_stream)
-    nb = A.load()
+    nb = A.load(snapshot_batches=snap)
     setup_s = time.perf_counter() - t_setup
     st0 = A.stats()
 
@@ -303,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             B = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=None if world == 1 else nid,
                                  stream=stream.cuda_stream)
-            B.load()
+            B.load(snapshot_batches=snap)
             B.assign_all()
             B.eval_timing()
             B.solution()
@@ -333,7 +340,7 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "nets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": d.name, "nets": d.n_nets, "grid": f"{d.X}x{d.Y}", "layers": d.L,
+            "config": {"workload": d.name, "batching": args.batching, "nets": d.n_nets, "grid": f"{d.X}x{d.Y}", "layers": d.L,
                        "pins": d.n_pins, "la_nodes": st["n_nodes"], "wirelength": st["wirelength"],
                        "via_cuts": via_cuts, "batches": nb, "max_height": st["max_height"],
                        "max_batch_nets": st["max_batch_nets"],

@@ -36,6 +36,7 @@ is_drv = np.zeros(base.n_pins, bool)
 is_drv[base.pin_ptr[:-1]] = True
 w[is_drv] = 0.0
 crit = (~is_drv) & (base.pin_slack <= np.quantile(base.pin_slack[~is_drv], 0.2))
+net_of_pin = np.repeat(np.arange(base.n_nets), np.diff(base.pin_ptr))
 
 
 def variant(name, **kw):
@@ -53,8 +54,13 @@ def variant(name, **kw):
     ev = A.eval_overflow()
     A.close()
     sd = t["sink_delay"]
+    # with the driver resistance the net delay gains r_drv * C_total at every sink: the term the
+    # look-ahead (cost' = cost + B ur) anticipates
+    sdd = sd + base.r_drv[net_of_pin] * t["net_cap"][net_of_pin]
     print(json.dumps({"variant": name, "workload": d.name, "k_assign_ms": p["assign_ms"],
-                      "weighted_delay_ps": float(np.dot(w, sd)), "max_critical_delay_ps": float(sd[crit].max()),
+                      "weighted_delay_ps": float(np.dot(w, sd)), "weighted_delay_with_driver_ps": float(np.dot(w, sdd)),
+                      "max_critical_delay_ps": float(sd[crit].max()),
+                      "max_critical_delay_with_driver_ps": float(sdd[crit].max()),
                       "total_net_cap_fF": float(t["net_cap"].sum()), "tof_wire": ev["tof_wire"],
                       "legacy_overflow": ev["legacy_wire"], "via_cuts": ev["via_cuts"]}), flush=True)
 
