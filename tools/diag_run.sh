@@ -1,2 +1,5 @@
-timeout 900 python tools/ablation.py --config 3 > gpurun_out/ablation_cfg3.jsonl 2> gpurun_out/ablation.err
-cat gpurun_out/ablation_cfg3.jsonl; tail -3 gpurun_out/ablation.err
+for C in 1 2 4; do
+  timeout 900 python bench.py --config $C --no-cpu-baseline > gpurun_out/bench_cfg$C.json 2> gpurun_out/bench_cfg$C.err
+  python -c "import json;d=json.load(open('gpurun_out/bench_cfg$C.json'));print($C, d['value']/1e6, 'Mnets/s', d['ms_per_step'], 'ms', d['config']['batches'], 'batches', 'e2e', d['e2e']['value']/1e6, d['roofline_step']['kernel_ms_per_step'])"
+  tail -2 gpurun_out/bench_cfg$C.err
+done
