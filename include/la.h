@@ -85,7 +85,8 @@ typedef struct {
     int32_t delta_lo, delta_hi; /* Eq. (3) marginal-table domain for d - c (reading R20)               */
     int32_t device;             /* CUDA device ordinal of this process                                 */
     int32_t rank, world;        /* this process's rank, number of ranks (1..8)                          */
-    const void *nccl_id;        /* 128-byte ncclUniqueId created by rank 0; NULL when world == 1       */
+    const void *nccl_id;        /* 128-byte ncclUniqueId created by rank 0; NULL when world == 1, or
+                                   with world > 1 for the host transport (la_get/put_decisions)      */
     void *stream;               /* cudaStream_t to enqueue on; NULL = library-owned stream             */
 } la_grid_desc;
 
@@ -183,6 +184,20 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch);
  * every commit.  Collective.  Enqueue only.
  * Errors: LA_ESTATE unless batch k was just assigned. */
 la_status la_commit_demand(la_ctx *ctx, int32_t batch);
+
+/* Host transport of the multi-GPU reconcile: a context created
+ * with world > 1 and nccl_id == NULL does not use NCCL; after la_assign_batch(k) the caller
+ * takes every rank's packed decisions (u32 per node of batch k: layer | b << 8 | t << 16 |
+ * 1 << 24 on the rank's own nets, 0 elsewhere) and net costs (f64 per net of batch k, 0 on
+ * other ranks' nets) with la_get_decisions, sums them element-wise over the ranks (a sum of
+ * disjoint slots: exact), hands the sums to every rank with la_put_decisions, then calls
+ * la_commit_demand(k).  Same results as the NCCL path; used to test the sharded path on
+ * one GPU and to reconcile over any other transport.  la_batch_extent gives the slot counts
+ * (nodes, nets) of batch k.  Errors: LA_ESTATE outside that sequence or on an NCCL or
+ * single-rank context; LA_ERANGE for a bad batch. */
+la_status la_batch_extent(la_ctx *ctx, int32_t batch, int64_t *nodes, int64_t *nets);
+la_status la_get_decisions(la_ctx *ctx, int32_t batch, uint32_t *dec, double *net_cost);
+la_status la_put_decisions(la_ctx *ctx, int32_t batch, const uint32_t *dec, const double *net_cost);
 
 /* Every remaining batch (the whole Alg. 2 loop), enqueued.  Collective.
  * Default (LA_SCHED_BATCH): la_assign_batch + la_commit_demand for every

@@ -102,6 +102,8 @@ struct la_ctx {
     int32_t schedule = LA_SCHED_BATCH;        // measured faster on B200; dataflow on request
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
+    bool host_xport = false;                  // world > 1 without NCCL: la_get_decisions / la_put_decisions
+    int32_t put_batch = -1;                   // host transport: batch whose reconciled decisions arrived
     int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
     unsigned long long *d_eval = nullptr;     // la_eval_overflow buffers (lazy)
     int8_t *d_eval_lay = nullptr;             // [3][MAXL] slot -> layer for the H, V and via planes
@@ -587,7 +589,6 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     if (!ok_nonneg(ws, 7)) return set_err(LA_EINVAL, "negative (or NaN) weight or exponent");
     if (g->delta_lo > g->delta_hi) return set_err(LA_EINVAL, "delta_lo > delta_hi");
     if (g->world < 1 || g->world > 64 || g->rank < 0 || g->rank >= g->world) return set_err(LA_EINVAL, "bad rank/world");
-    if (g->world > 1 && !g->nccl_id) return set_err(LA_EINVAL, "world > 1 needs nccl_id");
     bool hasH = false, hasV = false;
     for (int l = 0; l < L; l++) {
         if (g->dir[l] > 1) return set_err(LA_EINVAL, "dir must be 0 or 1");
@@ -724,7 +725,8 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "snapshot initial state"); }
 
-    if (g->world > 1) {
+    ctx->host_xport = g->world > 1 && !g->nccl_id;   // ranks reconciled by the caller (la_get/put_decisions)
+    if (g->world > 1 && g->nccl_id) {
         ncclUniqueId id;
         std::memcpy(&id, g->nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, g->world, id, g->rank);
@@ -1223,25 +1225,79 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     return LA_OK;
 }
 
+// This rank's packed decisions for batch k in S.dec (its shard's nodes; every other slot 0).
+static la_status pack_shard(la_ctx *ctx, int32_t batch) {
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
+    const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
+    const RankShare r = rank_share(ctx, batch);
+    CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
+    // the shard's big nets and small nets are two contiguous position ranges
+    const int64_t ranges[2][2] = {{r.big_beg, r.big_end}, {r.small_beg, r.small_end}};
+    for (int k = 0; k < 2; k++) {
+        if (ranges[k][1] <= ranges[k][0]) continue;
+        const int64_t p0 = k == 0 ? ctx->h_big_pos[ranges[k][0]] : ctx->h_small_pos[ranges[k][0]];
+        const int64_t p1 = (k == 0 ? ctx->h_big_pos[ranges[k][1] - 1] : ctx->h_small_pos[ranges[k][1] - 1]) + 1;
+        CK(launch_pack_decisions(ctx->S, ctx->h_net_node0[p0], ctx->h_net_node0[p1], ctx->stream));
+        ctx->stats.launches += 1;
+    }
+    return LA_OK;
+}
+
+la_status la_batch_extent(la_ctx *ctx, int32_t batch, int64_t *nodes, int64_t *nets) {
+    TRY(check_ready(ctx));
+    const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
+    if (batch < 0 || batch >= nb) return set_err(LA_ERANGE, "batch index out of range");
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
+    if (nodes) *nodes = ctx->h_net_node0[b1] - ctx->h_net_node0[b0];
+    if (nets) *nets = b1 - b0;
+    return LA_OK;
+}
+
+la_status la_get_decisions(la_ctx *ctx, int32_t batch, uint32_t *dec, double *net_cost) {
+    TRY(check_ready(ctx));
+    if (!ctx->host_xport) return set_err(LA_ESTATE, "not a host-transport context (world > 1, nccl_id NULL)");
+    if (!ctx->pending_commit || batch != ctx->next_batch) return set_err(LA_ESTATE, "batch not just assigned");
+    if (!dec || !net_cost) return set_err(LA_EINVAL, "null argument");
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
+    const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
+    TRY(pack_shard(ctx, batch));
+    CK(cudaMemcpyAsync(dec, ctx->S.dec + n0, sizeof(uint32_t) * (n1 - n0), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(net_cost, ctx->S.froot + b0, sizeof(double) * (b1 - b0), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.d2h_bytes += 4 * (n1 - n0) + 8 * (b1 - b0);
+    return LA_OK;
+}
+
+la_status la_put_decisions(la_ctx *ctx, int32_t batch, const uint32_t *dec, const double *net_cost) {
+    TRY(check_ready(ctx));
+    if (!ctx->host_xport) return set_err(LA_ESTATE, "not a host-transport context (world > 1, nccl_id NULL)");
+    if (!ctx->pending_commit || batch != ctx->next_batch) return set_err(LA_ESTATE, "batch not just assigned");
+    if (!dec || !net_cost) return set_err(LA_EINVAL, "null argument");
+    const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
+    const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
+    CK(cudaMemcpyAsync(ctx->S.dec + n0, dec, sizeof(uint32_t) * (n1 - n0), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->S.froot + b0, net_cost, sizeof(double) * (b1 - b0), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.h2d_bytes += 4 * (n1 - n0) + 8 * (b1 - b0);
+    ctx->put_batch = batch;
+    return LA_OK;
+}
+
 la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     TRY(check_ready(ctx));
     if (!ctx->pending_commit || batch != ctx->next_batch)
         return set_err(LA_ESTATE, "commit must follow the assignment of the same batch");
     const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
     const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
-    if (ctx->world > 1) {
+    if (ctx->world > 1 && ctx->host_xport) {
+        // the caller summed every rank's packed decisions and net costs (la_put_decisions)
+        if (ctx->put_batch != batch) return set_err(LA_ESTATE, "host transport: la_put_decisions must precede the commit");
+        CK(launch_unpack_decisions(ctx->S, n0, n1, ctx->stream));
+        ctx->stats.launches += 1;
+    } else if (ctx->world > 1) {
         // reconcile: every rank contributes its shard's packed decisions (others 0) -> sum
-        const RankShare r = rank_share(ctx, batch);
         int pr = prof_begin(ctx, K_RECONCILE);
-        CK(cudaMemsetAsync(ctx->S.dec + n0, 0, sizeof(uint32_t) * (n1 - n0), ctx->stream));
-        // the shard's big nets and small nets are two contiguous position ranges
-        const int64_t ranges[2][2] = {{r.big_beg, r.big_end}, {r.small_beg, r.small_end}};
-        for (int k = 0; k < 2; k++) {
-            if (ranges[k][1] <= ranges[k][0]) continue;
-            const int64_t p0 = k == 0 ? ctx->h_big_pos[ranges[k][0]] : ctx->h_small_pos[ranges[k][0]];
-            const int64_t p1 = (k == 0 ? ctx->h_big_pos[ranges[k][1] - 1] : ctx->h_small_pos[ranges[k][1] - 1]) + 1;
-            CK(launch_pack_decisions(ctx->S, ctx->h_net_node0[p0], ctx->h_net_node0[p1], ctx->stream));
-        }
+        TRY(pack_shard(ctx, batch));
         NK(ncclAllReduce(ctx->S.dec + n0, ctx->S.dec + n0, (size_t)(n1 - n0), ncclUint32, ncclSum, ctx->comm,
                          ctx->stream));
         NK(ncclAllReduce(ctx->S.froot + b0, ctx->S.froot + b0, (size_t)(b1 - b0), ncclFloat64, ncclSum, ctx->comm,

@@ -94,6 +94,9 @@ def _load():
         "la_set_tracing": ([c_void_p, c_i32], c_i32),
         "la_eval_overflow": ([c_void_p, P(la_eval)], c_i32),
         "la_set_snapshot_batches": ([c_void_p, P(c_i32), c_i64], c_i32),
+        "la_batch_extent": ([c_void_p, c_i32, P(c_i64), P(c_i64)], c_i32),
+        "la_get_decisions": ([c_void_p, c_i32, P(ctypes.c_uint32), P(c_f64)], c_i32),
+        "la_put_decisions": ([c_void_p, c_i32, P(ctypes.c_uint32), P(c_f64)], c_i32),
         "la_paper_batches": ([P(la_net_desc), P(c_i32), c_f64, c_i32, c_i64, P(c_i32), P(c_i32)], c_i32),
         "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
@@ -122,7 +125,7 @@ EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand"
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
            "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches",
-           "la_paper_batches")
+           "la_paper_batches", "la_batch_extent", "la_get_decisions", "la_put_decisions")
 
 
 def _check(st):
@@ -236,6 +239,22 @@ def la_paper_batches(d, criticality, alpha: float = 0.7, th: int = 3, max_batch:
     _check(_lib.la_paper_batches(ctypes.byref(desc), crit.ctypes.data_as(P(c_i32)), float(alpha), int(th),
                                  int(max_batch), out.ctypes.data_as(P(c_i32)), ctypes.byref(nb)))
     return out, int(nb.value)
+
+
+def la_get_decisions(ctx, batch: int):
+    """Host transport: this rank's packed decisions and net costs of ``batch`` (after assign)."""
+    nodes, nets = c_i64(0), c_i64(0)
+    _check(_lib.la_batch_extent(ctx, batch, ctypes.byref(nodes), ctypes.byref(nets)))
+    dec = np.zeros(nodes.value, np.uint32)
+    cost = np.zeros(nets.value, np.float64)
+    _check(_lib.la_get_decisions(ctx, batch, dec.ctypes.data_as(P(ctypes.c_uint32)), cost.ctypes.data_as(P(c_f64))))
+    return dec, cost
+
+
+def la_put_decisions(ctx, batch: int, dec, cost):
+    dec = np.ascontiguousarray(dec, np.uint32)
+    cost = np.ascontiguousarray(cost, np.float64)
+    _check(_lib.la_put_decisions(ctx, batch, dec.ctypes.data_as(P(ctypes.c_uint32)), cost.ctypes.data_as(P(c_f64))))
 
 
 def la_set_tracing(ctx, enable: bool):

@@ -79,7 +79,7 @@ def _desc(la, d, **over):
     (dict(W_D=-1.0), "negative"),
     (dict(delta_lo=5, delta_hi=4), "delta_lo"),
     (dict(routable=np.array([1, 0, 1, 0, 1, 0])), "routable"),
-    (dict(world=2, rank=0), "nccl_id"),
+    (dict(world=0, rank=0), "rank"),
     (dict(world=2, rank=3), "rank"),
 ])
 def test_init_grid_validation(la, over, msg):

@@ -338,3 +338,39 @@ def test_snapshot_batches_parity(la, kind):
     if kind == "conflict_free":
         seq = oracle.run(d)
         assert np.array_equal(seq["wires"], ref["wires"]) and np.array_equal(seq["wire_dem"], ref["wire_dem"])
+
+
+@pytest.mark.parametrize("world,cfg,n", [(2, 2, None), (3, 4, 60_000)])
+def test_sharded_path_host_transport(la, world, cfg, n):
+    """The multi-GPU data path on one GPU: `world` contexts, one per
+    rank, each assigns only its shard of every batch (la_shard_range over the batch's big and
+    small nets), the packed decisions and net costs of all ranks are summed on the host (the
+    NCCL all-reduce's job) and handed back, every rank commits the whole batch (k_commit).
+    Every replica must end bit-identical to the others and to the oracle."""
+    d = synth.make_config(cfg, n_nets=n)
+    ranks = [la.LayerAssigner(d, device=0, rank=r, world=world) for r in range(world)]
+    nbs = {A.load() for A in ranks}
+    assert len(nbs) == 1
+    nb = nbs.pop()
+    for k in range(nb):
+        for A in ranks:
+            A.assign_batch(k)
+        parts = [la.la_get_decisions(A.ctx, k) for A in ranks]
+        dec = np.sum([p[0] for p in parts], axis=0, dtype=np.uint64).astype(np.uint32)
+        cost = np.sum([p[1] for p in parts], axis=0)
+        owned = np.sum([(p[0] >> 24) & 1 for p in parts], axis=0)
+        assert np.all(owned == 1), "every node of the batch decided by exactly one rank"
+        for A in ranks:
+            la.la_put_decisions(A.ctx, k, dec, cost)
+            A.commit_demand(k)
+    outs = []
+    for A in ranks:
+        out = A.eval_timing()
+        out.update(A.solution())
+        wd, vd = A.demand()
+        out.update(wire_dem=wd, via_dem=vd, batch_of=A.batches())
+        outs.append(out)
+        A.close()
+    ref = oracle.run(d)
+    for out in outs:
+        assert_parity(out, ref, bitwise_fp=True)

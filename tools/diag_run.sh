@@ -1,5 +1,1 @@
-for C in 1 2 4; do
-  timeout 900 python bench.py --config $C --no-cpu-baseline > gpurun_out/bench_cfg$C.json 2> gpurun_out/bench_cfg$C.err
-  python -c "import json;d=json.load(open('gpurun_out/bench_cfg$C.json'));print($C, d['value']/1e6, 'Mnets/s', d['ms_per_step'], 'ms', d['config']['batches'], 'batches', 'e2e', d['e2e']['value']/1e6, d['roofline_step']['kernel_ms_per_step'])"
-  tail -2 gpurun_out/bench_cfg$C.err
-done
+timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
