@@ -190,13 +190,17 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     d = synth.make_config(args.config, n_nets=args.n_nets)
-    nid = None
-    if world > 1:
+    def fresh_nccl_id():
+        """A new ncclUniqueId from rank 0 for every communicator (an id is not reused)."""
+        if world == 1:
+            return None
         buf = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             buf.copy_(torch.frombuffer(bytearray(la.la_nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
-        nid = bytes(buf.cpu().numpy().tobytes())
+        return bytes(buf.cpu().numpy().tobytes())
+
+    nid = fresh_nccl_id()
     stream = torch.cuda.Stream(device=dev)
 
     def barrier():
@@ -305,10 +309,11 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         vals, h2d, d2h = [], 0, 0
         for i in range(args.e2e_steps + 1):
+            nid_e = fresh_nccl_id()
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            B = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=None if world == 1 else nid,
+            B = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=nid_e,
                                  stream=stream.cuda_stream)
             B.load(snapshot_batches=snap)
             B.assign_all()
