@@ -313,11 +313,33 @@ struct Builder {
     std::vector<int32_t> order, finalid, pre, vof;
     std::vector<uint8_t> seen;
 
-    int64_t vfind(uint64_t g) const {
-        auto it = std::lower_bound(vs.begin(), vs.end(), g);
-        return (it != vs.end() && *it == g) ? (int64_t)(it - vs.begin()) : -1;
+    // GCell -> vertex index: open-addressing hash over vs (built once per net)
+    std::vector<uint64_t> hkey;
+    std::vector<int32_t> hval;
+    uint64_t hmask = 0;
+    int hshift = 0;
+    void hbuild() {
+        int bits = 4;
+        while (((size_t)1 << bits) < 2 * vs.size()) bits++;
+        hkey.assign((size_t)1 << bits, ~0ull);
+        hval.resize((size_t)1 << bits);
+        hmask = ((uint64_t)1 << bits) - 1;
+        hshift = 64 - bits;
+        for (size_t i = 0; i < vs.size(); i++) {
+            uint64_t h = (vs[i] * 0x9E3779B97F4A7C15ull) >> hshift;
+            while (hkey[h] != ~0ull) h = (h + 1) & hmask;
+            hkey[h] = vs[i];
+            hval[h] = (int32_t)i;
+        }
     }
-    bool has_edge(uint64_t k) const { return std::binary_search(ek.begin(), ek.end(), k); }
+    int64_t vfind(uint64_t g) const {
+        uint64_t h = (g * 0x9E3779B97F4A7C15ull) >> hshift;
+        while (hkey[h] != ~0ull) {
+            if (hkey[h] == g) return hval[h];
+            h = (h + 1) & hmask;
+        }
+        return -1;
+    }
 
     double pin_weight(double slack) const {      // Eq. (4), reading R1/R2
         if (!(nd->wns < 0.0)) return ctx->w_floor;
@@ -374,6 +396,7 @@ struct Builder {
         if (ek.empty()) vs.push_back(g_drv);
         std::sort(vs.begin(), vs.end());
         vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+        hbuild();
         for (int64_t p = p0; p < p1; p++) {
             if (vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]) < 0) {
                 std::snprintf(buf, sizeof buf, "net %lld: pin %lld GCell not on the route", (long long)net, (long long)p);
@@ -386,15 +409,15 @@ struct Builder {
             return buf;
         }
         mask.assign(nv, 0);
-        for (size_t i = 0; i < nv; i++) {
-            uint64_t g = vs[i];
-            int x = (int)(g % X), y = (int)(g / X);
-            uint8_t m = 0;
-            if (x + 1 < X && has_edge(g * 2)) m |= 1 << DIR_E;
-            if (x > 0 && has_edge((g - 1) * 2)) m |= 1 << DIR_W;
-            if (y + 1 < Y && has_edge(g * 2 + 1)) m |= 1 << DIR_N;
-            if (y > 0 && has_edge((g - X) * 2 + 1)) m |= 1 << DIR_S;
-            mask[i] = m;
+        for (uint64_t k : ek) {                      // both endpoints of every unit edge
+            const uint64_t g = k >> 1;
+            if (k & 1) {
+                mask[vfind(g)] |= 1 << DIR_N;
+                mask[vfind(g + X)] |= 1 << DIR_S;
+            } else {
+                mask[vfind(g)] |= 1 << DIR_E;
+                mask[vfind(g + 1)] |= 1 << DIR_W;
+            }
         }
         // connectivity from the driver
         {
