@@ -101,9 +101,9 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 struct DevBuf {
     void *p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    ~DevBuf() { if (p) dfree(p); }
     template <class T> T *as() { return static_cast<T *>(p); }
-    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+    cudaError_t alloc(size_t bytes) { return dmalloc(&p, bytes ? bytes : 16); }
 };
 
 #define BCK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
@@ -111,9 +111,9 @@ struct DevBuf {
 }  // namespace
 
 void DagDev::release() {
-    if (off) cudaFree(off);
-    if (succ) cudaFree(succ);
-    if (indeg) cudaFree(indeg);
+    if (off) dfree(off);
+    if (succ) dfree(succ);
+    if (indeg) dfree(indeg);
     off = nullptr; succ = nullptr; indeg = nullptr;
     n = n_edges = 0;
 }
@@ -169,9 +169,9 @@ cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int ele
         dag->release();
         dag->n = n_nets;
         dag->n_edges = n_edges;
-        BCK(cudaMalloc(&dag->off, 8 * (n_nets + 1)));
-        BCK(cudaMalloc(&dag->succ, 4 * std::max<int64_t>(n_edges, 1)));
-        BCK(cudaMalloc(&dag->indeg, 4 * n_nets));
+        BCK(dmalloc(&dag->off, 8 * (n_nets + 1)));
+        BCK(dmalloc(&dag->succ, 4 * std::max<int64_t>(n_edges, 1)));
+        BCK(dmalloc(&dag->indeg, 4 * n_nets));
         BCK(cudaMemcpyAsync(dag->off, off.p, 8 * (n_nets + 1), cudaMemcpyDeviceToDevice, s));
         BCK(cudaMemcpyAsync(dag->succ, succ.p, 4 * std::max<int64_t>(n_edges, 1), cudaMemcpyDeviceToDevice, s));
         BCK(cudaMemcpyAsync(dag->indeg, indeg.p, 4 * n_nets, cudaMemcpyDeviceToDevice, s));
@@ -221,9 +221,9 @@ cudaError_t gpu_dag_to_positions(DagDev &dag, const int64_t *h_rank_of_pos, int6
     BCK(rop.alloc(8 * std::max<int64_t>(n, 1)));
     BCK(por.alloc(4 * std::max<int64_t>(n, 1)));
     BCK(deg.alloc(8 * (n + 1)));
-    BCK(cudaMalloc(off_p, 8 * (n + 1)));
-    BCK(cudaMalloc(succ_p, 4 * std::max<int64_t>(dag.n_edges, 1)));
-    BCK(cudaMalloc(indeg_p, 4 * std::max<int64_t>(n, 1)));
+    BCK(dmalloc(off_p, 8 * (n + 1)));
+    BCK(dmalloc(succ_p, 4 * std::max<int64_t>(dag.n_edges, 1)));
+    BCK(dmalloc(indeg_p, 4 * std::max<int64_t>(n, 1)));
     if (n == 0) {
         BCK(cudaMemsetAsync(*off_p, 0, 8, s));
         return cudaStreamSynchronize(s);

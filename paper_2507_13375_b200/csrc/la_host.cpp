@@ -146,10 +146,12 @@ struct la_ctx {
     }
 
     ~la_ctx() {
-        for (void *p : dev_allocs) cudaFree(p);
+        if (stream) cudaStreamSynchronize(stream);   // frees are ordered on the legacy stream
+        cudaDeviceSynchronize();
+        for (void *p : dev_allocs) dfree(p);
         void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab,
                       d_ticket, d_trace, d_eval, d_eval_lay, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
-        for (void *p : gp) if (p) cudaFree(p);
+        for (void *p : gp) if (p) dfree(p);
         if (comm) ncclCommDestroy(comm);
         for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
         for (auto e : ev_pool) cudaEventDestroy(e);
@@ -182,7 +184,7 @@ la_status cuda_fail(la_ctx *ctx, cudaError_t e, const char *where) {
 template <class T>
 la_status dev_upload(la_ctx *ctx, T **dst, const T *src, size_t n) {
     void *p = nullptr;
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16));
+    cudaError_t e = dmalloc(&p, std::max<size_t>(n * sizeof(T), 16));
     if (e != cudaSuccess) {
         ctx->poisoned = true;
         return set_err(e == cudaErrorMemoryAllocation ? LA_ENOMEM : LA_ECUDA,
@@ -681,6 +683,13 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
 
     cudaError_t e = cudaSetDevice(g->device);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "cudaSetDevice"); }
+    {   // keep freed device memory in the default pool for the next context (see dmalloc)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     if (g->stream) {
         ctx->stream = static_cast<cudaStream_t>(g->stream);
     } else {
@@ -692,7 +701,7 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     auto up = [&](auto **dst, const auto *src, size_t n) -> la_status {
         using T = std::remove_const_t<std::remove_reference_t<decltype(*src)>>;
         void *p = nullptr;
-        cudaError_t ee = cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16));
+        cudaError_t ee = dmalloc(&p, std::max<size_t>(n * sizeof(T), 16));
         if (ee != cudaSuccess) return set_err(ee == cudaErrorMemoryAllocation ? LA_ENOMEM : LA_ECUDA,
                                               std::string("cudaMalloc: ") + cudaGetErrorString(ee));
         *dst = static_cast<T *>(p);
@@ -732,8 +741,8 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     G.Mpos = ctx->d_Mpos; G.Mzero = ctx->d_Mzero; G.tab = ctx->d_tab;
     e = launch_pack_state(G, ctx->d_wcap, d_wdem0, ctx->d_vcap, d_vdem0, ctx->d_wire_off, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (d_wdem0) cudaFree(d_wdem0);
-    if (d_vdem0) cudaFree(d_vdem0);
+    if (d_wdem0) dfree(d_wdem0);
+    if (d_vdem0) dfree(d_vdem0);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "pack initial state"); }
     // pristine copy of the initial packed state for la_reset
     size_t bH = sizeof(int32_t) * (size_t)(g->X - 1) * g->Y * ctx->LH;
@@ -1119,7 +1128,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         CK(assign_resident_ctas(ctx->L, ctx->LD, ctx->NS, ctx->NP, &per_sm, &n_sm));
         if (per_sm < 1) return set_err(LA_ECUDA, "k_assign does not fit on an SM");
         ctx->grid = per_sm * n_sm;
-        CK(cudaMalloc(&ctx->d_ticket, sizeof(unsigned long long) * 2 * (nb + 1)));
+        CK(dmalloc(&ctx->d_ticket, sizeof(unsigned long long) * 2 * (nb + 1)));
         CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
         ctx->h_big_pos = big_pos;
         ctx->h_small_pos = small_pos;
@@ -1133,14 +1142,14 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
         if (!big_pos.empty()) ctx->n_big_ctas = std::max(1, std::min(ctx->n_big_ctas, ctx->grid - 1));
         if (const char *e = getenv("GAPLA_HYBRID")) ctx->hybrid = atoi(e) != 0;
-        CK(cudaMalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+        CK(dmalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
         if (N) CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
         // a big net keeps its DP state in its CTA's shared memory, or in a per-CTA global slot
         const size_t need = assign_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD);
         ctx->gslot_bytes = 0;
         if (max_big_nodes > 0 && need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP)) {
             ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
-            CK(cudaMalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));   // hybrid: any CTA
+            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));   // hybrid: any CTA
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
@@ -1640,8 +1649,8 @@ la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem) {
     if (!ctx) return set_err(LA_EINVAL, "null context");
     if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
     int32_t *dw = nullptr, *dv = nullptr;
-    CK(cudaMalloc(&dw, sizeof(int32_t) * std::max<int64_t>(ctx->n_wire_api, 1)));
-    cudaError_t e = cudaMalloc(&dv, sizeof(int32_t) * std::max<int64_t>(ctx->n_via_api, 1));
+    CK(dmalloc(&dw, sizeof(int32_t) * std::max<int64_t>(ctx->n_wire_api, 1)));
+    cudaError_t e = dmalloc(&dv, sizeof(int32_t) * std::max<int64_t>(ctx->n_via_api, 1));
     if (e == cudaSuccess) e = launch_unpack_demand(ctx->G, ctx->d_wcap, ctx->d_vcap, dw, dv, ctx->d_wire_off, ctx->stream);
     if (e == cudaSuccess && wire_dem)
         e = cudaMemcpyAsync(wire_dem, dw, sizeof(int32_t) * ctx->n_wire_api, cudaMemcpyDeviceToHost, ctx->stream);
@@ -1650,8 +1659,8 @@ la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e == cudaSuccess)
         ctx->stats.d2h_bytes += (wire_dem ? 4 * ctx->n_wire_api : 0) + (via_dem ? 4 * ctx->n_via_api : 0);
-    cudaFree(dw);
-    if (dv) cudaFree(dv);
+    dfree(dw);
+    if (dv) dfree(dv);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_demand");
     return LA_OK;
 }
@@ -1723,11 +1732,11 @@ la_status la_eval_overflow(la_ctx *ctx, la_eval *out) {
     const size_t nh = (size_t)MAXL * 2 * nbins;
     const size_t nwords = 2 * nh + 2 * MAXL + 1 + MAXL + 1;   // hist w, hist v, legacy w, legacy v, oob, wl, vcuts
     if (!ctx->d_eval) {
-        CK(cudaMalloc(&ctx->d_eval, sizeof(unsigned long long) * nwords));
+        CK(dmalloc(&ctx->d_eval, sizeof(unsigned long long) * nwords));
         int8_t lay[3][MAXL] = {};
         for (int l = 0; l < L; l++) lay[ctx->dir[l]][ctx->G.lidx[l]] = (int8_t)l;
         for (int k = 0; k < L - 1; k++) lay[2][k] = (int8_t)k;            // via cut k: ofw of its lower layer (R36)
-        CK(cudaMalloc(&ctx->d_eval_lay, sizeof(lay)));
+        CK(dmalloc(&ctx->d_eval_lay, sizeof(lay)));
         CK(cudaMemcpyAsync(ctx->d_eval_lay, lay, sizeof(lay), cudaMemcpyHostToDevice, ctx->stream));
     }
     unsigned long long *b = ctx->d_eval;
@@ -1783,7 +1792,7 @@ la_status la_eval_overflow(la_ctx *ctx, la_eval *out) {
 la_status la_set_tracing(la_ctx *ctx, int32_t enable) {
     TRY(check_ready(ctx));
     if (enable && !ctx->d_trace) {
-        CK(cudaMalloc(&ctx->d_trace, sizeof(int64_t) * 5 * std::max<int64_t>(ctx->n_nets, 1)));
+        CK(dmalloc(&ctx->d_trace, sizeof(int64_t) * 5 * std::max<int64_t>(ctx->n_nets, 1)));
         CK(cudaMemsetAsync(ctx->d_trace, 0, sizeof(int64_t) * 5 * std::max<int64_t>(ctx->n_nets, 1), ctx->stream));
     }
     ctx->tracing = enable != 0;

@@ -12,6 +12,18 @@
 
 namespace gapla {
 
+// Device allocations of the library go through the stream-ordered allocator's default pool
+// (cudaMallocAsync on the legacy stream, then a sync so any stream may use the memory); the
+// pool keeps freed memory (release threshold raised in la_init_grid), so a new context for
+// the next design does not pay the driver's page mapping again.
+template <class T>
+inline cudaError_t dmalloc(T **p, size_t bytes) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(p), bytes ? bytes : 16, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    return e;
+}
+inline cudaError_t dfree(void *p) { return p ? cudaFreeAsync(p, 0) : cudaSuccess; }
+
 constexpr int MAXL = 16;                      // layers supported by the kernels
 constexpr int MAXKIDS = 4;                    // a GCell has 4 neighbours -> <= 4 children
 constexpr int MAXPAIRS = MAXL * (MAXL + 1) / 2;
