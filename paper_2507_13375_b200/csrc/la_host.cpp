@@ -879,18 +879,24 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("tree build");
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
-    for (int64_t i = 0; i < N; i++) by_rank[i] = i;
     if (n->order_key) {
-        const int64_t *ok = n->order_key;
-        par_sort(by_rank, [ok](int64_t a, int64_t b) { return ok[a] != ok[b] ? ok[a] < ok[b] : a < b; }, nthr);
+        // sort (key, index) pairs in place of indices: contiguous keys, no indirection in the comparator
+        std::vector<std::pair<int64_t, int64_t>> kv(N);
+        par_for(N, nthr, [&](int64_t i) { kv[i] = {n->order_key[i], i}; });
+        par_sort(kv, [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) { return a < b; },
+                 nthr);
+        par_for(N, nthr, [&](int64_t r) { by_rank[r] = kv[r].second; });
+    } else {
+        for (int64_t i = 0; i < N; i++) by_rank[i] = i;
     }
     std::vector<int64_t> fp_pos(N + 1, 0);
-    for (int64_t r = 0; r < N; r++) {
-        int64_t net = by_rank[r];
+    par_for(N, nthr, [&](int64_t r) {
+        const int64_t net = by_rank[r];
         const Chunk &ch = chunks[chunk_of[net]];
-        int64_t i = net - ch.beg;
-        fp_pos[r + 1] = fp_pos[r] + (ch.fp_off[i + 1] - ch.fp_off[i]);
-    }
+        const int64_t i = net - ch.beg;
+        fp_pos[r + 1] = ch.fp_off[i + 1] - ch.fp_off[i];
+    });
+    for (int64_t r = 0; r < N; r++) fp_pos[r + 1] += fp_pos[r];
     const int64_t n_fp = fp_pos[N];
     std::vector<uint64_t> keys(n_fp);
     {
