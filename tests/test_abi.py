@@ -117,3 +117,22 @@ def test_shard_range_partitions(la, n, world):
         assert b == c
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 1
+
+
+def test_paper_batches_argument_errors(la):
+    """la_paper_batches validates its arguments (include/la.h): alpha > 0, max_batch >= 1,
+    non-negative criticality (host-only call, no GPU needed)."""
+    d = synth.make_config(1)
+    crit = np.zeros(d.n_nets, np.int32)
+    for kw in (dict(alpha=0.0), dict(max_batch=0)):
+        args = dict(alpha=0.7, th=3, max_batch=100)
+        args.update(kw)
+        with pytest.raises(la.LaError) as ei:
+            la.la_paper_batches(d, crit, **args)
+        assert ei.value.status == la.LA_EINVAL
+    bad = crit.copy()
+    bad[3] = -1
+    with pytest.raises(la.LaError, match="criticality"):
+        la.la_paper_batches(d, bad)
+    b, nb = la.la_paper_batches(d, crit, max_batch=10**9)
+    assert nb >= 1 and b.min() == 0 and b.max() == nb - 1

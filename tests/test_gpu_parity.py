@@ -374,3 +374,25 @@ def test_sharded_path_host_transport(la, world, cfg, n):
     ref = oracle.run(d)
     for out in outs:
         assert_parity(out, ref, bitwise_fp=True)
+
+
+def test_new_call_order_errors(la):
+    """Call-order errors of the widened API: snapshot batches after la_load_nets, the host
+    transport on a single-rank context, the dataflow schedule with snapshot batches."""
+    d = synth.make_config(1)
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    with pytest.raises(la.LaError) as ei:
+        la.la_set_snapshot_batches(A.ctx, np.zeros(d.n_nets, np.int32))
+    assert ei.value.status == la.LA_ESTATE
+    A.assign_batch(0)
+    with pytest.raises(la.LaError) as ei:
+        la.la_get_decisions(A.ctx, 0)
+    assert ei.value.status == la.LA_ESTATE
+    A.close()
+    B = la.LayerAssigner(d, device=0)
+    B.load(snapshot_batches=np.zeros(d.n_nets, np.int32))
+    with pytest.raises(la.LaError) as ei:
+        B.set_schedule(la.LA_SCHED_DATAFLOW)
+    assert ei.value.status == la.LA_EINVAL
+    B.close()
