@@ -342,12 +342,10 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
     if (lane < L) {
         double V = 0.0;
         w.Vt[lane * MAXL + lane] = 0.0;
-#pragma unroll
-        for (int t = 1; t < MAXL; ++t) {
-            if (t > lane && t < L) {
-                V = V + kap[t - 1];
-                w.Vt[lane * MAXL + t] = V;
-            }
+#pragma unroll 1
+        for (int t = lane + 1; t < L; ++t) {
+            V = V + kap[t - 1];
+            w.Vt[lane * MAXL + t] = V;
         }
     }
     if (nk == 1) {
