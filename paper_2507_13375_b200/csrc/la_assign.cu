@@ -210,9 +210,10 @@ __device__ __forceinline__ int window_argmin(const WarpScr &w, const Shared &sh,
     double m = dinf();
     int jb = -1;
     const double *row = w.cpt + (e * MAXKIDS + k) * MAXE;
-#pragma unroll
-    for (int s = 0; s < MAXE; ++s) {
-        if (s < sh.ndir[dk]) {
+    const int nd = sh.ndir[dk];
+#pragma unroll 1
+    for (int s = 0; s < nd; ++s) {
+        {
             const int j = sh.lay_of[dk][s];
             if (j >= b && j <= t) {
                 const double cp = row[s];
