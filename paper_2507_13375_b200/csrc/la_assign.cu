@@ -142,6 +142,7 @@ __device__ __forceinline__ double kappa_w(const DevGrid &G, const Shared &sh, in
 
 // n-th (1-based) set bit of m
 __device__ __forceinline__ int nth_bit(uint32_t m, int n) {
+#pragma unroll 1
     for (int k = 1; k < n; ++k) m &= m - 1;
     return __ffs(m) - 1;
 }
@@ -157,6 +158,7 @@ __device__ __forceinline__ void finish_layer(const NetCtx &c, const Shared &sh, 
     const NodeRec &nd = nb.nd[i];
     double F0 = 0.0, C0 = 0.0;
     const int q0 = nd.sink0, qn = nd.nsink;
+#pragma unroll 1
     for (int q = q0; q < q0 + qn; ++q) {
         const double cq = nb.sk[q].cap;
         F0 = F0 + nb.sk[q].w * (cq * sh.T.VR[nb.player[q] * MAXL + l]);
@@ -197,6 +199,7 @@ __device__ void leaves_dp(const NetCtx &c, const Shared &sh, const DevGrid &G, i
         const bool pins = nl != 255;
         const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
         double V = 0.0;
+#pragma unroll 1
         for (int k = b0; k < t0; ++k) V = V + nb.kap[i * Lm1 + k];
         finish_layer(c, sh, G, i, false, l, s, V, 0.0, b0, t0, 0u);
     }
@@ -550,13 +553,16 @@ __device__ __forceinline__ void commit_node(const DevGrid &G, uint32_t xy, int e
         const int a = run_lo(edir, x, y, len);
         if (edir <= 1) {
             int32_t *wp = G.wH + ((int64_t)y * (G.X - 1) + a) * G.LH + G.lidx[l];
+#pragma unroll 1
             for (int e = 0; e < len; ++e) atomicAdd(wp + (int64_t)e * G.LH, 2);
         } else {
             int32_t *wp = G.wV + ((int64_t)x * (G.Y - 1) + a) * G.LV + G.lidx[l];
+#pragma unroll 1
             for (int e = 0; e < len; ++e) atomicAdd(wp + (int64_t)e * G.LV, 2);
         }
     }
     int32_t *vp = G.via + ((int64_t)y * G.X + x) * (G.L - 1);
+#pragma unroll 1
     for (int k = b; k < t; ++k) atomicAdd(vp + k, 2);
 }
 
@@ -571,6 +577,7 @@ __device__ __forceinline__ void backtrack_node(const NetCtx &c, const Shared &sh
     nd.st = (dec >> 4) & 0xf;
     const uint32_t js = dec >> 8;
     const int nk = nd.nkid;
+#pragma unroll 1
     for (int k = 0; k < nk; ++k) nb.nd[nd.kid[k]].lay = (uint8_t)((js >> (4 * k)) & 0xf);
 }
 
