@@ -598,6 +598,13 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
 // times): the NON-aligned barrier.sync counts threads, whereas __syncthreads
 // (bar.sync = barrier.sync.aligned) requires converged warps.
 __device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+// The same over the `n` threads of named barrier `id` (a half-CTA running one big net).
+// Immediate barrier ids keep ptxas from reserving all 16 (id 0: whole CTA, 1 / 2: halves).
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    if (id == 1) asm volatile("barrier.sync 1, %0;" ::"r"(n) : "memory");
+    else if (id == 2) asm volatile("barrier.sync 2, %0;" ::"r"(n) : "memory");
+    else asm volatile("barrier.sync 0, %0;" ::"r"(n) : "memory");
+}
 
 // Wait until net `net` has no unfinished predecessor (dataflow mode), with a
 // growing back-off so waiting warps leave the issue slots to working ones.
@@ -623,8 +630,8 @@ __device__ __forceinline__ void trace_end(int64_t *tr) {
 template <bool CTA>
 __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Shared &sh, const DevGrid &G,
                                         const DevForest &F, const DevScratch &S, const AssignLaunch &a, int64_t net,
-                                        int64_t n0, int q_base, int ns, int tid, int nthr) {
-    auto sync = [] { if (CTA) cta_sync(); else __syncwarp(); };
+                                        int64_t n0, int q_base, int ns, int tid, int nthr, int bar = 0) {
+    auto sync = [bar, nthr] { if (CTA) bar_sync(bar, nthr); else __syncwarp(); };
     const int nn = c.nn, lane = threadIdx.x & 31, warp = tid >> 5, nwarps = nthr >> 5;
     const bool flow = a.wait != nullptr;
     const int pdrv = F.net_pdrv[net];
@@ -649,7 +656,7 @@ __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Share
         int hi = lo + 1;
         while (hi < nn && c.nb.nd[hi].height == h) ++hi;
         for (int i = lo + warp; i < hi; i += nwarps) node_dp_wide(c, w, sh, G, i, pdrv, lane);
-        if (CTA) cta_sync();
+        if (CTA) bar_sync(bar, nthr);
         lo = hi;
     }
     if (tid == 0) {
@@ -683,7 +690,7 @@ __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Share
 // ------------------------------------------------------------------ kernel --
 __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
-    __shared__ int64_t big_item;
+    __shared__ int64_t big_item[2];
     extern __shared__ __align__(16) char dyn[];
     stage_tab(sh.T, G.tab);
     if (threadIdx.x < MAXL) {
@@ -710,14 +717,17 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
 
     // hybrid (batch mode: no waits): every CTA first takes big nets, then small ones
     if (a.hybrid || (int)blockIdx.x < a.n_big_ctas) {
-        // ---------------- big nets: the whole CTA per net ----------------
+        // ---------------- big nets: each half-CTA (2 warps) per net ----------------
+        // (a whole CTA idles at the level barriers of chain-like trees; two nets per CTA
+        // halve that).  DP state in the half's two slots, a global slot beyond that.
+        const int half = warp >> 1, htid = threadIdx.x & 63, bar = 1 + half;
         const int64_t n_work = a.big_end - a.big_beg;
-        char *gmine = a.gscratch ? a.gscratch + (int64_t)blockIdx.x * a.gslot_bytes : nullptr;
+        char *gmine = a.gscratch ? a.gscratch + ((int64_t)blockIdx.x * 2 + half) * a.gslot_bytes : nullptr;
         for (;;) {
-            cta_sync();
-            if (threadIdx.x == 0) big_item = (int64_t)atomicAdd(a.ticket + 1, 1ull);
-            cta_sync();
-            const int64_t wk = big_item;
+            bar_sync(bar, 64);
+            if (htid == 0) big_item[half] = (int64_t)atomicAdd(a.ticket + 1, 1ull);
+            bar_sync(bar, 64);
+            const int64_t wk = big_item[half];
             if (wk >= n_work) {
                 if (a.hybrid) break;
                 return;
@@ -726,9 +736,9 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
             const int64_t net = rec.x, n0 = (uint32_t)rec.y;
             const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
             const NetLay lay = net_layout(nn, ns, L, LD);
-            char *base = lay.bytes <= ASSIGN_WARPS * slay.bytes ? dyn : gmine;
+            char *base = lay.bytes <= 2 * slay.bytes ? dyn + (int64_t)half * 2 * slay.bytes : gmine;
             const NetCtx c{net_buf(base, lay), L, LD, nn};
-            run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, threadIdx.x, blockDim.x);
+            run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, htid, 64, bar);
         }
     }
 
@@ -764,8 +774,8 @@ size_t assign_net_bytes(int nodes, int sinks, int L, int LD) { return (size_t)ne
 
 int assign_nets_per_cta() { return ASSIGN_WARPS; }
 
-size_t assign_cta_net_bytes(int L, int LD, int NS, int NP) {
-    return (size_t)ASSIGN_WARPS * net_layout(NS, NP, L, LD).bytes;
+size_t assign_cta_net_bytes(int L, int LD, int NS, int NP) {   // shared memory of one big net (half-CTA)
+    return (size_t)2 * net_layout(NS, NP, L, LD).bytes;
 }
 
 cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm) {

@@ -1155,7 +1155,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->gslot_bytes = 0;
         if (max_big_nodes > 0 && need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP)) {
             ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
-            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid));   // hybrid: any CTA
+            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid * 2));   // per half-CTA
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
