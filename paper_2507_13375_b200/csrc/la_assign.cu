@@ -720,13 +720,17 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
         // ---------------- big nets: each half-CTA (2 warps) per net ----------------
         // (a whole CTA idles at the level barriers of chain-like trees; two nets per CTA
         // halve that).  DP state in the half's two slots, a global slot beyond that.
-        const int half = warp >> 1, htid = threadIdx.x & 63, bar = 1 + half;
+        // (big_split == 0: the whole CTA per net, for latency-bound launches with few nets)
+        const bool split = a.big_split != 0;
+        const int half = split ? warp >> 1 : 0, gsz = split ? 64 : 128;
+        const int htid = threadIdx.x & (gsz - 1), bar = split ? 1 + half : 0;
+        const int nslots = split ? 2 : ASSIGN_WARPS;
         const int64_t n_work = a.big_end - a.big_beg;
         char *gmine = a.gscratch ? a.gscratch + ((int64_t)blockIdx.x * 2 + half) * a.gslot_bytes : nullptr;
         for (;;) {
-            bar_sync(bar, 64);
+            bar_sync(bar, gsz);
             if (htid == 0) big_item[half] = (int64_t)atomicAdd(a.ticket + 1, 1ull);
-            bar_sync(bar, 64);
+            bar_sync(bar, gsz);
             const int64_t wk = big_item[half];
             if (wk >= n_work) {
                 if (a.hybrid) break;
@@ -736,9 +740,9 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
             const int64_t net = rec.x, n0 = (uint32_t)rec.y;
             const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
             const NetLay lay = net_layout(nn, ns, L, LD);
-            char *base = lay.bytes <= 2 * slay.bytes ? dyn + (int64_t)half * 2 * slay.bytes : gmine;
+            char *base = lay.bytes <= nslots * slay.bytes ? dyn + (int64_t)half * nslots * slay.bytes : gmine;
             const NetCtx c{net_buf(base, lay), L, LD, nn};
-            run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, htid, 64, bar);
+            run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, htid, gsz, bar);
         }
     }
 

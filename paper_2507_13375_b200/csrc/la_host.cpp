@@ -116,6 +116,7 @@ struct la_ctx {
     int32_t n_big_ctas = 0;
     std::vector<int32_t> snap_batch;          // la_set_snapshot_batches (input order); empty: conflict-free
     bool hybrid = true;                       // batch-mode launches: all CTAs take big nets first
+    int32_t big_split = -1;                   // -1: per launch (launch_grid); GAPLA_BIG_SPLIT=0/1 forces
     bool tracing = false;
     // tickets and the dataflow DAG (device)
     unsigned long long *d_ticket = nullptr;   // [n_batches + 1]: [0] dataflow, [1 + b] batch b
@@ -1148,6 +1149,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
         if (!big_pos.empty()) ctx->n_big_ctas = std::max(1, std::min(ctx->n_big_ctas, ctx->grid - 1));
         if (const char *e = getenv("GAPLA_HYBRID")) ctx->hybrid = atoi(e) != 0;
+        if (const char *e = getenv("GAPLA_BIG_SPLIT")) ctx->big_split = atoi(e);
         CK(dmalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
         if (N) CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
         // a big net keeps its DP state in its CTA's shared memory, or in a per-CTA global slot
@@ -1215,6 +1217,10 @@ static RankShare rank_share(const la_ctx *ctx, int32_t batch) {
 // Grid of one launch: the big-role CTAs it needs, then the small-role CTAs.
 static int launch_grid(const la_ctx *ctx, AssignLaunch &al) {
     const int64_t nbig = al.big_end - al.big_beg, nsmall = al.small_end - al.small_beg;
+    // big nets by half-CTAs when the launch is throughput-bound (several nets per resident
+    // warp), by whole CTAs (lower latency per big net) when it is bound by its slowest net
+    al.big_split = ctx->big_split >= 0 ? ctx->big_split
+                                       : (nbig + nsmall > (int64_t)4 * ctx->grid * ASSIGN_WARPS ? 1 : 0);
     const int npc = assign_nets_per_cta();
     if (!al.wait && ctx->hybrid) {   // batch mode: every CTA takes the batch's big nets first
         al.hybrid = 1;

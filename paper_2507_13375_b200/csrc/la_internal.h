@@ -106,6 +106,7 @@ struct AssignLaunch {
     int64_t small_beg, small_end;             // this launch's range of small_pos
     int32_t n_big_ctas;                       // CTAs [0, n_big_ctas) take big nets
     int32_t hybrid;                           // batch mode: every CTA takes big nets first, then small
+    int32_t big_split;                        // big nets by half-CTAs (throughput) or whole CTAs (latency)
     unsigned long long *ticket;               // [0] small, [1] big; zeroed before the launch
     int32_t *wait;                            // dataflow mode: unfinished predecessors per net
     const int64_t *succ_off;                  // [n_nets+1] successor CSR (forest order)
