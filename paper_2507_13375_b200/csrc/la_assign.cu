@@ -112,15 +112,31 @@ __device__ __forceinline__ NetBuf net_buf(char *b, const NetLay &w) {
     return n;
 }
 
-// Per-warp scratch of the wide node routine.
+// Per-warp scratch of the wide node routine, sized for the grid's L (rows of V) and LD (son
+// layer slots): V(b, t) [L][L]; cost'(l_e; s_k, slot) [LD][MAXKIDS][LD]; per entry best G',
+// key and layer.
 struct WarpScr {
-    double Vt[MAXL * MAXL];               // V(b, t) of the current node, [b][t]
-    double cpt[MAXE * MAXKIDS * MAXE];    // cost'(l_e; s_k, slot s), [e][k][s]
-    double bestG[MAXE];                   // per entry: best G'
-    uint32_t bestK[MAXE];                 // per entry: (t - b) << 4 | b, bit 8 = none
-    uint8_t el[MAXE];                     // per entry: its layer
+    double *Vt, *cpt, *bestG;
+    uint32_t *bestK;                      // (t - b) << 4 | b, bit 8 = none
+    uint8_t *el;
+    int vs, cs;                           // row strides: V (L), cost' (LD)
 };
-constexpr int SCR_BYTES = (int)((sizeof(WarpScr) + 15) & ~(size_t)15);
+
+__host__ __device__ inline int scr_bytes(int L, int LD) {
+    return ((8 * L * L + 8 * LD * MAXKIDS * LD + 8 * MAXE + 4 * MAXE + MAXE) + 15) & ~15;
+}
+
+__device__ __forceinline__ WarpScr warp_scr(char *b, int L, int LD) {
+    WarpScr w;
+    w.Vt = (double *)b;
+    w.cpt = w.Vt + L * L;
+    w.bestG = w.cpt + LD * MAXKIDS * LD;
+    w.bestK = (uint32_t *)(w.bestG + MAXE);
+    w.el = (uint8_t *)(w.bestK + MAXE);
+    w.vs = L;
+    w.cs = LD;
+    return w;
+}
 
 struct Shared {          // per-CTA static shared memory
     TechTab T;
@@ -212,7 +228,7 @@ __device__ __forceinline__ int window_argmin(const WarpScr &w, const Shared &sh,
                                              double *mv) {
     double m = dinf();
     int jb = -1;
-    const double *row = w.cpt + (e * MAXKIDS + k) * MAXE;
+    const double *row = w.cpt + (e * MAXKIDS + k) * w.cs;
     const int nd = sh.ndir[dk];
 #pragma unroll 1
     for (int s = 0; s < nd; ++s) {
@@ -285,7 +301,7 @@ __device__ __forceinline__ void node_dp_1son(const NetCtx &c, WarpScr &w, const 
             else if (j < b0) { b = j; m = pd; jm = jd; }
             else if (jnext > t0) { m = pu; jm = ju; }        // last son layer inside [b0, t0]: the base span
             if (jm >= 0) {
-                Gp = w.Vt[b * MAXL + t] + m;
+                Gp = w.Vt[b * w.vs + t] + m;
                 key = (uint32_t)(((t - b) << 4) | b);
             }
         }
@@ -315,7 +331,7 @@ __device__ __forceinline__ void node_dp_1son(const NetCtx &c, WarpScr &w, const 
                 const int b = key & 0xf, t = b + (int)((key >> 4) & 0xf), jm = (int)(key >> 12);
                 const SlotRec &rr = nb.sl[kk * LD + sh.lidx[jm]];
                 const double Bv = wdk * rr.C;
-                const double Gv = w.Vt[b * MAXL + t] + (rr.A + Bv * sh.T.VR[l * MAXL + jm]);
+                const double Gv = w.Vt[b * w.vs + t] + (rr.A + Bv * sh.T.VR[l * MAXL + jm]);
                 finish_layer(c, sh, G, i, root, l, slot, Gv, 0.0 + rr.C, b, t, (uint32_t)jm);
             }
         }
@@ -345,11 +361,11 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
     // (1) V table: lane b sums its row ascending from b (R10, R23)
     if (lane < L) {
         double V = 0.0;
-        w.Vt[lane * MAXL + lane] = 0.0;
+        w.Vt[lane * w.vs + lane] = 0.0;
 #pragma unroll 1
         for (int t = lane + 1; t < L; ++t) {
             V = V + kap[t - 1];
-            w.Vt[lane * MAXL + t] = V;
+            w.Vt[lane * w.vs + t] = V;
         }
     }
     if (nk == 1) {
@@ -359,10 +375,10 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
         return;
     }
     // (2) cost' table (O5, R16-R17): +inf where the son is infeasible on the layer
-    const int ncp = nE * nk * MAXE;
+    const int ncp = nE * nk * LD;
     for (int idx = lane; idx < ncp; idx += 32) {
-        const int e = idx / (nk * MAXE), r = idx - e * (nk * MAXE);
-        const int k = r / MAXE, s = r - k * MAXE;
+        const int e = idx / (nk * LD), r = idx - e * (nk * LD);
+        const int k = r / LD, s = r - k * LD;
         int kk = 0, dk = 0;
 #pragma unroll
         for (int q = 0; q < MAXKIDS; ++q) if (q == k) { kk = kid[q]; dk = kdt[q]; }
@@ -377,7 +393,7 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
             const double cost = A + Bv * sh.T.VR[l * MAXL + j];
             cp = cost + Bv * urn;
         }
-        w.cpt[(e * MAXKIDS + k) * MAXE + s] = cp;
+        w.cpt[(e * MAXKIDS + k) * w.cs + s] = cp;
     }
     __syncwarp();
     // (3) lanes over (entry e, span bottom b): 8-lane segments, one per entry, lane s8 takes
@@ -405,7 +421,7 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
                 if (k < nk) window_argmin(w, sh, e, k, kdt[k], b, t0, &m[k]);
             }
             auto evaluate = [&](int t) {
-                double g = w.Vt[b * MAXL + t];
+                double g = w.Vt[b * w.vs + t];
                 bool feas = true;
 #pragma unroll
                 for (int k = 0; k < MAXKIDS; ++k)
@@ -423,7 +439,7 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
 #pragma unroll
                 for (int k = 0; k < MAXKIDS; ++k)
                     if (k < nk && kdt[k] == dtt) {
-                        const double cp = w.cpt[(e * MAXKIDS + k) * MAXE + st];
+                        const double cp = w.cpt[(e * MAXKIDS + k) * w.cs + st];
                         if (cp < m[k]) m[k] = cp;
                     }
                 evaluate(t);
@@ -451,7 +467,7 @@ __device__ void node_dp_wide(const NetCtx &c, WarpScr &w, const Shared &sh, cons
             else nb.sl[i * LD + e].A = dinf();
         } else {
             const int b = key & 0xf, t = b + (int)(key >> 4);
-            double Gv = w.Vt[b * MAXL + t], K = 0.0;
+            double Gv = w.Vt[b * w.vs + t], K = 0.0;
             uint32_t js = 0;
 #pragma unroll
             for (int k = 0; k < MAXKIDS; ++k) {
@@ -713,7 +729,7 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
     const int L = G.L, LD = a.LD;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const NetLay slay = net_layout(a.NS, a.NP, L, LD);
-    WarpScr &w = *reinterpret_cast<WarpScr *>(dyn + ASSIGN_WARPS * slay.bytes + warp * SCR_BYTES);
+    WarpScr w = warp_scr(dyn + ASSIGN_WARPS * slay.bytes + warp * scr_bytes(L, LD), L, LD);
 
     // hybrid (batch mode: no waits): every CTA first takes big nets, then small ones
     if (a.hybrid || (int)blockIdx.x < a.n_big_ctas) {
@@ -771,7 +787,7 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(D
 }  // namespace
 
 size_t assign_smem_bytes(int L, int LD, int NS, int NP) {
-    return (size_t)ASSIGN_WARPS * (net_layout(NS, NP, L, LD).bytes + SCR_BYTES);
+    return (size_t)ASSIGN_WARPS * (net_layout(NS, NP, L, LD).bytes + scr_bytes(L, LD));
 }
 
 size_t assign_net_bytes(int nodes, int sinks, int L, int LD) { return (size_t)net_layout(nodes, sinks, L, LD).bytes; }
