@@ -158,35 +158,63 @@ __global__ void __launch_bounds__(ELMORE_THREADS) k_elmore(DevGrid G, DevForest 
         const int ln = S.lay[n], b = S.sb[n], t = S.st[n];
         TK(ln) = (n == n1 - 1) ? 0.0 : S.Tin[n];
         const int q0 = F.sink0[n], qn = F.nsink[n], nk = F.nkid[n];
-        for (int k = ln; k < t; ++k) {
-            const int j = k + 1;
-            double acc = 0.0;
-            for (int q = q0; q < q0 + qn; ++q) if (F.p_layer[q] >= j) acc = acc + F.p_cap[q];
-            for (int i = 0; i < nk; ++i) {
+        // the node's branches, read once: sons (layer, Cw + Cdown, Rw, Cw, Cdown) and up to 4
+        // sinks (layer, C_q) in registers; the C>= / C<= sums below keep the canonical order
+        int lsk[MAXKIDS];
+        double cbk[MAXKIDS], rwk[MAXKIDS], cwk[MAXKIDS], cdk[MAXKIDS];
+        int64_t sk[MAXKIDS];
+#pragma unroll
+        for (int i = 0; i < MAXKIDS; ++i) {
+            lsk[i] = 0; cbk[i] = rwk[i] = cwk[i] = cdk[i] = 0.0; sk[i] = 0;
+            if (i < nk) {
                 const int64_t s = F.kid[n * 4 + i];
-                const int ls = S.lay[s];
-                if (ls >= j) acc = acc + (T.c[ls] * (double)F.len[s] + S.Cd[s]);
+                const int ls = S.lay[s], len = F.len[s];
+                sk[i] = s;
+                lsk[i] = ls;
+                cwk[i] = T.c[ls] * (double)len;
+                rwk[i] = T.r[ls] * (double)len;
+                cdk[i] = S.Cd[s];
+                cbk[i] = cwk[i] + cdk[i];
             }
-            TK(k + 1) = TK(k) + T.vr[k] * acc;
         }
-        for (int k = ln; k > b; --k) {
-            const int j = k - 1;
+        const bool few = qn <= 4;
+        int pl[4];
+        double pc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            pl[u] = 0; pc[u] = 0.0;
+            if (few && u < qn) { pl[u] = F.p_layer[q0 + u]; pc[u] = F.p_cap[q0 + u]; }
+        }
+        // C>=(n, j) (up = true) or C<=(n, j): sinks in input order, then sons in child order
+        auto branch_sum = [&](int j, bool up) {
             double acc = 0.0;
-            for (int q = q0; q < q0 + qn; ++q) if (F.p_layer[q] <= j) acc = acc + F.p_cap[q];
-            for (int i = 0; i < nk; ++i) {
-                const int64_t s = F.kid[n * 4 + i];
-                const int ls = S.lay[s];
-                if (ls <= j) acc = acc + (T.c[ls] * (double)F.len[s] + S.Cd[s]);
+            if (few) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < qn && (up ? pl[u] >= j : pl[u] <= j)) acc = acc + pc[u];
+            } else {
+                for (int q = q0; q < q0 + qn; ++q) {
+                    const int pq = F.p_layer[q];
+                    if (up ? pq >= j : pq <= j) acc = acc + F.p_cap[q];
+                }
             }
-            TK(k - 1) = TK(k) + T.vr[k - 1] * acc;
+#pragma unroll
+            for (int i = 0; i < MAXKIDS; ++i)
+                if (i < nk && (up ? lsk[i] >= j : lsk[i] <= j)) acc = acc + cbk[i];
+            return acc;
+        };
+        for (int k = ln; k < t; ++k) TK(k + 1) = TK(k) + T.vr[k] * branch_sum(k + 1, true);
+        for (int k = ln; k > b; --k) TK(k - 1) = TK(k) + T.vr[k - 1] * branch_sum(k - 1, false);
+        if (few) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u < qn) S.sink_delay[F.p_orig[q0 + u]] = TK(pl[u]);
+        } else {
+            for (int q = q0; q < q0 + qn; ++q) S.sink_delay[F.p_orig[q]] = TK(F.p_layer[q]);
         }
-        for (int q = q0; q < q0 + qn; ++q) S.sink_delay[F.p_orig[q]] = TK(F.p_layer[q]);
-        for (int i = 0; i < nk; ++i) {
-            const int64_t s = F.kid[n * 4 + i];
-            const int ls = S.lay[s], len = F.len[s];
-            const double Cw = T.c[ls] * (double)len, Rw = T.r[ls] * (double)len;
-            S.Tin[s] = TK(ls) + Rw * (0.5 * Cw + S.Cd[s]);
-        }
+#pragma unroll
+        for (int i = 0; i < MAXKIDS; ++i)
+            if (i < nk) S.Tin[sk[i]] = TK(lsk[i]) + rwk[i] * (0.5 * cwk[i] + cdk[i]);
     }
 #undef TK
 }
