@@ -156,7 +156,10 @@ typedef struct {
 
 /* Create a context: validate the grid, allocate the packed device demand
  * planes, build the Eq. (3) marginal tables and the via-R table, set up NCCL
- * when world > 1.
+ * when world > 1 and nccl_id is given.  Device memory comes from the device's
+ * default stream-ordered pool (cudaMallocAsync); the library raises the pool's
+ * release threshold, so memory freed by la_destroy stays reserved for the next
+ * context of the process.
  * Errors: LA_EINVAL when L < 2 or L > 16, X or Y <= 1 or > 65535, any r, c,
  * vr, ofw, W_*, s_pos, s_zero or capacity negative, delta_lo > delta_hi, a
  * direction without a routable layer, bad rank/world; LA_ECUDA / LA_ENCCL on
