@@ -570,16 +570,16 @@ __device__ __forceinline__ void commit_node(const DevGrid &G, uint32_t xy, int e
         if (edir <= 1) {
             int32_t *wp = G.wH + ((int64_t)y * (G.X - 1) + a) * G.LH + G.lidx[l];
 #pragma unroll 1
-            for (int e = 0; e < len; ++e) atomicAdd(wp + (int64_t)e * G.LH, 2);
+            for (int e = 0; e < len; ++e) red_add(wp + (int64_t)e * G.LH, 2);
         } else {
             int32_t *wp = G.wV + ((int64_t)x * (G.Y - 1) + a) * G.LV + G.lidx[l];
 #pragma unroll 1
-            for (int e = 0; e < len; ++e) atomicAdd(wp + (int64_t)e * G.LV, 2);
+            for (int e = 0; e < len; ++e) red_add(wp + (int64_t)e * G.LV, 2);
         }
     }
     int32_t *vp = G.via + ((int64_t)y * G.X + x) * (G.L - 1);
 #pragma unroll 1
-    for (int k = b; k < t; ++k) atomicAdd(vp + k, 2);
+    for (int k = b; k < t; ++k) red_add(vp + k, 2);
 }
 
 // Backtrack of node i (Alg. 4): its span from choice[i][l_i], its sons' layers from entry.

@@ -9,6 +9,11 @@ namespace gapla {
 
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
+// Demand commit: a fire-and-forget integer reduction (RED, no returned value to wait for).
+__device__ __forceinline__ void red_add(int32_t *p, int32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
 
 // Eq. (3) marginal cost of one more unit on an element (reading R18):

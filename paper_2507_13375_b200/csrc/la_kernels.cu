@@ -86,15 +86,15 @@ __global__ void k_commit(DevGrid G, DevForest F, DevScratch S, int64_t node_beg,
         const int a = run_lo(ed, x, y, len);
         if (ed <= 1) {
             int32_t *wp = G.wH + ((int64_t)y * (G.X - 1) + a) * G.LH + G.lidx[l];
-            for (int i = 0; i < len; ++i) atomicAdd(wp + (int64_t)i * G.LH, 2);
+            for (int i = 0; i < len; ++i) red_add(wp + (int64_t)i * G.LH, 2);
         } else {
             int32_t *wp = G.wV + ((int64_t)x * (G.Y - 1) + a) * G.LV + G.lidx[l];
-            for (int i = 0; i < len; ++i) atomicAdd(wp + (int64_t)i * G.LV, 2);
+            for (int i = 0; i < len; ++i) red_add(wp + (int64_t)i * G.LV, 2);
         }
     }
     const int b = S.sb[n], t = S.st[n];
     int32_t *vp = G.via + ((int64_t)y * G.X + x) * (G.L - 1);
-    for (int k = b; k < t; ++k) atomicAdd(vp + k, 2);
+    for (int k = b; k < t; ++k) red_add(vp + k, 2);
 }
 
 __global__ void k_pack_dec(DevScratch S, int64_t node_beg, int64_t node_end) {
