@@ -203,13 +203,15 @@ la_status la_get_decisions(la_ctx *ctx, int32_t batch, uint32_t *dec, double *ne
 la_status la_put_decisions(la_ctx *ctx, int32_t batch, const uint32_t *dec, const double *net_cost);
 
 /* Every remaining batch (the whole Alg. 2 loop), enqueued.  Collective.
- * Default (LA_SCHED_BATCH): la_assign_batch + la_commit_demand for every
- * remaining batch, one k_assign launch per batch in which every CTA first takes
- * the batch's big nets, then its small nets.  With one rank, schedule
- * LA_SCHED_DATAFLOW and no batch assigned since the last load / la_reset, this
- * is ONE persistent launch in which each net starts as soon as every
- * earlier-priority net sharing a footprint element with it has committed
- * (DESIGN §2).  Both are bit-identical to sequential assignment. */
+ * LA_SCHED_BATCH: la_assign_batch + la_commit_demand for every remaining batch,
+ * one k_assign launch per batch in which every CTA first takes the batch's big
+ * nets, then its small nets.  LA_SCHED_DATAFLOW (one rank, no batch assigned
+ * since the last load / la_reset): ONE persistent launch in which each net
+ * starts as soon as every earlier-priority net sharing a footprint element with
+ * it has committed.  Without la_set_schedule the library picks
+ * DATAFLOW when the design has at most as many nets as resident warps (one wave,
+ * latency-bound) and BATCH otherwise.  Both are bit-identical to sequential
+ * assignment. */
 la_status la_assign_all(la_ctx *ctx);
 
 /* Paper-style snapshot batches (PAPER §III-A l.224-226 "nets in a
@@ -245,7 +247,7 @@ la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t 
 la_status la_paper_batches(const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
                            int64_t max_batch, int32_t *batch_of, int32_t *n_batches);
 
-/* Schedule used by la_assign_all on one rank; LA_SCHED_BATCH is the default. */
+/* Schedule used by la_assign_all on one rank; automatic until set. */
 enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };
 la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an unknown value */
 

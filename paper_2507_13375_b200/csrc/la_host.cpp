@@ -99,7 +99,7 @@ struct la_ctx {
     int32_t LD = 0;                           // layer slots per direction
     int32_t NS = NS_DEFAULT, NP = NP_DEFAULT; // small-path capacities of k_assign
     int32_t grid = 0;                         // resident k_assign CTAs (persistent grid)
-    int32_t schedule = LA_SCHED_BATCH;        // measured faster on B200; dataflow on request
+    int32_t schedule = -1;                    // -1: automatic (la_assign_all); else LA_SCHED_*
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
     bool host_xport = false;                  // world > 1 without NCCL: la_get_decisions / la_put_decisions
@@ -1412,7 +1412,11 @@ static la_status build_flow_lists(la_ctx *ctx) {
 la_status la_assign_all(la_ctx *ctx) {
     TRY(check_ready(ctx));
     const int32_t nb = (int32_t)ctx->batch_net0.size() - 1;
-    if (ctx->world == 1 && ctx->fuse_commit && ctx->schedule == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
+    // automatic schedule: one dataflow launch when the whole design fits in one wave
+    // of resident warps (latency-bound), batch by batch otherwise (throughput-bound)
+    const int32_t sched = ctx->schedule >= 0 ? ctx->schedule
+                        : (ctx->n_nets <= (int64_t)ctx->grid * ASSIGN_WARPS ? LA_SCHED_DATAFLOW : LA_SCHED_BATCH);
+    if (ctx->world == 1 && ctx->fuse_commit && sched == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
         ctx->next_batch == 0 && !ctx->flow_dirty) {
         // one persistent launch over every net, in bottom-level priority order
         TRY(build_flow_lists(ctx));
