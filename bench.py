@@ -32,7 +32,7 @@ DEFAULT_CONFIG = 5
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, help="BASELINE.json config (1-based)")
     ap.add_argument("--n-nets", type=int, default=None, help="override the config's net count")
