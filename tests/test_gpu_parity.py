@@ -340,7 +340,7 @@ def test_snapshot_batches_parity(la, kind):
         assert np.array_equal(seq["wires"], ref["wires"]) and np.array_equal(seq["wire_dem"], ref["wire_dem"])
 
 
-@pytest.mark.parametrize("world,cfg,n", [(2, 2, None), (3, 4, 60_000)])
+@pytest.mark.parametrize("world,cfg,n", [(2, 2, None), (3, 4, 60_000), (4, 2, 40_000), (8, 3, 60_000)])
 def test_sharded_path_host_transport(la, world, cfg, n):
     """The multi-GPU data path on one GPU: `world` contexts, one per
     rank, each assigns only its shard of every batch (la_shard_range over the batch's big and
