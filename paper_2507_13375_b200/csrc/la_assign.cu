@@ -609,12 +609,10 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t *p) {
     return v;
 }
 
-// CTA barrier that is correct when a warp arrives diverged (one thread spins
-// on a dependency counter; warps leave a level's node loop at different
-// times): the NON-aligned barrier.sync counts threads, whereas __syncthreads
-// (bar.sync = barrier.sync.aligned) requires converged warps.
-__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
-// The same over the `n` threads of named barrier `id` (a half-CTA running one big net).
+// CTA barriers are the NON-aligned barrier.sync (it counts threads; __syncthreads =
+// barrier.sync.aligned requires converged warps, and a group's warps reach it diverged: one thread
+// spins on a dependency counter, warps leave a level's node loop at different times).
+// Over the `n` threads of named barrier `id` (0: the whole CTA; 1 / 2: a half-CTA running one big net).
 // Immediate barrier ids keep ptxas from reserving all 16 (id 0: whole CTA, 1 / 2: halves).
 __device__ __forceinline__ void bar_sync(int id, int n) {
     if (id == 1) asm volatile("barrier.sync 1, %0;" ::"r"(n) : "memory");

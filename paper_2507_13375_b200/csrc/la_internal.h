@@ -77,10 +77,10 @@ struct DevForest {
 // its warp's slot; a larger ("big") net is run by a whole CTA.
 constexpr int NS_DEFAULT = 28;              // replaced at load time by the SLOT_BYTES fit
 constexpr int NP_DEFAULT = 48;
-constexpr int SLOT_BYTES = 4096;            // shared memory per warp's net slot (4 warps per CTA, 6 CTAs per SM)
+constexpr int SLOT_BYTES = 4096;            // shared memory per warp's net slot (4 warps per CTA, 7 CTAs per SM)
 constexpr int ASSIGN_WARPS = 4;
 #ifndef ASSIGN_MIN_CTAS
-#define ASSIGN_MIN_CTAS 6                   // k_assign CTAs per SM the register budget targets
+#define ASSIGN_MIN_CTAS 7                   // k_assign CTAs per SM the register budget targets
 #endif
 
 struct DevScratch {

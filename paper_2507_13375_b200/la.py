@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "lib", "libgapla.so")
+SO_PATH = os.path.join(_PKG, "lib", os.environ.get("GAPLA_SO", "libgapla.so"))   # GAPLA_SO: A/B builds in lib/
 
 P = ctypes.POINTER
 c_i32, c_i64, c_u8, c_f64, c_void_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8, ctypes.c_double, ctypes.c_void_p
