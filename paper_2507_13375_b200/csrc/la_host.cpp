@@ -21,9 +21,12 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include <nccl.h>
 
@@ -48,11 +51,26 @@ const int OPP[4] = {DIR_W, DIR_E, DIR_S, DIR_N};
 }  // namespace
 
 namespace gapla {
-// Host staging vectors without the serial zero-fill of value-initialisation.
+// Host staging vectors without the serial zero-fill of value-initialisation.  Large buffers
+// (>= 32 MB: the forest staging, footprint keys) are 2 MB-aligned and madvise'd for transparent
+// huge pages, so the threads that first touch them take ~500x fewer page faults.
 template <class T>
 struct default_init_alloc : std::allocator<T> {
     template <class U> struct rebind { using other = default_init_alloc<U>; };
     using std::allocator<T>::allocator;
+    static constexpr size_t HUGE_MIN = (size_t)32 << 20, HUGE_ALIGN = (size_t)2 << 20;
+    T *allocate(size_t n) {
+        const size_t bytes = n * sizeof(T);
+        if (bytes < HUGE_MIN) return std::allocator<T>::allocate(n);
+        void *p = std::aligned_alloc(HUGE_ALIGN, (bytes + HUGE_ALIGN - 1) & ~(HUGE_ALIGN - 1));
+        if (!p) throw std::bad_alloc();
+        madvise(p, bytes, MADV_HUGEPAGE);   // advisory: ignored where THP is off
+        return static_cast<T *>(p);
+    }
+    void deallocate(T *p, size_t n) {
+        if (n * sizeof(T) < HUGE_MIN) std::allocator<T>::deallocate(p, n);
+        else std::free(p);
+    }
     template <class U> void construct(U *p) { ::new ((void *)p) U; }
     template <class U, class... A> void construct(U *p, A &&...a) { ::new ((void *)p) U(std::forward<A>(a)...); }
 };
@@ -234,6 +252,15 @@ void par_for(int64_t n, unsigned nthr, F f) {
     for (unsigned t = 1; t < nthr; t++)
         th.emplace_back([&, t] { for (int64_t i = n * t / nthr; i < n * (t + 1) / nthr; i++) f(i); });
     for (int64_t i = 0; i < n / nthr; i++) f(i);
+    for (auto &x : th) x.join();
+}
+
+// Run f(t, begin, end) on nthr threads over contiguous blocks [n*t/nthr, n*(t+1)/nthr).
+template <class F>
+void par_chunks(int64_t n, unsigned nthr, F f) {
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nthr; t++) th.emplace_back([&, t] { f(t, n * t / nthr, n * (t + 1) / nthr); });
+    f(0, 0, n / nthr);
     for (auto &x : th) x.join();
 }
 
@@ -844,6 +871,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         worker();
         for (auto &t : th) t.join();
     }
+    phase("  build threads");
     for (auto &ch : chunks)
         if (ch.err_net >= 0) return set_err(LA_EINVAL, ch.err);
 
@@ -880,13 +908,56 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("tree build");
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
-    if (n->order_key) {
+    // key range of order_key: a small range (priorities, wirelengths) is ordered by a parallel
+    // counting sort, stable in input order -- the same (key, index) order as the comparison sort
+    int64_t kmin = 0, kmax = -1;
+    if (n->order_key && N > 0) {
+        const unsigned nt = std::max(1u, nthr);
+        std::vector<int64_t> lo(nt, INT64_MAX), hi(nt, INT64_MIN);
+        par_chunks(N, nt, [&](unsigned t, int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; i++) { lo[t] = std::min(lo[t], n->order_key[i]); hi[t] = std::max(hi[t], n->order_key[i]); }
+        });
+        kmin = *std::min_element(lo.begin(), lo.end());
+        kmax = *std::max_element(hi.begin(), hi.end());
+    }
+    const uint64_t span = (uint64_t)kmax - (uint64_t)kmin;    // no signed overflow for any key range
+    const unsigned nt_c = (unsigned)std::max<int64_t>(1, std::min<int64_t>(std::max(1u, nthr), N / 65536 + 1));
+    bool permutation = false;                           // keys kmin .. kmin+N-1, each once: rank = key - kmin
+    if (n->order_key && N > 0 && span == (uint64_t)(N - 1)) {
+        par_for(N, nthr, [&](int64_t r) { by_rank[r] = -1; });
+        par_for(N, nthr, [&](int64_t i) { by_rank[n->order_key[i] - kmin] = i; });
+        std::atomic<bool> full{true};
+        par_chunks(N, nt_c, [&](unsigned, int64_t a, int64_t b) {
+            for (int64_t r = a; r < b; r++) if (by_rank[r] < 0) { full = false; break; }
+        });
+        permutation = full;                             // N writes fill N slots only if no key repeats
+        if (permutation) phase("  priority order (permutation)");
+    }
+    const bool counting = !permutation && n->order_key && N > 0 &&
+                          span < (uint64_t)std::min<int64_t>(N + 1024, ((int64_t)1 << 23) / nt_c);   // <= 64 MB of counters
+    if (counting) {
+        const int64_t R = kmax - kmin + 1;
+        const unsigned nt = nt_c;
+        std::vector<std::vector<int64_t>> cnt(nt, std::vector<int64_t>(R, 0));
+        par_chunks(N, nt, [&](unsigned t, int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; i++) cnt[t][n->order_key[i] - kmin]++;
+        });
+        int64_t run = 0;                                    // exclusive offsets, key-major, then thread (input) order
+        for (int64_t k = 0; k < R; k++)
+            for (unsigned t = 0; t < nt; t++) { const int64_t c = cnt[t][k]; cnt[t][k] = run; run += c; }
+        par_chunks(N, nt, [&](unsigned t, int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; i++) by_rank[cnt[t][n->order_key[i] - kmin]++] = i;
+        });
+        phase("  priority sort (counting)");
+    } else if (permutation) {
+    } else if (n->order_key) {
         // sort (key, index) pairs in place of indices: contiguous keys, no indirection in the comparator
         std::vector<std::pair<int64_t, int64_t>> kv(N);
         par_for(N, nthr, [&](int64_t i) { kv[i] = {n->order_key[i], i}; });
         par_sort(kv, [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) { return a < b; },
                  nthr);
         par_for(N, nthr, [&](int64_t r) { by_rank[r] = kv[r].second; });
+        phase("  priority sort");
     } else {
         for (int64_t i = 0; i < N; i++) by_rank[i] = i;
     }
@@ -899,7 +970,8 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     });
     for (int64_t r = 0; r < N; r++) fp_pos[r + 1] += fp_pos[r];
     const int64_t n_fp = fp_pos[N];
-    std::vector<uint64_t> keys(n_fp);
+    phase("  footprint offsets");
+    hvec<uint64_t> keys(n_fp);
     {
         std::atomic<int64_t> nx{0};
         auto fill = [&]() {
@@ -946,10 +1018,10 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                                              &ctx->stats.launches, &dag);
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "conflict-free batching"); }
     }
-    std::vector<uint64_t>().swap(keys);
+    hvec<uint64_t>().swap(keys);
     auto t2 = std::chrono::steady_clock::now();
     ctx->batch_of_net.assign(N, 0);
-    for (int64_t r = 0; r < N; r++) ctx->batch_of_net[by_rank[r]] = batch_of_rank[r];
+    par_for(N, nthr, [&](int64_t r) { ctx->batch_of_net[by_rank[r]] = batch_of_rank[r]; });
 
     phase("GPU batching");
     // ---- batch-major net order: by batch, then node count descending, then rank
@@ -960,10 +1032,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         for (int32_t b = 0; b < nb; b++) cnt[b + 1] += cnt[b];
         ctx->batch_net0.assign(cnt.begin(), cnt.end());
         std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
-        for (int64_t r = 0; r < N; r++) {
-            int64_t net = by_rank[r];
-            pos_net[cur[ctx->batch_of_net[net]]++] = net;
-        }
+        for (int64_t r = 0; r < N; r++) pos_net[cur[batch_of_rank[r]]++] = by_rank[r];
         // big nets (CTA path) first, then by node count descending, then rank: the longest nets
         // start first.  Key per position: !big | (65535 - nodes) | offset in the batch (rank order).
         std::atomic<int32_t> nxt{0};
@@ -998,10 +1067,12 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     small_pos.reserve(N);
     ctx->batch_big0.assign(1, 0);
     ctx->batch_small0.assign(1, 0);
+    std::vector<uint8_t> big_at(N);
+    par_for(N, nthr, [&](int64_t p) { big_at[p] = is_big(pos_net[p]) ? 1 : 0; });
     for (int32_t b = 0; b < nb; b++) {
         for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++) {
-            const int64_t net = pos_net[p];
-            if (is_big(net)) {
+            if (big_at[p]) {
+                const int64_t net = pos_net[p];
                 big_pos.push_back((int32_t)p);
                 max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
                 max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
@@ -1024,9 +1095,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->fuse_commit = false;                                  // commits after the whole batch (snapshot)
         ctx->schedule = LA_SCHED_BATCH;
     } else {
-        std::vector<int64_t> rank_of_net(N), rank_of_pos(N);
-        for (int64_t r = 0; r < N; r++) rank_of_net[by_rank[r]] = r;
-        for (int64_t p = 0; p < N; p++) rank_of_pos[p] = rank_of_net[pos_net[p]];
+        hvec<int64_t> rank_of_net(N), rank_of_pos(N);
+        par_for(N, nthr, [&](int64_t r) { rank_of_net[by_rank[r]] = r; });
+        par_for(N, nthr, [&](int64_t p) { rank_of_pos[p] = rank_of_net[pos_net[p]]; });
         cudaError_t e = gpu_dag_to_positions(dag, rank_of_pos.data(), &ctx->d_succ_off, &ctx->d_succ, &ctx->d_indeg,
                                              ctx->stream, &ctx->stats.launches);
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "dependency DAG"); }
@@ -1036,12 +1107,14 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     // offsets in final order
     std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
     int64_t max_nodes = 0;
+    par_for(N, nthr, [&](int64_t p) {
+        node0[p + 1] = nn_of[pos_net[p]];
+        sink0g[p + 1] = ns_of[pos_net[p]];
+    });
     for (int64_t p = 0; p < N; p++) {
-        const int64_t net = pos_net[p];
-        const int64_t nn = nn_of[net];
-        node0[p + 1] = node0[p] + nn;
-        sink0g[p + 1] = sink0g[p] + ns_of[net];
-        max_nodes = std::max(max_nodes, nn);
+        max_nodes = std::max(max_nodes, node0[p + 1]);
+        node0[p + 1] += node0[p];
+        sink0g[p + 1] += sink0g[p];
     }
     const int64_t NN = node0[N], NS = sink0g[N];
     ctx->n_nodes = NN;
@@ -1141,7 +1214,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->h_small_pos = small_pos;
         ctx->h_net_node0.assign(node0.begin(), node0.end());
         ctx->h_net_sink0.assign(sink0g.begin(), sink0g.end());
+        phase("  (ticket alloc)");
         const std::vector<int4> ib = pack_nets(ctx, big_pos), is = pack_nets(ctx, small_pos);
+        phase("  (pack_nets)");
         TRY(dev_upload(ctx, &ctx->d_big_pos, ib.data(), ib.size()));
         TRY(dev_upload(ctx, &ctx->d_small_pos, is.data(), is.size()));
         // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
@@ -1161,7 +1236,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
+    phase("  (slots)");
     CK(cudaStreamSynchronize(ctx->stream));
+    phase("  (sync)");
     ctx->h_xy.swap(xy);
     ctx->h_len.swap(len);
     ctx->h_edir.swap(edir);

@@ -396,3 +396,25 @@ def test_new_call_order_errors(la):
         B.set_schedule(la.LA_SCHED_DATAFLOW)
     assert ei.value.status == la.LA_EINVAL
     B.close()
+
+
+@pytest.mark.parametrize("kind", ["permutation", "reversed", "ties", "sparse", "negative"])
+def test_priority_key_shapes(la, kind):
+    """Alg. 2's net order is (order_key, index) ascending (reading R43 / DESIGN §3).  la_load_nets
+    takes it by direct placement (a permutation of a key range), a stable parallel counting sort
+    (small key range, ties by index: 'ties' uses 150k nets so several threads split the count),
+    or a comparison sort (sparse or huge ranges); every shape must give the oracle's order, batches
+    and solution bit for bit."""
+    n = 150_000 if kind == "ties" else 30_000
+    d = synth.make_config(2, n_nets=n)
+    rng = np.random.default_rng(11)
+    if kind == "reversed":
+        d.order_key = (d.n_nets - 1 - d.order_key).astype(np.int64) + 7
+    elif kind == "ties":
+        d.order_key = rng.integers(0, 300, d.n_nets).astype(np.int64)
+    elif kind == "sparse":
+        d.order_key = (d.order_key * 1_000_003 + rng.integers(0, 2, d.n_nets)).astype(np.int64) - (1 << 62)
+    elif kind == "negative":
+        d.order_key = rng.integers(-(1 << 62), 1 << 62, d.n_nets).astype(np.int64)
+        d.order_key[:4] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max, 0, 0]
+    assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
