@@ -702,7 +702,11 @@ __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Share
 }
 
 // ------------------------------------------------------------------ kernel --
-__global__ void __launch_bounds__(ASSIGN_WARPS * 32, ASSIGN_MIN_CTAS) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
+// Two register budgets of the same kernel: MINB = ASSIGN_CTAS_LAT (6 CTAs/SM, 80 registers) for
+// launches bound by their slowest net (fewer spills on the serial path), MINB = ASSIGN_CTAS_THR
+// (7 CTAs/SM, 72 registers) for throughput-bound launches (more resident warps hide latency).
+template <int MINB>
+__global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
     __shared__ int64_t big_item[2];
     extern __shared__ __align__(16) char dyn[];
@@ -796,11 +800,18 @@ size_t assign_cta_net_bytes(int L, int LD, int NS, int NP) {   // shared memory 
     return (size_t)2 * net_layout(NS, NP, L, LD).bytes;
 }
 
-cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm) {
-    const size_t smem = assign_smem_bytes(L, LD, NS, NP);
-    cudaError_t e = cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int MINB>
+static cudaError_t resident(size_t smem, int *per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(k_assign<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_assign, ASSIGN_WARPS * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_assign<MINB>, ASSIGN_WARPS * 32, smem);
+}
+
+cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm_lat, int *per_sm_thr, int *n_sm) {
+    const size_t smem = assign_smem_bytes(L, LD, NS, NP);
+    cudaError_t e = resident<ASSIGN_CTAS_LAT>(smem, per_sm_lat);
+    if (e != cudaSuccess) return e;
+    e = resident<ASSIGN_CTAS_THR>(smem, per_sm_thr);
     if (e != cudaSuccess) return e;
     int dev = 0;
     e = cudaGetDevice(&dev);
@@ -808,17 +819,23 @@ cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int
     return cudaDeviceGetAttribute(n_sm, cudaDevAttrMultiProcessorCount, dev);
 }
 
-cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
-                          cudaStream_t s) {
-    if ((a.small_end <= a.small_beg && a.big_end <= a.big_beg) || grid <= 0) return cudaSuccess;
-    const size_t smem = assign_smem_bytes(G.L, a.LD, a.NS, a.NP);
+template <int MINB>
+static cudaError_t launch(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
+                          size_t smem, cudaStream_t s) {
     if (a.wait) {
         // dataflow mode: every CTA must be co-resident (nets wait on each other)
         void *args[] = {(void *)&G, (void *)&F, (void *)&S, (void *)&a};
-        return cudaLaunchCooperativeKernel((const void *)k_assign, dim3(grid), dim3(ASSIGN_WARPS * 32), args, smem, s);
+        return cudaLaunchCooperativeKernel((const void *)k_assign<MINB>, dim3(grid), dim3(ASSIGN_WARPS * 32), args, smem, s);
     }
-    k_assign<<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
+    k_assign<MINB><<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
+                          bool throughput, cudaStream_t s) {
+    if ((a.small_end <= a.small_beg && a.big_end <= a.big_beg) || grid <= 0) return cudaSuccess;
+    const size_t smem = assign_smem_bytes(G.L, a.LD, a.NS, a.NP);
+    return throughput ? launch<ASSIGN_CTAS_THR>(G, F, S, a, grid, smem, s) : launch<ASSIGN_CTAS_LAT>(G, F, S, a, grid, smem, s);
 }
 
 }  // namespace gapla

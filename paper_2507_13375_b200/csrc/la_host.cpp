@@ -116,7 +116,9 @@ struct la_ctx {
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
     int32_t LD = 0;                           // layer slots per direction
     int32_t NS = NS_DEFAULT, NP = NP_DEFAULT; // small-path capacities of k_assign
-    int32_t grid = 0;                         // resident k_assign CTAs (persistent grid)
+    int32_t grid = 0;                         // resident k_assign CTAs (persistent grid), latency variant
+    int32_t grid_thr = 0;                     // the same, throughput variant (more CTAs per SM)
+    int32_t assign_variant = -1;              // -1: per launch; GAPLA_ASSIGN_VARIANT=0 latency / 1 throughput
     int32_t schedule = -1;                    // -1: automatic (la_assign_all); else LA_SCHED_*
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
@@ -318,7 +320,7 @@ struct BuiltNet {
     std::vector<double> p_cap, p_w;
     std::vector<int64_t> p_orig;
     std::vector<uint64_t> fp;      // footprint elements
-    int64_t wl = 0;
+    int64_t wl = 0;                // unit edges (summed over the nets appended)
     int64_t wsw = 0;               // sum over tree edges of len x #legal layers of the edge direction
 };
 
@@ -340,7 +342,8 @@ struct Builder {
     std::vector<int32_t> sink_cnt, sink_beg;        // sinks per node: CSR over sink_list
     std::vector<int64_t> sink_list, pin_node;       // input pin indices, grouped by node in input order
     std::vector<double> w, ur, pwq;                 // pwq: Eq. (4) weight per pin of the net
-    std::vector<int32_t> order, finalid, pre, vof;
+    std::vector<int32_t> order, finalid, pre, vof, hcnt;
+    int last_height = 0;                            // height of the last built net's root
     std::vector<uint8_t> seen;
 
     // GCell -> vertex index: open-addressing hash over vs (built once per net)
@@ -556,16 +559,22 @@ struct Builder {
         for (int32_t n : pre)
             ur[n] = (ppar[n] < 0) ? (nd->r_drv ? nd->r_drv[net] : 0.0) : ur[ppar[n]] + ctx->r_avg * plen[n];
         // final order: height ascending, then preorder
-        order.assign(pre.begin(), pre.end());
-        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return pheight[a] < pheight[b]; });
+        // (counting sort by height, stable in preorder; the root has the largest height)
+        hcnt.assign((size_t)pheight[pre[0]] + 2, 0);
+        for (int32_t n : pre) hcnt[pheight[n] + 1]++;
+        for (size_t h = 1; h < hcnt.size(); h++) hcnt[h] += hcnt[h - 1];
+        order.resize(nn);
+        for (int32_t n : pre) order[hcnt[pheight[n]]++] = n;
         finalid.assign(nn, -1);
         for (size_t i = 0; i < nn; i++) finalid[order[i]] = (int32_t)i;
-        out.xy.resize(nn); out.kid.assign(nn * 4, -1); out.len.resize(nn); out.edir.resize(nn);
-        out.nkid.resize(nn); out.nl.resize(nn); out.nh.resize(nn); out.sink0.resize(nn); out.nsink.resize(nn);
-        out.wd.resize(nn); out.ur.resize(nn); out.height.resize(nn);
-        out.p_layer.clear(); out.p_cap.clear(); out.p_w.clear(); out.p_orig.clear();
-        for (size_t i = 0; i < nn; i++) {
-            int32_t n = order[i];
+        // appended to the chunk's arrays (node ids and sink offsets stay net-local)
+        const size_t b0 = out.xy.size(), q0 = out.p_layer.size();
+        out.xy.resize(b0 + nn); out.kid.resize((b0 + nn) * 4, -1); out.len.resize(b0 + nn); out.edir.resize(b0 + nn);
+        out.nkid.resize(b0 + nn); out.nl.resize(b0 + nn); out.nh.resize(b0 + nn); out.sink0.resize(b0 + nn);
+        out.nsink.resize(b0 + nn); out.wd.resize(b0 + nn); out.ur.resize(b0 + nn); out.height.resize(b0 + nn);
+        for (size_t j = 0; j < nn; j++) {
+            const size_t i = b0 + j;
+            int32_t n = order[j];
             out.xy[i] = (uint32_t)px[n] | ((uint32_t)py[n] << 16);
             for (int k = 0; k < pnk[n]; k++) out.kid[i * 4 + k] = finalid[pkids[n][k]];
             out.len[i] = plen[n];
@@ -576,7 +585,7 @@ struct Builder {
             out.wd[i] = ctx->W_D * w[n];
             out.ur[i] = ur[n];
             out.height[i] = (uint16_t)std::min(pheight[n], 65535);
-            out.sink0[i] = (int32_t)out.p_layer.size();
+            out.sink0[i] = (int32_t)(out.p_layer.size() - q0);
             out.nsink[i] = (uint16_t)(sink_beg[n + 1] - sink_beg[n]);
             for (int32_t qi = sink_beg[n]; qi < sink_beg[n + 1]; qi++) {
                 const int64_t q = sink_list[qi];
@@ -588,14 +597,13 @@ struct Builder {
             }
         }
         // footprint = unit edges U node GCells (disjoint element spaces)
-        out.fp.clear();
         for (uint64_t k : ek) out.fp.push_back(k);
         const uint64_t gbase = (uint64_t)2 * X * Y;
         for (size_t n = 0; n < nn; n++) out.fp.push_back(gbase + (uint64_t)py[n] * X + px[n]);
-        out.wl = (int64_t)ek.size();
-        out.wsw = 0;
+        out.wl += (int64_t)ek.size();
         for (size_t n = 0; n < nn; n++)
             if (ppar[n] >= 0) out.wsw += (int64_t)plen[n] * nlegal[(pedir[n] == DIR_E || pedir[n] == DIR_W) ? 0 : 1];
+        last_height = pheight[pre[0]];
         return "";
     }
 };
@@ -607,12 +615,8 @@ struct Chunk {
     BuiltNet acc;                                      // concatenated arrays
     std::string err;
     int64_t err_net = -1;
-    int64_t wl = 0, wsw = 0;
     int max_height = 0;
 };
-
-template <class T>
-void append(std::vector<T> &a, const std::vector<T> &b) { a.insert(a.end(), b.begin(), b.end()); }
 
 }  // namespace
 
@@ -839,7 +843,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     auto worker = [&]() {
         Builder B{ctx, n};
         for (int l = 0; l < ctx->L; l++) if (ctx->routable[l]) B.nlegal[ctx->dir[l]]++;
-        BuiltNet bn;
         for (;;) {
             int64_t c = next.fetch_add(1);
             if (c >= nchunks) break;
@@ -848,20 +851,13 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             ch.sink_off.assign(1, 0);
             ch.fp_off.assign(1, 0);
             for (int64_t net = ch.beg; net < ch.end; net++) {
-                std::string err = B.build(net, bn);
+                BuiltNet &a = ch.acc;                        // the net's tree is appended to the chunk
+                std::string err = B.build(net, a);
                 if (!err.empty()) { ch.err = err; ch.err_net = net; break; }
-                BuiltNet &a = ch.acc;
-                append(a.xy, bn.xy); append(a.kid, bn.kid); append(a.len, bn.len); append(a.edir, bn.edir);
-                append(a.nkid, bn.nkid); append(a.nl, bn.nl); append(a.nh, bn.nh); append(a.sink0, bn.sink0);
-                append(a.nsink, bn.nsink); append(a.wd, bn.wd); append(a.ur, bn.ur); append(a.height, bn.height);
-                append(a.p_layer, bn.p_layer); append(a.p_cap, bn.p_cap); append(a.p_w, bn.p_w);
-                append(a.p_orig, bn.p_orig); append(a.fp, bn.fp);
                 ch.node_off.push_back((int64_t)a.xy.size());
                 ch.sink_off.push_back((int64_t)a.p_layer.size());
                 ch.fp_off.push_back((int64_t)a.fp.size());
-                ch.wl += bn.wl;
-                ch.wsw += bn.wsw;
-                if (!bn.height.empty()) ch.max_height = std::max<int>(ch.max_height, bn.height.back());
+                ch.max_height = std::max<int>(ch.max_height, B.last_height);
             }
         }
     };
@@ -1170,7 +1166,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (NN >= ((int64_t)1 << 31) || NS >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "forest too large");
     int64_t wl = 0, wsw = 0;
     int maxh = 0;
-    for (auto &ch : chunks) { wl += ch.wl; wsw += ch.wsw; maxh = std::max(maxh, ch.max_height); }
+    for (auto &ch : chunks) { wl += ch.acc.wl; wsw += ch.acc.wsw; maxh = std::max(maxh, ch.max_height); }
     chunks.clear();
     chunks.shrink_to_fit();
 
@@ -1204,10 +1200,12 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("forest upload");
     // persistent k_assign grid, tickets, dataflow counters, big-net slots
     {
-        int per_sm = 0, n_sm = 0;
-        CK(assign_resident_ctas(ctx->L, ctx->LD, ctx->NS, ctx->NP, &per_sm, &n_sm));
-        if (per_sm < 1) return set_err(LA_ECUDA, "k_assign does not fit on an SM");
+        int per_sm = 0, per_sm_thr = 0, n_sm = 0;
+        CK(assign_resident_ctas(ctx->L, ctx->LD, ctx->NS, ctx->NP, &per_sm, &per_sm_thr, &n_sm));
+        if (per_sm < 1 || per_sm_thr < 1) return set_err(LA_ECUDA, "k_assign does not fit on an SM");
         ctx->grid = per_sm * n_sm;
+        ctx->grid_thr = per_sm_thr * n_sm;
+        if (const char *e = getenv("GAPLA_ASSIGN_VARIANT")) ctx->assign_variant = atoi(e) != 0 ? 1 : 0;
         CK(dmalloc(&ctx->d_ticket, sizeof(unsigned long long) * 2 * (nb + 1)));
         CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
         ctx->h_big_pos = big_pos;
@@ -1232,7 +1230,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->gslot_bytes = 0;
         if (max_big_nodes > 0 && need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP)) {
             ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
-            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->grid * 2));   // per half-CTA
+            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * std::max(ctx->grid, ctx->grid_thr) * 2));   // per half-CTA
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
@@ -1291,22 +1289,27 @@ static RankShare rank_share(const la_ctx *ctx, int32_t batch) {
     return r;
 }
 
-// Grid of one launch: the big-role CTAs it needs, then the small-role CTAs.
-static int launch_grid(const la_ctx *ctx, AssignLaunch &al) {
+// Grid of one launch: the big-role CTAs it needs, then the small-role CTAs.  *thr selects the
+// kernel variant: a launch of many nets per resident warp runs the 7-CTA/SM build, one bound by
+// its slowest net (and every dataflow launch) the 6-CTA/SM build.
+static int launch_grid(const la_ctx *ctx, AssignLaunch &al, bool *thr) {
     const int64_t nbig = al.big_end - al.big_beg, nsmall = al.small_end - al.small_beg;
-    // big nets by half-CTAs when the launch is throughput-bound (several nets per resident
-    // warp), by whole CTAs (lower latency per big net) when it is bound by its slowest net
-    al.big_split = ctx->big_split >= 0 ? ctx->big_split
-                                       : (nbig + nsmall > (int64_t)4 * ctx->grid * ASSIGN_WARPS ? 1 : 0);
+    const bool busy = nbig + nsmall > (int64_t)4 * ctx->grid * ASSIGN_WARPS;
+    // big nets by half-CTAs when the launch is throughput-bound, by whole CTAs (lower latency
+    // per big net) when it is bound by its slowest net
+    al.big_split = ctx->big_split >= 0 ? ctx->big_split : (busy ? 1 : 0);
+    const bool wide = nbig + nsmall > (int64_t)12 * ctx->grid * ASSIGN_WARPS;   // measured crossover
+    *thr = !al.wait && (ctx->assign_variant >= 0 ? ctx->assign_variant == 1 : wide);
+    const int gmax = *thr ? ctx->grid_thr : ctx->grid;
     const int npc = assign_nets_per_cta();
     if (!al.wait && ctx->hybrid) {   // batch mode: every CTA takes the batch's big nets first
         al.hybrid = 1;
         al.n_big_ctas = 0;
-        return (int)std::min<int64_t>(ctx->grid, std::max<int64_t>(nbig, (nsmall + npc - 1) / npc));
+        return (int)std::min<int64_t>(gmax, std::max<int64_t>(nbig, (nsmall + npc - 1) / npc));
     }
     al.hybrid = 0;
     al.n_big_ctas = (int32_t)std::min<int64_t>(ctx->n_big_ctas, nbig);
-    const int64_t small_ctas = std::min<int64_t>(ctx->grid - ctx->n_big_ctas, (nsmall + npc - 1) / npc);
+    const int64_t small_ctas = std::min<int64_t>(gmax - ctx->n_big_ctas, (nsmall + npc - 1) / npc);
     return al.n_big_ctas + (int)small_ctas;
 }
 
@@ -1337,9 +1340,10 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     const RankShare r = rank_share(ctx, batch);
     al.big_beg = r.big_beg; al.big_end = r.big_end; al.small_beg = r.small_beg; al.small_end = r.small_end;
     al.ticket = ctx->d_ticket + 2 * (1 + batch);
-    const int grid = launch_grid(ctx, al);
+    bool thr = false;
+    const int grid = launch_grid(ctx, al, &thr);
     int pi = prof_begin(ctx, K_ASSIGN);
-    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
+    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, thr, ctx->stream));
     prof_end(ctx, pi);
     if (grid > 0) ctx->stats.launches += 1;
     ctx->pending_commit = true;
@@ -1508,9 +1512,10 @@ la_status la_assign_all(la_ctx *ctx) {
         al.wait = ctx->d_wait;
         al.succ_off = ctx->d_succ_off;
         al.succ = ctx->d_succ;
-        const int grid = launch_grid(ctx, al);
+        bool thr = false;
+        const int grid = launch_grid(ctx, al, &thr);
         int pi = prof_begin(ctx, K_ASSIGN);
-        CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, ctx->stream));
+        CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, thr, ctx->stream));
         prof_end(ctx, pi);
         if (grid > 0) ctx->stats.launches += 1;
         ctx->flow_dirty = true;

@@ -77,10 +77,13 @@ struct DevForest {
 // its warp's slot; a larger ("big") net is run by a whole CTA.
 constexpr int NS_DEFAULT = 28;              // replaced at load time by the SLOT_BYTES fit
 constexpr int NP_DEFAULT = 48;
-constexpr int SLOT_BYTES = 4096;            // shared memory per warp's net slot (4 warps per CTA, 7 CTAs per SM)
+constexpr int SLOT_BYTES = 4096;            // shared memory per warp's net slot (4 warps per CTA, 6-7 CTAs per SM)
 constexpr int ASSIGN_WARPS = 4;
-#ifndef ASSIGN_MIN_CTAS
-#define ASSIGN_MIN_CTAS 7                   // k_assign CTAs per SM the register budget targets
+#ifndef ASSIGN_CTAS_LAT
+#define ASSIGN_CTAS_LAT 6                   // k_assign CTAs per SM, latency-bound launches (80 registers)
+#endif
+#ifndef ASSIGN_CTAS_THR
+#define ASSIGN_CTAS_THR 7                   // k_assign CTAs per SM, throughput-bound launches (72 registers)
 #endif
 
 struct DevScratch {
@@ -122,9 +125,9 @@ size_t assign_smem_bytes(int L, int LD, int NS, int NP);
 size_t assign_net_bytes(int nodes, int sinks, int L, int LD);
 int assign_nets_per_cta();
 size_t assign_cta_net_bytes(int L, int LD, int NS, int NP);   // shared memory a big net may use
-cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm, int *n_sm);
+cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm_lat, int *per_sm_thr, int *n_sm);
 cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
-                          cudaStream_t s);
+                          bool throughput, cudaStream_t s);
 cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t node_beg,
                           int64_t node_end, cudaStream_t s);
 cudaError_t launch_pack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);

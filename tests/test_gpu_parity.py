@@ -418,3 +418,14 @@ def test_priority_key_shapes(la, kind):
         d.order_key = rng.integers(-(1 << 62), 1 << 62, d.n_nets).astype(np.int64)
         d.order_key[:4] = [np.iinfo(np.int64).min, np.iinfo(np.int64).max, 0, 0]
     assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
+
+
+@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_assign_variants_bitwise(la, cfg, variant, monkeypatch):
+    """k_assign is built at two register budgets (6 CTAs/SM for latency-bound launches, 7 for
+    throughput-bound ones, chosen per launch); forcing either one on every launch must give the
+    oracle's solution bit for bit."""
+    monkeypatch.setenv("GAPLA_ASSIGN_VARIANT", variant)
+    d = synth.make_config(cfg)
+    assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)

@@ -23,7 +23,7 @@ for r in csv.DictReader(lines):
 per = defaultdict(lambda: defaultdict(float))
 launches = defaultdict(set)
 for r in rows:
-    k = r["Kernel Name"].split("(")[0].split("::")[-1]
+    k = r["Kernel Name"].split("(")[0].split("::")[-1].split("<")[0]   # k_assign<6> / <7>: one kernel
     launches[k].add(r["ID"])
     unit = r.get("Metric Unit", "")
     v = float(r["Metric Value"].replace(",", ""))
