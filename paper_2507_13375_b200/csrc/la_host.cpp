@@ -1116,80 +1116,105 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     ctx->n_nodes = NN;
     ctx->n_sinks = NS;
     phase("offsets");
-    // host staging in device layout
-    hvec<uint32_t> xy(NN);
-    hvec<int32_t> kid(NN * 4), len(NN), sink0(NN);
-    hvec<uint8_t> edir(NN), nkid(NN), nl(NN), nh(NN), pdrv(N);
-    hvec<uint16_t> nsink(NN), height(NN);
-    hvec<double> wd(NN), ur(NN);
-    hvec<uint8_t> p_layer(NS);
-    hvec<double> p_cap(NS), p_w(NS);
-    hvec<int64_t> p_orig(NS);
-    std::vector<int64_t> net_id(N);
-    {
-        std::atomic<int64_t> nx{0};
-        auto lay = [&]() {
-            const int64_t step = 2048;
-            for (;;) {
-                int64_t a = nx.fetch_add(step);
-                if (a >= N) break;
-                for (int64_t p = a; p < std::min(N, a + step); p++) {
-                    int64_t net = pos_net[p];
-                    const Chunk &ch = chunks[chunk_of[net]];
-                    const BuiltNet &A = ch.acc;
-                    int64_t i = net - ch.beg;
-                    int64_t s0 = ch.node_off[i], s1 = ch.node_off[i + 1];
-                    int64_t q0 = ch.sink_off[i];
-                    int64_t d0 = node0[p], e0 = sink0g[p];
-                    net_id[p] = net;
-                    pdrv[p] = n->pin_layer[n->pin_ptr[net]];
-                    for (int64_t k = s0; k < s1; k++) {
-                        int64_t d = d0 + (k - s0);
-                        xy[d] = A.xy[k];
-                        for (int j = 0; j < 4; j++) kid[d * 4 + j] = A.kid[k * 4 + j] < 0 ? -1 : (int32_t)(d0 + A.kid[k * 4 + j]);
-                        len[d] = A.len[k]; edir[d] = A.edir[k]; nkid[d] = A.nkid[k]; nl[d] = A.nl[k]; nh[d] = A.nh[k];
-                        sink0[d] = (int32_t)(e0 + A.sink0[k]);
-                        nsink[d] = A.nsink[k]; wd[d] = A.wd[k]; ur[d] = A.ur[k]; height[d] = A.height[k];
-                    }
-                    for (int64_t q = q0; q < ch.sink_off[i + 1]; q++) {
-                        int64_t d = e0 + (q - q0);
-                        p_layer[d] = A.p_layer[q]; p_cap[d] = A.p_cap[q]; p_w[d] = A.p_w[q]; p_orig[d] = A.p_orig[q];
-                    }
-                }
-            }
-        };
-        std::vector<std::thread> th;
-        for (unsigned i = 1; i < nthr; i++) th.emplace_back(lay);
-        lay();
-        for (auto &t : th) t.join();
-    }
     if (NN >= ((int64_t)1 << 31) || NS >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "forest too large");
+    // ---- upload the trees as built (chunk by chunk, input order); k_permute_forest lays them out
+    // batch-major on the GPU (rebasing child ids and sink offsets) -- no host staging pass
+    std::vector<int64_t> cnode(nchunks + 1, 0), csink(nchunks + 1, 0);
+    for (int64_t c = 0; c < nchunks; c++) {
+        cnode[c + 1] = cnode[c] + (int64_t)chunks[c].acc.xy.size();
+        csink[c + 1] = csink[c] + (int64_t)chunks[c].acc.p_layer.size();
+    }
+    if (cnode[nchunks] != NN || csink[nchunks] != NS) return set_err(LA_EINVAL, "internal: forest size mismatch");
+    hvec<int64_t> src_node0(N), src_sink0(N);
+    hvec<uint8_t> pdrv(N);
+    std::vector<int64_t> net_id(N);
+    par_for(N, nthr, [&](int64_t p) {
+        const int64_t net = pos_net[p];
+        const int32_t c = chunk_of[net];
+        const Chunk &ch = chunks[c];
+        const int64_t i = net - ch.beg;
+        src_node0[p] = cnode[c] + ch.node_off[i];
+        src_sink0[p] = csink[c] + ch.sink_off[i];
+        net_id[p] = net;
+        pdrv[p] = n->pin_layer[n->pin_ptr[net]];
+    });
     int64_t wl = 0, wsw = 0;
     int maxh = 0;
     for (auto &ch : chunks) { wl += ch.acc.wl; wsw += ch.acc.wsw; maxh = std::max(maxh, ch.max_height); }
+    phase("forest source offsets");
+
+    ForestSrc src{};
+    std::vector<void *> raw;                                // input-order device copies, freed below
+    auto raw_up = [&](auto member, const std::vector<int64_t> &base, int per, auto **dst) -> cudaError_t {
+        using T = typename std::remove_reference<decltype(chunks[0].acc.*member)>::type::value_type;
+        T *d = nullptr;
+        cudaError_t e = dmalloc(&d, sizeof(T) * std::max<int64_t>(base[nchunks] * per, 1));
+        if (e != cudaSuccess) return e;
+        raw.push_back(d);
+        for (int64_t c = 0; c < nchunks; c++) {
+            const auto &v = chunks[c].acc.*member;
+            if (v.empty()) continue;
+            e = cudaMemcpyAsync(d + base[c] * per, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx->stream);
+            if (e != cudaSuccess) return e;
+            ctx->stats.h2d_bytes += (int64_t)(sizeof(T) * v.size());
+        }
+        *dst = d;
+        return cudaSuccess;
+    };
+    CK(raw_up(&BuiltNet::xy, cnode, 1, &src.xy)); CK(raw_up(&BuiltNet::kid, cnode, 4, &src.kid));
+    CK(raw_up(&BuiltNet::len, cnode, 1, &src.len)); CK(raw_up(&BuiltNet::sink0, cnode, 1, &src.sink0));
+    CK(raw_up(&BuiltNet::edir, cnode, 1, &src.edir)); CK(raw_up(&BuiltNet::nkid, cnode, 1, &src.nkid));
+    CK(raw_up(&BuiltNet::nl, cnode, 1, &src.nl)); CK(raw_up(&BuiltNet::nh, cnode, 1, &src.nh));
+    CK(raw_up(&BuiltNet::nsink, cnode, 1, &src.nsink)); CK(raw_up(&BuiltNet::height, cnode, 1, &src.height));
+    CK(raw_up(&BuiltNet::wd, cnode, 1, &src.wd)); CK(raw_up(&BuiltNet::ur, cnode, 1, &src.ur));
+    CK(raw_up(&BuiltNet::p_layer, csink, 1, &src.p_layer)); CK(raw_up(&BuiltNet::p_cap, csink, 1, &src.p_cap));
+    CK(raw_up(&BuiltNet::p_w, csink, 1, &src.p_w)); CK(raw_up(&BuiltNet::p_orig, csink, 1, &src.p_orig));
+    int64_t *d_srcn = nullptr, *d_srcs = nullptr, *d_dsts = nullptr;
+    CK(dmalloc(&d_srcn, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcn);
+    CK(dmalloc(&d_srcs, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcs);
+    CK(dmalloc(&d_dsts, sizeof(int64_t) * (N + 1))); raw.push_back(d_dsts);
+    if (N) {
+        CK(cudaMemcpyAsync(d_srcn, src_node0.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(d_srcs, src_sink0.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(d_dsts, sink0g.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->stats.h2d_bytes += 8 * (3 * N + 1);
+    src.src_node0 = d_srcn; src.src_sink0 = d_srcs; src.dst_sink0 = d_dsts;
     chunks.clear();
     chunks.shrink_to_fit();
+    phase("forest upload (as built)");
 
-
-    phase("forest staging");
-    // ---- upload forest, allocate scratch
     DevForest &F = ctx->F;
     F.n_nets = N; F.n_nodes = NN; F.n_sinks = NS;
     uint32_t *d_xy; int32_t *d_kid, *d_len, *d_sink0; uint8_t *d_edir, *d_nkid, *d_nl, *d_nh, *d_pl, *d_pdrv;
     uint16_t *d_nsink, *d_height; double *d_wd, *d_ur, *d_pc, *d_pw; int64_t *d_po, *d_node0, *d_netid;
-    TRY(dev_upload(ctx, &d_xy, xy.data(), NN)); TRY(dev_upload(ctx, &d_kid, kid.data(), NN * 4));
-    TRY(dev_upload(ctx, &d_len, len.data(), NN)); TRY(dev_upload(ctx, &d_sink0, sink0.data(), NN));
-    TRY(dev_upload(ctx, &d_edir, edir.data(), NN)); TRY(dev_upload(ctx, &d_nkid, nkid.data(), NN));
-    TRY(dev_upload(ctx, &d_nl, nl.data(), NN)); TRY(dev_upload(ctx, &d_nh, nh.data(), NN));
-    TRY(dev_upload(ctx, &d_nsink, nsink.data(), NN)); TRY(dev_upload(ctx, &d_wd, wd.data(), NN));
-    TRY(dev_upload(ctx, &d_height, height.data(), NN));
-    TRY(dev_upload(ctx, &d_ur, ur.data(), NN)); TRY(dev_upload(ctx, &d_pl, p_layer.data(), NS));
-    TRY(dev_upload(ctx, &d_pc, p_cap.data(), NS)); TRY(dev_upload(ctx, &d_pw, p_w.data(), NS));
-    TRY(dev_upload(ctx, &d_po, p_orig.data(), NS)); TRY(dev_upload(ctx, &d_node0, node0.data(), N + 1));
+    TRY(dev_alloc(ctx, &d_xy, NN)); TRY(dev_alloc(ctx, &d_kid, NN * 4));
+    TRY(dev_alloc(ctx, &d_len, NN)); TRY(dev_alloc(ctx, &d_sink0, NN));
+    TRY(dev_alloc(ctx, &d_edir, NN)); TRY(dev_alloc(ctx, &d_nkid, NN));
+    TRY(dev_alloc(ctx, &d_nl, NN)); TRY(dev_alloc(ctx, &d_nh, NN));
+    TRY(dev_alloc(ctx, &d_nsink, NN)); TRY(dev_alloc(ctx, &d_wd, NN));
+    TRY(dev_alloc(ctx, &d_height, NN));
+    TRY(dev_alloc(ctx, &d_ur, NN)); TRY(dev_alloc(ctx, &d_pl, NS));
+    TRY(dev_alloc(ctx, &d_pc, NS)); TRY(dev_alloc(ctx, &d_pw, NS));
+    TRY(dev_alloc(ctx, &d_po, NS)); TRY(dev_upload(ctx, &d_node0, node0.data(), N + 1));
     TRY(dev_upload(ctx, &d_netid, net_id.data(), N)); TRY(dev_upload(ctx, &d_pdrv, pdrv.data(), N));
     F.xy = d_xy; F.kid = d_kid; F.len = d_len; F.edir = d_edir; F.nkid = d_nkid; F.nl = d_nl; F.nh = d_nh;
     F.sink0 = d_sink0; F.nsink = d_nsink; F.wd = d_wd; F.ur = d_ur; F.p_layer = d_pl; F.p_cap = d_pc; F.p_w = d_pw;
     F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv; F.height = d_height;
+    CK(launch_permute_forest(F, src, ctx->stream));
+    ctx->stats.launches += N > 0 ? 1 : 0;
+    // the host keeps x/y, length and direction per node (batch-major) for la_get_solution
+    hvec<uint32_t> xy(NN);
+    hvec<int32_t> len(NN);
+    hvec<uint8_t> edir(NN);
+    if (NN) {
+        CK(cudaMemcpyAsync(xy.data(), d_xy, sizeof(uint32_t) * NN, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(len.data(), d_len, sizeof(int32_t) * NN, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(edir.data(), d_edir, NN, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    ctx->stats.d2h_bytes += 9 * NN;
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (void *q : raw) dfree(q);
     DevScratch &S = ctx->S;
     TRY(dev_alloc(ctx, &S.froot, N));
     TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
@@ -1197,7 +1222,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
     TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
     if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
-    phase("forest upload");
+    phase("scratch alloc");
     // persistent k_assign grid, tickets, dataflow counters, big-net slots
     {
         int per_sm = 0, per_sm_thr = 0, n_sm = 0;

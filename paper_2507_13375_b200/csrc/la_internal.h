@@ -72,6 +72,18 @@ struct DevForest {
     const uint8_t *net_pdrv;                  // driver pin layer
 };
 
+// The trees as built (input-order chunks, net-local child ids and sink offsets), indexed by the
+// batch-major position p through src_node0 / src_sink0; dst_sink0 = first sink of position p.
+struct ForestSrc {
+    const uint32_t *xy;
+    const int32_t *kid, *len, *sink0;
+    const uint8_t *edir, *nkid, *nl, *nh, *p_layer;
+    const uint16_t *nsink, *height;
+    const double *wd, *ur, *p_cap, *p_w;
+    const int64_t *p_orig;
+    const int64_t *src_node0, *src_sink0, *dst_sink0;   // [n_nets] / [n_nets] / [n_nets + 1]
+};
+
 // Default capacities of k_assign's shared-memory net slot: a net whose LA tree has
 // at most NS nodes and at most NP sinks is "small" and keeps all its DP state in
 // its warp's slot; a larger ("big") net is run by a whole CTA.
@@ -128,6 +140,7 @@ size_t assign_cta_net_bytes(int L, int LD, int NS, int NP);   // shared memory a
 cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm_lat, int *per_sm_thr, int *n_sm);
 cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           bool throughput, cudaStream_t s);
+cudaError_t launch_permute_forest(const DevForest &F, const ForestSrc &src, cudaStream_t s);
 cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t node_beg,
                           int64_t node_end, cudaStream_t s);
 cudaError_t launch_pack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);

@@ -219,6 +219,46 @@ __global__ void __launch_bounds__(ELMORE_THREADS) k_elmore(DevGrid G, DevForest 
 #undef TK
 }
 
+// ------------------------------------------------------------ forest layout --
+// la_load_nets uploads the trees as the host threads built them (input-order chunks, net-local
+// child ids and sink offsets) and this kernel lays them out batch-major: a warp per net, lanes
+// over its nodes and sinks.  src holds the built arrays, F the destination (its pointers are
+// const for the kernels that read it; they were allocated here, so the casts are sound).
+__global__ void k_permute_forest(DevForest F, ForestSrc src, int64_t n_nets) {
+    const int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (p >= n_nets) return;
+    const int64_t d0 = F.net_node0[p], nn = F.net_node0[p + 1] - d0;
+    const int64_t e0 = src.dst_sink0[p], ns = src.dst_sink0[p + 1] - e0;
+    const int64_t s0 = src.src_node0[p], q0 = src.src_sink0[p];
+    for (int64_t j = lane; j < nn; j += 32) {
+        const int64_t d = d0 + j, s = s0 + j;
+        const_cast<uint32_t *>(F.xy)[d] = src.xy[s];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t c = src.kid[s * 4 + k];
+            const_cast<int32_t *>(F.kid)[d * 4 + k] = c < 0 ? -1 : (int32_t)(d0 + c);
+        }
+        const_cast<int32_t *>(F.len)[d] = src.len[s];
+        const_cast<uint8_t *>(F.edir)[d] = src.edir[s];
+        const_cast<uint8_t *>(F.nkid)[d] = src.nkid[s];
+        const_cast<uint8_t *>(F.nl)[d] = src.nl[s];
+        const_cast<uint8_t *>(F.nh)[d] = src.nh[s];
+        const_cast<int32_t *>(F.sink0)[d] = (int32_t)(e0 + src.sink0[s]);
+        const_cast<uint16_t *>(F.nsink)[d] = src.nsink[s];
+        const_cast<double *>(F.wd)[d] = src.wd[s];
+        const_cast<double *>(F.ur)[d] = src.ur[s];
+        const_cast<uint16_t *>(F.height)[d] = src.height[s];
+    }
+    for (int64_t j = lane; j < ns; j += 32) {
+        const int64_t d = e0 + j, q = q0 + j;
+        const_cast<uint8_t *>(F.p_layer)[d] = src.p_layer[q];
+        const_cast<double *>(F.p_cap)[d] = src.p_cap[q];
+        const_cast<double *>(F.p_w)[d] = src.p_w[q];
+        const_cast<int64_t *>(F.p_orig)[d] = src.p_orig[q];
+    }
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -260,6 +300,12 @@ cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64
     int64_t n = node_end - node_beg;
     if (n <= 0) return cudaSuccess;
     k_unpack_dec<<<nblk(n, 256), 256, 0, s>>>(S, node_beg, node_end);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute_forest(const DevForest &F, const ForestSrc &src, cudaStream_t s) {
+    if (F.n_nets <= 0) return cudaSuccess;
+    k_permute_forest<<<nblk(F.n_nets * 32, 256), 256, 0, s>>>(F, src, F.n_nets);
     return cudaGetLastError();
 }
 
