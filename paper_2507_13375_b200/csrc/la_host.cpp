@@ -119,6 +119,7 @@ struct la_ctx {
     int32_t grid = 0;                         // resident k_assign CTAs (persistent grid), latency variant
     int32_t grid_thr = 0;                     // the same, throughput variant (more CTAs per SM)
     int32_t assign_variant = -1;              // -1: per launch; GAPLA_ASSIGN_VARIANT=0 latency / 1 throughput
+    int32_t thr_nets_per_warp = 12;           // throughput variant above this many nets per resident warp
     int32_t schedule = -1;                    // -1: automatic (la_assign_all); else LA_SCHED_*
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
@@ -1231,6 +1232,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->grid = per_sm * n_sm;
         ctx->grid_thr = per_sm_thr * n_sm;
         if (const char *e = getenv("GAPLA_ASSIGN_VARIANT")) ctx->assign_variant = atoi(e) != 0 ? 1 : 0;
+        if (const char *e = getenv("GAPLA_THR_NETS_PER_WARP")) ctx->thr_nets_per_warp = std::max(1, atoi(e));
         CK(dmalloc(&ctx->d_ticket, sizeof(unsigned long long) * 2 * (nb + 1)));
         CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
         ctx->h_big_pos = big_pos;
@@ -1323,7 +1325,7 @@ static int launch_grid(const la_ctx *ctx, AssignLaunch &al, bool *thr) {
     // big nets by half-CTAs when the launch is throughput-bound, by whole CTAs (lower latency
     // per big net) when it is bound by its slowest net
     al.big_split = ctx->big_split >= 0 ? ctx->big_split : (busy ? 1 : 0);
-    const bool wide = nbig + nsmall > (int64_t)12 * ctx->grid * ASSIGN_WARPS;   // measured crossover
+    const bool wide = nbig + nsmall > (int64_t)ctx->thr_nets_per_warp * ctx->grid * ASSIGN_WARPS;   // DESIGN §5 v11
     *thr = !al.wait && (ctx->assign_variant >= 0 ? ctx->assign_variant == 1 : wide);
     const int gmax = *thr ? ctx->grid_thr : ctx->grid;
     const int npc = assign_nets_per_cta();
