@@ -1,0 +1,102 @@
+"""Small hot-path runs for compute-sanitizer (memcheck / racecheck / synccheck), SURVEY §4 T5.
+
+Each scenario runs the library through the C ABI on a design small enough for the sanitizer's
+instrumentation, and checks the result against the CPU oracle (so a run that "passes" the
+sanitizer but computes garbage is still caught).  Scenarios cover both schedules, both
+register variants of k_assign, the big-net (half-CTA / whole-CTA / global-slot) paths, the
+snapshot-batch mode and the host-transport multi-rank path.
+
+    python tools/sanitize_run.py [scenario ...]      (default: all)
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from gen import synth  # noqa: E402
+from oracle import oracle  # noqa: E402
+from paper_2507_13375_b200 import la  # noqa: E402
+
+KEYS = ("wires", "vias", "wire_dem", "via_dem", "net_cost", "sink_delay", "net_cap", "net_rc")
+
+
+def check(got, ref, what):
+    for k in KEYS:
+        if not np.array_equal(np.asarray(got[k]), np.asarray(ref[k])):
+            raise SystemExit(f"{what}: {k} differs from the oracle")
+    print(f"{what}: ok ({len(got['wires'])} wires)", flush=True)
+
+
+def run(d, schedule=None, snap=None):
+    A = la.LayerAssigner(d, device=0)
+    A.load(snapshot_batches=snap)
+    if schedule is not None:
+        A.set_schedule(schedule)
+    out = A.run()
+    A.close()
+    return out
+
+
+def sc_cfg1_batch():
+    d = synth.make_config(1)
+    check(run(d, la.LA_SCHED_BATCH), oracle.run(d), "cfg1 batch")
+
+
+def sc_cfg1_flow():
+    d = synth.make_config(1)
+    check(run(d, la.LA_SCHED_DATAFLOW), oracle.run(d), "cfg1 dataflow")
+
+
+def sc_cfg2_small():
+    d = synth.make_config(2, n_nets=6000)
+    check(run(d, la.LA_SCHED_BATCH), oracle.run(d), "cfg2[6000] batch")
+
+
+def sc_bignets():
+    # config 4's high-fanout mix (64-256 pins): big nets on half-CTAs / whole CTAs / global slots
+    d = synth.make_config(4, n_nets=4000)
+    check(run(d, la.LA_SCHED_BATCH), oracle.run(d), "cfg4[4000] batch (big nets)")
+    check(run(d, la.LA_SCHED_DATAFLOW), oracle.run(d), "cfg4[4000] dataflow (big nets)")
+
+
+def sc_snapshot():
+    d = synth.make_config(1)
+    sb = np.random.default_rng(3).integers(0, 8, d.n_nets).astype(np.int32)
+    check(run(d, snap=sb), oracle.run(d, snap_batch=sb), "cfg1 snapshot batches")
+
+
+def sc_host_transport():
+    d = synth.make_config(1)
+    world = 2
+    ranks = [la.LayerAssigner(d, device=0, rank=r, world=world) for r in range(world)]
+    nb = [A.load() for A in ranks][0]
+    for k in range(nb):
+        for A in ranks:
+            A.assign_batch(k)
+        parts = [la.la_get_decisions(A.ctx, k) for A in ranks]
+        dec = np.sum([p[0] for p in parts], axis=0, dtype=np.uint64).astype(np.uint32)
+        cost = np.sum([p[1] for p in parts], axis=0)
+        for A in ranks:
+            la.la_put_decisions(A.ctx, k, dec, cost)
+            A.commit_demand(k)
+    ref = oracle.run(d)
+    for A in ranks:
+        out = A.eval_timing()
+        out.update(A.solution())
+        wd, vd = A.demand()
+        out.update(wire_dem=wd, via_dem=vd)
+        check(out, ref, f"cfg1 host transport rank {A.grid_desc.rank}")
+        A.close()
+
+
+SCENARIOS = {k[3:]: v for k, v in globals().items() if k.startswith("sc_")}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(SCENARIOS)
+    for n in names:
+        SCENARIOS[n]()
