@@ -327,6 +327,7 @@ struct NetState {
     std::vector<double> wd;        // W_D * w_n (Eq. 5) per node
     std::vector<double> ur;        // O3
     std::vector<double> f, dlc;    // [node][L]
+    std::vector<double> gp;        // [node][L] G' of the chosen span (Alg. 3 l.404 key; exposed for the pins)
     std::vector<int> cb, ct;       // choice (b, t) per [node][L]
     std::vector<int> entry;        // [node][L][4]
     std::vector<int> lay, sb, st;  // backtracked entry layer, span
@@ -452,6 +453,7 @@ void node_dp(const Ctx &C, const ONets *N, int64_t drv, const Tree &T, NetState 
             }
         }
         if (!have) continue;
+        st.gp[nlidx] = bGp;
         st.f[nlidx] = F0 + bG;          // Alg. 3 l.405
         st.dlc[nlidx] = C0 + bK;
         st.cb[nlidx] = bb;
@@ -460,6 +462,40 @@ void node_dp(const Ctx &C, const ONets *N, int64_t drv, const Tree &T, NetState 
     }
 }
 
+
+// O2 weights and O3 upstream resistance of one net (PAPER §III-C l.316-318, §III-D l.452).
+//   wd_n = W_D * max of w_q over sinks q in subtree(n) (Eq. 5, reading R3), 0 if none (R39)
+//   ur(root) = r_drv; ur(n) = ur(parent) + r_avg * len_n, len_n = n's own parent-edge length (R6)
+void net_weights_ur(const Ctx &C, const ONets *nets, int64_t net, int64_t drv, const Tree &T, NetState &st) {
+    const OGrid *g = C.g;
+    const size_t nn = T.x.size();
+    st.wd.assign(nn, 0.0);
+    st.ur.assign(nn, 0.0);
+    std::vector<double> w(nn, 0.0);
+    for (auto it = T.pre.rbegin(); it != T.pre.rend(); ++it) {
+        int n = *it;
+        double m = 0.0;
+        for (int64_t q : T.pins[n]) if (q != drv) m = std::max(m, pin_weight(g, nets->pin_slack[q], nets->wns));
+        for (int k : T.kids[n]) m = std::max(m, w[k]);
+        w[n] = m;
+    }
+    for (size_t n = 0; n < nn; n++) st.wd[n] = g->W_D * w[n];
+    for (int n : T.pre)
+        st.ur[n] = (T.par[n] < 0) ? (nets->r_drv ? nets->r_drv[net] : 0.0) : st.ur[T.par[n]] + C.r_avg * T.len[n];
+}
+
+// O6 over one net (children before parents): allocates and fills st.f/dlc/gp/cb/ct/entry.
+void net_dp(const Ctx &C, const ONets *nets, int64_t drv, const Tree &T, NetState &st) {
+    const size_t nn = T.x.size();
+    const int L = C.L;
+    st.f.assign(nn * L, INF);
+    st.dlc.assign(nn * L, 0.0);
+    st.gp.assign(nn * L, INF);
+    st.cb.assign(nn * L, -1);
+    st.ct.assign(nn * L, -1);
+    st.entry.assign(nn * L * 4, -1);
+    for (auto it = T.pre.rbegin(); it != T.pre.rend(); ++it) node_dp(C, nets, drv, T, st, *it);
+}
 
 // Elmore O9 canonical fast form, on the backtracked solution.
 void elmore(const Ctx &C, const ONets *N, int64_t drv, const Tree &T, const NetState &st,
@@ -556,6 +592,50 @@ int oracle_tree(const OGrid *g, const ONets *nets, int64_t net, int32_t *out, in
     return 0;
 }
 
+// Internals of O2/O3/O6 for ONE net on the grid's initial demand (exposed for the look-ahead pins,
+// SURVEY §8(c) c.5 O3 and (iii)/(iv); the arithmetic is oracle_run's own, shared functions).
+// Nodes in preorder ids (as oracle_tree).  Per node: ur, wd; per (node, l): f, dlc, G' of the
+// chosen span, choice (b, t) (-1 if infeasible) and the sons' entry layers [4].
+int oracle_net_dp(const OGrid *g, const ONets *nets, int64_t net, int32_t max_nodes, int32_t *n_out, double *ur,
+                  double *wd, double *f, double *dlc, double *gp, int32_t *cb, int32_t *ct, int32_t *entry, char *err) {
+    Ctx C;
+    C.g = g; C.nets = nets; C.X = g->X; C.Y = g->Y; C.L = g->L;
+    char buf[256] = {0};
+    C.err = buf;
+    const int L = C.L;
+    C.wire_off.resize(L + 1);
+    C.wire_off[0] = 0;
+    for (int l = 0; l < L; l++)
+        C.wire_off[l + 1] = C.wire_off[l] + (g->dir[l] == 0 ? (int64_t)(C.X - 1) * C.Y : (int64_t)C.X * (C.Y - 1));
+    int64_t nw = C.wire_off[L], nvia = (int64_t)(L - 1) * C.X * C.Y;
+    C.wdem.assign(nw, 0);
+    C.vdem.assign(nvia, 0);
+    if (g->wire_dem0) std::memcpy(C.wdem.data(), g->wire_dem0, 4 * nw);
+    if (g->via_dem0) std::memcpy(C.vdem.data(), g->via_dem0, 4 * nvia);
+    build_tables(C);
+    Tree T;
+    NetState st;
+    NetView nv{nets->pin_ptr[net], nets->pin_ptr[net + 1], nets->seg_ptr[net], nets->seg_ptr[net + 1]};
+    if (nv.p1 <= nv.p0) { if (err) std::snprintf(err, 256, "net %lld: no pins", (long long)net); return -1; }
+    if (!build_tree(C, net, nv, T)) { if (err) std::memcpy(err, buf, 256); return -1; }
+    const int64_t drv = nv.p0;
+    const int nn = (int)T.x.size();
+    *n_out = nn;
+    if (nn > max_nodes) { if (err) std::snprintf(err, 256, "net %lld: %d nodes > max_nodes", (long long)net, nn); return -2; }
+    net_weights_ur(C, nets, net, drv, T, st);
+    net_dp(C, nets, drv, T, st);
+    for (int n = 0; n < nn; n++) {
+        ur[n] = st.ur[n];
+        wd[n] = st.wd[n];
+        for (int l = 0; l < L; l++) {
+            size_t i = (size_t)n * L + l;
+            f[i] = st.f[i]; dlc[i] = st.dlc[i]; gp[i] = st.gp[i]; cb[i] = st.cb[i]; ct[i] = st.ct[i];
+            for (int k = 0; k < 4; k++) entry[i * 4 + k] = st.entry[i * 4 + k];
+        }
+    }
+    return 0;
+}
+
 int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     Ctx C;
     C.g = g; C.nets = nets; C.X = g->X; C.Y = g->Y; C.L = g->L;
@@ -618,31 +698,10 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
         const size_t nn = T.x.size();
         if (out->n_nodes) out->n_nodes[net] = (int32_t)nn;
 
-        // O2 weights: w_n = max of w_q over sinks in subtree(n) (Eq. 5, R3), 0 if none (R39)
-        st.wd.assign(nn, 0.0);
-        st.ur.assign(nn, 0.0);
-        {
-            std::vector<double> w(nn, 0.0);
-            for (auto it = T.pre.rbegin(); it != T.pre.rend(); ++it) {
-                int n = *it;
-                double m = 0.0;
-                for (int64_t q : T.pins[n]) if (q != drv) m = std::max(m, pin_weight(g, nets->pin_slack[q], nets->wns));
-                for (int k : T.kids[n]) m = std::max(m, w[k]);
-                w[n] = m;
-            }
-            for (size_t n = 0; n < nn; n++) st.wd[n] = g->W_D * w[n];
-            // O3: ur(root) = r_drv; ur(n) = ur(parent) + r_avg * len (R6)
-            for (int n : T.pre)
-                st.ur[n] = (T.par[n] < 0) ? (nets->r_drv ? nets->r_drv[net] : 0.0) : st.ur[T.par[n]] + C.r_avg * T.len[n];
-        }
+        net_weights_ur(C, nets, net, drv, T, st);
         auto t0 = std::chrono::steady_clock::now();
-        st.f.assign(nn * L, INF);
-        st.dlc.assign(nn * L, 0.0);
-        st.cb.assign(nn * L, -1);
-        st.ct.assign(nn * L, -1);
-        st.entry.assign(nn * L * 4, -1);
         // O6 bottom-up (children before parents)
-        for (auto it = T.pre.rbegin(); it != T.pre.rend(); ++it) node_dp(C, nets, drv, T, st, *it);
+        net_dp(C, nets, drv, T, st);
         // O7 backtrack (Alg. 4): root layer = driver pin layer (R13)
         st.lay.assign(nn, -1); st.sb.assign(nn, -1); st.st.assign(nn, -1);
         int root = T.pre[0];

@@ -68,6 +68,9 @@ def _load():
         _lib.oracle_pin_weight.restype = c_f64
         _lib.oracle_tree.argtypes = [P(OGrid), P(ONets), c_i64, P(c_i32), c_i32, P(c_i32), ctypes.c_char_p]
         _lib.oracle_tree.restype = ctypes.c_int
+        _lib.oracle_net_dp.argtypes = [P(OGrid), P(ONets), c_i64, c_i32, P(c_i32), P(c_f64), P(c_f64), P(c_f64),
+                                       P(c_f64), P(c_f64), P(c_i32), P(c_i32), P(c_i32), ctypes.c_char_p]
+        _lib.oracle_net_dp.restype = ctypes.c_int
     return _lib
 
 
@@ -194,6 +197,31 @@ def tree(d, net: int):
     if rc != 0:
         raise OracleError(err.value.decode())
     return out[: cnt.value]
+
+
+def net_dp(d, net: int) -> dict:
+    """O2/O3/O6 internals of one net on the design's initial demand (nodes in oracle_tree's
+    preorder ids): ur, wd per node; f, dlc, gp (G' of the chosen span), cb, ct [node][L];
+    entry [node][L][4] (son layers).  Exposed for the look-ahead pins."""
+    lib = _load()
+    keep = []
+    g = _grid(d, keep)
+    n = _nets(d, keep)
+    M = d.unit_edges_total() + 2
+    L = d.L
+    ur, wd = np.zeros(M, np.float64), np.zeros(M, np.float64)
+    f, dlc, gp = (np.zeros((M, L), np.float64) for _ in range(3))
+    cb, ct = np.zeros((M, L), np.int32), np.zeros((M, L), np.int32)
+    entry = np.zeros((M, L, 4), np.int32)
+    cnt = c_i32()
+    err = ctypes.create_string_buffer(256)
+    rc = lib.oracle_net_dp(ctypes.byref(g), ctypes.byref(n), net, M, ctypes.byref(cnt), _ptr(ur, c_f64),
+                           _ptr(wd, c_f64), _ptr(f, c_f64), _ptr(dlc, c_f64), _ptr(gp, c_f64), _ptr(cb, c_i32),
+                           _ptr(ct, c_i32), _ptr(entry, c_i32), err)
+    if rc != 0:
+        raise OracleError(err.value.decode())
+    k = cnt.value
+    return dict(ur=ur[:k], wd=wd[:k], f=f[:k], dlc=dlc[:k], gp=gp[:k], cb=cb[:k], ct=ct[:k], entry=entry[:k])
 
 
 def evaluate(d, wire_dem, via_dem, wires, vias) -> dict:

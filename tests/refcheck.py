@@ -310,3 +310,139 @@ def elmore_definitional(d, pins, nodes, lay, spans):
                 u = parent[u]
             delays[q] = s
     return delays, sum(cap.values()), sum(rc_term.values())
+
+
+# ---------------------------------------------------------------- look-ahead (O3) and node-local DP
+def upstream_r(d, net, nodes):
+    """O3 written from PAPER l.452 (reading R6) as a walk down from the root: ur(root) = r_drv,
+    ur(child) = ur(parent) + r_avg * (the child's own edge length).  Returns a list per node."""
+    ra = r_avg(d)
+    ur = [0.0] * len(nodes)
+    ur[0] = float(d.r_drv[net])
+    todo = [0]
+    while todo:
+        v = todo.pop()
+        for k in nodes[v]["kids"]:
+            ur[k] = ur[v] + ra * nodes[k]["len"]
+            todo.append(k)
+    return ur
+
+
+def subtree_wd(d, net, nodes):
+    """W_D x max sink weight over each node's subtree (Eq. (5), R3), 0 if none (R39)."""
+    pins = net_pins(d, net)
+    w = [0.0] * len(nodes)
+
+    def rec(v):
+        m = 0.0
+        for q in nodes[v]["pins"]:
+            if q != 0:
+                m = max(m, pin_w(d, pins[q][4]))
+        for k in nodes[v]["kids"]:
+            m = max(m, rec(k))
+        w[v] = m
+        return m
+
+    rec(0)
+    return [d.W_D * x for x in w]
+
+
+def _vr_asc(d, a, b):
+    s = 0.0
+    for k in range(min(a, b), max(a, b)):
+        s = s + d.vr[k]
+    return s
+
+
+def node_local_enumeration(d, net, nodes, dp, omap):
+    """for every node n and entry layer l with a finite oracle f,
+    enumerate EVERY tuple of son layers (each son on a legal layer where its oracle f is finite),
+    take the tuple's minimal covering via span [min(b0, js), max(t0, js)], and evaluate
+    G' = ((V + cost'_1) + cost'_2) + ... with the O5 expression order, V summed ascending from b.
+    The minimum over tuples must equal the oracle's G' (dp['gp']) bitwise (kappa >= 0 and rounded
+    addition is monotone).  Where that minimum is attained by one tuple only, the oracle's son
+    layers and span must be that tuple and its cover.  (iv): at the minimising tuple,
+    G' - G = ur_n x sum(B_i) within rounding, and the oracle's f = F0 + G bitwise.
+    ``omap[v]`` is the oracle's node id of refcheck node v.  Returns (checked, unique) counts."""
+    pins = net_pins(d, net)
+    wd_arr, vd_arr = dem_arrays(d)
+    L = d.L
+    ur = upstream_r(d, net, nodes)
+    wdv = subtree_wd(d, net, nodes)
+    checked = unique = 0
+    for v, nd in enumerate(nodes):
+        o = omap[v]
+        assert dp["ur"][o] == ur[v], ("ur", v, dp["ur"][o], ur[v])
+        assert dp["wd"][o] == wdv[v], ("wd", v)
+        root = v == 0
+        kap = []
+        for k in range(L - 1):
+            i = via_idx(d, k, nd["x"], nd["y"])
+            kap.append(d.W_VIA + (d.W_CONG * d.ofw[k]) * marginal(d, int(d.via_cap[i]), int(vd_arr[i])))
+        pl = [pins[q][2] for q in nd["pins"]]
+        sons = nd["kids"]
+        # per son: legal finite layers and the O5 terms (A, B, capb) from the son's oracle f / dlc
+        opts = []
+        for s in sons:
+            sn = nodes[s]
+            cells, _ = run_cells(sn)
+            lst = []
+            for j in legal_layers(d, sn["edir"]):
+                fs = dp["f"][omap[s]][j]
+                if not math.isfinite(fs):
+                    continue
+                Rw, Cw = d.r[j] * sn["len"], d.c[j] * sn["len"]
+                D = dp["dlc"][omap[s]][j]
+                S = 0.0
+                for (x, y) in cells:
+                    wi = wire_idx(d, j, x, y)
+                    S = S + marginal(d, int(d.wire_cap[wi]), int(wd_arr[wi]))
+                A = ((fs + wdv[s] * (Rw * (0.5 * Cw + D))) + d.W_CAP * Cw) + (d.W_CONG * d.ofw[j]) * S
+                lst.append((j, A, wdv[s] * (Cw + D), Cw + D))
+            opts.append(lst)
+        entries = [pins[0][2]] if root else legal_layers(d, nd["edir"])
+        for l in entries:
+            if not math.isfinite(dp["f"][o][l]):
+                continue
+            b0 = min([l] + pl) if pl else l
+            t0 = max([l] + pl) if pl else l
+            best, arg, cnt = math.inf, None, 0
+            for combo in itertools.product(*opts):
+                js = [c[0] for c in combo]
+                b, t = min([b0] + js), max([t0] + js)
+                V = 0.0
+                for k in range(b, t):
+                    V = V + kap[k]
+                Gp, G, Bs = V, V, 0.0
+                for (j, A, B, _) in combo:
+                    cost = A + B * _vr_asc(d, l, j)
+                    G = G + cost
+                    Gp = Gp + (cost + B * ur[v])
+                    Bs = Bs + B
+                if Gp < best:
+                    best, arg, cnt = Gp, (js, b, t, G, Bs), 1
+                elif Gp == best:
+                    cnt += 1
+            assert best == dp["gp"][o][l], ("min G'", v, l, best, dp["gp"][o][l])
+            js, b, t, G, Bs = arg
+            gap = best - G
+            assert abs(gap - ur[v] * Bs) <= 1e-12 * max(1.0, abs(best)), ("cost' - cost", v, l, gap, ur[v] * Bs)
+            checked += 1
+            if cnt == 1:
+                unique += 1
+                assert (dp["cb"][o][l], dp["ct"][o][l]) == (b, t), ("span", v, l)
+                assert [int(dp["entry"][o][l][i]) for i in range(len(sons))] == js, ("son layers", v, l)
+                F0 = 0.0
+                for q in nd["pins"]:
+                    if q == 0:
+                        continue
+                    wq = d.W_D * pin_w(d, pins[q][4]) if root else wdv[v]
+                    F0 = F0 + wq * (pins[q][3] * _vr_asc(d, pins[q][2], l))
+                assert dp["f"][o][l] == F0 + G, ("f = F0 + G", v, l)
+    return checked, unique
+
+
+def oracle_node_map(nodes, otree):
+    """refcheck node index -> oracle node id, matched by GCell (one LA node per GCell)."""
+    at = {(int(r[0]), int(r[1])): i for i, r in enumerate(otree)}
+    return [at[(nd["x"], nd["y"])] for nd in nodes]

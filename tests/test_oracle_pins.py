@@ -5,6 +5,7 @@ routine to produce an expected value: expected values are closed forms, hand
 numbers (tests/golden/), brute-force enumeration (tests/refcheck.py), an
 independent definitional Elmore, or invariants.
 """
+import copy
 import math
 
 import numpy as np
@@ -424,3 +425,129 @@ def test_paper_batches_library_equals_oracle():
         got, nb = la.la_paper_batches(d, crit, 0.7, 3, mb)
         ref, nbr = oracle.paper_batches(d.pin_ptr, d.pin_slack, d.seg_ptr, d.seg_xy, d.wns, crit, 0.7, 3, mb)
         assert nb == nbr and np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ O3 look-ahead
+def _tree_ids(d, net=0):
+    """(x, y) -> oracle node id."""
+    return {(int(r[0]), int(r[1])): i for i, r in enumerate(oracle.tree(d, net))}
+
+
+@pytest.mark.parametrize("r_avg", [0.003, float("nan")])
+def test_ur_chain_closed_form(r_avg):
+    """O3 closed form on a chain (SURVEY §8(c) c.5 'O3 ur'; PAPER l.452 'node distances and the
+    average unit-length metal resistance r_avg'; reading R6): pins along one straight run give a
+    chain root -> n1 -> n2 -> n3 with ur(n_k) = r_drv + r_avg * (distance from the driver), strictly
+    increasing.  r_avg = NaN means the mean r of the routable layers (Alg. 1 input, l.240)."""
+    d = synth.empty_design(12, 6, 6)
+    d.r_avg = r_avg
+    d.routable = np.array([1, 1, 1, 1, 0, 1], np.uint8)
+    ra = 0.003 if r_avg == r_avg else float(np.mean(d.r[[0, 1, 2, 3, 5]]))
+    d = synth.with_nets(d, [dict(pins=[(0, 2, 0, 1.0, -5.0), (2, 2, 0, 1.0, -5.0), (5, 2, 1, 1.0, -5.0),
+                                       (9, 2, 0, 1.0, -5.0)], segs=[(0, 2, 9, 2)], r_drv=1.25)])
+    ids = _tree_ids(d)
+    ur = oracle.net_dp(d, 0)["ur"]
+    got = [ur[ids[(x, 2)]] for x in (0, 2, 5, 9)]
+    want = [1.25 + ra * x for x in (0, 2, 5, 9)]
+    assert got[0] == 1.25                                        # ur(root) = r_drv exactly
+    for g_, w_ in zip(got, want):
+        assert g_ == pytest.approx(w_, rel=1e-15)
+    assert all(a < b for a, b in zip(got, got[1:]))
+
+
+def _fig8_design(case):
+    G = golden("lookahead_fig8.json")
+    t, w, n = G["tech"], G["weights"], G["net"]
+    d = synth.empty_design(8, 8, t["L"])
+    d.dir = np.array(t["dir"], np.uint8)
+    d.routable = np.array(t["routable"], np.uint8)
+    d.r, d.c, d.vr = (np.array(t[k], np.float64) for k in ("r", "c", "vr"))
+    d.r_avg = t["r_avg"]
+    for k in ("W_D", "W_CAP", "W_CONG", "W_VIA", "w_floor"):
+        setattr(d, k, w[k])
+    d = synth.with_nets(d, [dict(pins=[tuple(p) for p in n["pins"]], segs=[tuple(s) for s in n["segs"]],
+                                 r_drv=G["cases"][case]["r_drv"])])
+    d.wns = w["wns"]
+    return d, G["cases"][case]
+
+
+@pytest.mark.parametrize("case", ["r_drv_0", "r_drv_0p04"])
+def test_lookahead_fig8_hand_example(case):
+    """The paper's look-ahead example on the Fig. 8 tree (f'_6 = ... + w^d (d_67 +
+    r^est_6 c_6)), worked by hand in tests/golden/lookahead_fig8.json: ur of every node, the two
+    cost' candidates of son 7 at node 6, the full solution and the net cost.  With r_drv = 0.04 the
+    look-ahead moves edge 67 from layer 0 (plain cost) to layer 2; with r_drv = 0 it does not."""
+    d, want = _fig8_design(case)
+    ids = _tree_ids(d)
+    coord = {"3": (0, 0), "4": (2, 0), "5": (4, 0), "6": (2, 3), "7": (4, 3)}
+    dp = oracle.net_dp(d, 0)
+    for k, u in want["ur"].items():
+        assert dp["ur"][ids[coord[k]]] == pytest.approx(u, rel=1e-12, abs=1e-15), ("ur", k)
+    j = want["layers"]["67"]
+    # node 6, entry 1: G' = V(b, t) + cost'(1; 7, j*) with V = 0 (W_VIA = W_CONG = 0)
+    assert dp["gp"][ids[coord["6"]]][1] == pytest.approx(want["node6_cost_prime"][str(j)], rel=1e-12)
+    assert min(want["node6_cost_prime"].values()) == want["node6_cost_prime"][str(j)]
+    r = oracle.run(d)
+    edge = {"34": (0, 0, 2, 0), "45": (2, 0, 4, 0), "46": (2, 0, 2, 3), "67": (2, 3, 4, 3)}
+    lay = {tuple(int(v) for v in w[:4]): int(w[4]) for w in r["wires"]}
+    assert {k: lay[e] for k, e in edge.items()} == want["layers"]
+    assert sorted(tuple(int(v) for v in x) for x in r["vias"]) == sorted(tuple(x) for x in want["vias"])
+    assert r["net_cost"][0] == pytest.approx(want["net_cost"], rel=1e-12)
+
+
+@pytest.mark.parametrize("seed,L,r_avg", [(131, 4, float("nan")), (132, 6, 0.05), (133, 4, 0.2), (134, 6, 0.01)])
+def test_node_local_enumeration(seed, L, r_avg):
+    """SURVEY §8(c) c.5 (iii)/(iv) on random nets with W_D > 0 and r_drv > 0 (look-ahead live):
+    for every node and entry layer, the minimum over ALL son-layer tuples (each with its minimal
+    covering via span, tests/refcheck.py) equals the oracle's span-DP G' bitwise; the oracle's span
+    and son layers are the unique minimiser's; cost' - cost = ur_n * sum B (iv); f = F0 + G; and
+    ur / wd equal an independent top-down walk."""
+    checked = unique = 0
+    for d, nodes in _dp_cases(seed, L, rdrv_mode=1, max_nodes=8, want=40):
+        d.W_D = 100.0
+        d.r_avg = r_avg
+        omap = rc.oracle_node_map(nodes, oracle.tree(d, 0))
+        c, u = rc.node_local_enumeration(d, 0, nodes, oracle.net_dp(d, 0), omap)
+        checked += c
+        unique += u
+    assert checked > 100 and unique > checked // 2
+
+
+def test_lookahead_is_live_on_random_nets():
+    """The pins above exercise a live term: on the same random pool, switching the look-ahead
+    off (r_drv = r_avg = 0, the Table IV 'w/o ahead' ablation) changes the
+    chosen layers of some nets."""
+    changed = 0
+    for d, nodes in _dp_cases(133, 4, rdrv_mode=1, max_nodes=8, want=150):
+        d.W_D, d.r_avg = 1000.0, 0.2
+        a = oracle.run(d)
+        e = copy.copy(d)
+        e.r_avg = 0.0
+        e.r_drv = np.zeros_like(d.r_drv)
+        b = oracle.run(e)
+        changed += int(not np.array_equal(a["wires"], b["wires"]))
+    assert changed >= 3
+
+
+def test_eq3_clamp_outside_table_domain():
+    """Reading R20: d - c outside [delta_lo, delta_hi] clamps to the nearest end of the table.
+    Straight 2-pin net on layer 0 only (other H layers unroutable), W_D = W_CAP = W_VIA = 0:
+    the cost is ofw[0] * sum of M_pos over the run's edges, by hand, with d - c = 10 > delta_hi = 2
+    on the first edge and -8 < delta_lo = -3 on the second."""
+    d = synth.empty_design(8, 8, 4, cap_wire=5, cap_via=16)
+    d.delta_lo, d.delta_hi = -3, 2
+    d.routable = np.array([1, 1, 0, 1], np.uint8)
+    d.W_D = d.W_CAP = d.W_VIA = 0.0
+    d = synth.with_nets(d, [dict(pins=[(1, 4, 0, 1.0, -5.0), (3, 4, 0, 1.0, -5.0)], segs=[(1, 4, 3, 4)])])
+    d.wire_dem0 = np.zeros(d.wire_cap.shape[0], np.int32)
+    d.wire_dem0[4 * (d.X - 1) + 1] = 15        # layer 0 edge (1,4)-(2,4): d - c = 10 -> clamp to 2
+    d.wire_dem0[4 * (d.X - 1) + 2] = 0         # layer 0 edge (2,4)-(3,4): d - c = -5 -> clamp to -3
+    d.wire_cap = d.wire_cap.copy()
+    d.wire_cap[4 * (d.X - 1) + 2] = 8          # ... make it -8
+    M = lambda dl: math.exp(0.5 * (dl + 1)) - math.exp(0.5 * dl)
+    # via cuts: the pins sit on layer 0 = the wire layer, so no vias; V = 0
+    want = 2.0 * (M(2) + M(-3))                # ofw[0] = 2 (generator tech, d.2)
+    r = oracle.run(d)
+    assert int(r["wires"][0][4]) == 0 and len(r["vias"]) == 0
+    assert r["net_cost"][0] == pytest.approx(want, rel=1e-14)
+    assert r["net_cost"][0] != pytest.approx(2.0 * (M(10) + M(-8)), rel=1e-6)
