@@ -160,7 +160,8 @@ typedef struct {
  * default stream-ordered pool (cudaMallocAsync); the library raises the pool's
  * release threshold, so memory freed by la_destroy stays reserved for the next
  * context of the process.
- * Errors: LA_EINVAL when L < 2 or L > 16, X or Y <= 1 or > 65535, any r, c,
+ * Errors: LA_EINVAL when L < 2 or L > 16, X or Y <= 1 or > 65535, 3 X Y >= 2^32
+ * (footprint element ids of the batching pass are 32-bit), any r, c,
  * vr, ofw, W_*, s_pos, s_zero or capacity negative, delta_lo > delta_hi, a
  * direction without a routable layer, bad rank/world; LA_ECUDA / LA_ENCCL on
  * device errors; LA_ENOMEM. */
@@ -178,6 +179,11 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches);
 
 /* Alg. 3 + Alg. 4 for batch k on this rank's shard of the batch: bottom-up
  * candidate DP with look-ahead, then backtrack.  Enqueue only.
+ * At world == 1 (conflict-free batches) the demand commit of batch k is FUSED into
+ * this call's kernel (each net commits as soon as it is backtracked), so la_get_demand
+ * between la_assign_batch(k) and la_commit_demand(k) already sees batch k's demand;
+ * la_commit_demand(k) then only advances the batch state.  With world > 1 or snapshot
+ * batches the commit happens in la_commit_demand (after the reconcile).
  * Errors: LA_ERANGE (k out of range), LA_ESTATE (k is not the next batch). */
 la_status la_assign_batch(la_ctx *ctx, int32_t batch);
 
@@ -268,7 +274,8 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias,
                           int64_t *wire_ptr, int32_t *wires,
                           int64_t *via_ptr, int32_t *vias, double *net_cost);
 
-/* Current demand in the API layout of la_grid_desc (either may be NULL). */
+/* Current demand in the API layout of la_grid_desc (either may be NULL).  Includes the
+ * commits enqueued so far (see la_assign_batch for the fused world == 1 commit). */
 la_status la_get_demand(la_ctx *ctx, int32_t *wire_dem, int32_t *via_dem);
 
 /* Conflict-free batch id of every net, input order. */

@@ -38,6 +38,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 extern "C" {
 
 struct OGrid {
@@ -94,6 +96,9 @@ struct OOut {
     // batch reads the demand at the start of its batch, and the batch's commits are applied
     // after all its nets (integer adds: their order does not matter).  NULL: sequential.
     const int32_t *snap_batch;
+    // mode 2: > 1 = the nets of each conflict-free batch on this many host
+    // threads (exact by c.2); 0 / 1 = mode 1, sequential.  Ignored with snap_batch.
+    int32_t threads;
 };
 
 }  // extern "C"
@@ -636,6 +641,106 @@ int oracle_net_dp(const OGrid *g, const ONets *nets, int64_t net, int32_t max_no
     return 0;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Per-net outputs of one net (filled by solve_net; copied into OOut by the caller).
+struct NetResult {
+    double cost, ncap, nrc, seconds;
+    std::vector<std::array<int32_t, 5>> wires;
+    std::vector<std::array<int32_t, 4>> vias;
+};
+
+// O2/O3 + O6 + O7 + O8 + O9 for one net whose tree T is built: DP on the current demand, backtrack,
+// commit (into C's demand, or appended to pend_w / pend_v in snapshot mode), Elmore.
+void solve_net(Ctx &C, const ONets *nets, int64_t net, const Tree &T, NetState &st, bool want_sol,
+               std::vector<int64_t> *pend_w, std::vector<int64_t> *pend_v, double *sink_delay, NetResult &R) {
+    const int L = C.L;
+    const int64_t drv = nets->pin_ptr[net];
+    const size_t nn = T.x.size();
+    net_weights_ur(C, nets, net, drv, T, st);
+    auto t0 = std::chrono::steady_clock::now();
+    // O6 bottom-up (children before parents)
+    net_dp(C, nets, drv, T, st);
+    // O7 backtrack (Alg. 4): root layer = driver pin layer (R13)
+    st.lay.assign(nn, -1); st.sb.assign(nn, -1); st.st.assign(nn, -1);
+    int root = T.pre[0];
+    st.lay[root] = nets->pin_layer[drv];
+    R.cost = st.f[(size_t)root * L + st.lay[root]];
+    for (int n : T.pre) {
+        size_t idx = (size_t)n * L + st.lay[n];
+        st.sb[n] = st.cb[idx];
+        st.st[n] = st.ct[idx];
+        for (size_t i = 0; i < T.kids[n].size(); i++) st.lay[T.kids[n][i]] = st.entry[idx * 4 + i];
+    }
+    // O8 commit: +1 per unit edge on the chosen layer, +1 per via cut
+    for (int n : T.pre) {
+        if (T.par[n] >= 0) {
+            int j = st.lay[n], x = T.x[n], y = T.y[n], len = T.len[n];
+            for (int i = 0; i < len; i++) {
+                int64_t idx;
+                switch (T.edir[n]) {
+                    case DIR_E: idx = wire_index(C, j, x - len + i, y); break;
+                    case DIR_W: idx = wire_index(C, j, x + i, y); break;
+                    case DIR_N: idx = wire_index(C, j, x, y - len + i); break;
+                    default:    idx = wire_index(C, j, x, y + i); break;
+                }
+                if (pend_w) pend_w->push_back(idx);
+                else C.wdem[idx] += 1;
+            }
+        }
+        for (int k = st.sb[n]; k < st.st[n]; k++) {
+            if (pend_v) pend_v->push_back(via_index(C, k, T.x[n], T.y[n]));
+            else C.vdem[via_index(C, k, T.x[n], T.y[n])] += 1;
+        }
+    }
+    // O9 Elmore
+    elmore(C, nets, drv, T, st, sink_delay, &R.ncap, &R.nrc);
+    R.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    R.wires.clear();
+    R.vias.clear();
+    if (want_sol) {
+        for (int n : T.pre) {
+            if (T.par[n] < 0) continue;
+            int p = T.par[n];
+            R.wires.push_back({std::min(T.x[n], T.x[p]), std::min(T.y[n], T.y[p]), std::max(T.x[n], T.x[p]),
+                               std::max(T.y[n], T.y[p]), st.lay[n]});
+        }
+        std::sort(R.wires.begin(), R.wires.end());
+        for (int n : T.pre)
+            if (st.st[n] > st.sb[n]) R.vias.push_back({T.x[n], T.y[n], st.sb[n], st.st[n]});
+        std::sort(R.vias.begin(), R.vias.end());
+    }
+}
+
+// Tree of net `net` after the pin checks (no pins, pin layer >= L, route errors).
+bool checked_tree(Ctx &C, const ONets *nets, int64_t net, Tree &T, char *err) {
+    NetView nv{nets->pin_ptr[net], nets->pin_ptr[net + 1], nets->seg_ptr[net], nets->seg_ptr[net + 1]};
+    if (nv.p1 <= nv.p0) { std::snprintf(err, 256, "net %lld: no pins", (long long)net); return false; }
+    for (int64_t p = nv.p0; p < nv.p1; p++)
+        if (nets->pin_layer[p] >= C.L) { std::snprintf(err, 256, "net %lld: pin layer >= L", (long long)net); return false; }
+    char buf[256] = {0};
+    char *keep = C.err;
+    C.err = buf;
+    bool ok = build_tree(C, net, nv, T);
+    C.err = keep;
+    if (!ok) std::memcpy(err, buf, 256);
+    return ok;
+}
+
+// footprint(j) = unit 2D edges of its route U GCells of its LA nodes; element spaces disjoint
+// (SURVEY §8(c) c.2).
+void footprint(const Ctx &C, const Tree &T, std::vector<int64_t> &fp) {
+    fp.clear();
+    for (int64_t k : T.edges) fp.push_back(k);   // unit edges: 2*(y*X+x)+t
+    for (size_t n = 0; n < T.x.size(); n++) fp.push_back((int64_t)2 * C.X * C.Y + (int64_t)T.y[n] * C.X + T.x[n]);
+}
+
+}  // namespace
+
+extern "C" {
+
 int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     Ctx C;
     C.g = g; C.nets = nets; C.X = g->X; C.Y = g->Y; C.L = g->L;
@@ -672,106 +777,135 @@ int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
         pend_v.clear();
     };
     int64_t nrun = (out->max_nets_to_run > 0 && out->max_nets_to_run < NN) ? out->max_nets_to_run : NN;
-
-    // batch recurrence: footprint = unit edges U node GCells; element spaces disjoint
-    std::vector<int32_t> last;
-    if (out->batch_of) last.assign((size_t)3 * C.X * C.Y, -1);
+    const bool want_sol = out->wire_ptr || out->via_ptr;
 
     std::vector<std::vector<std::array<int32_t, 5>>> wires_of(out->wire_ptr ? NN : 0);
     std::vector<std::vector<std::array<int32_t, 4>>> vias_of(out->via_ptr ? NN : 0);
     if (out->net_cost) for (int64_t i = 0; i < NN; i++) out->net_cost[i] = std::numeric_limits<double>::quiet_NaN();
     if (out->sink_delay) for (int64_t p = 0; p < nets->pin_ptr[NN]; p++) out->sink_delay[p] = 0.0;
+    std::vector<double> dummy;   // sink-delay sink when the caller passes none
+    double *sd = out->sink_delay;
+    if (!sd) { dummy.assign(nets->pin_ptr[NN], 0.0); sd = dummy.data(); }
+    auto store = [&](int64_t net, NetResult &R) {
+        if (out->net_cost) out->net_cost[net] = R.cost;
+        if (out->net_cap) out->net_cap[net] = R.ncap;
+        if (out->net_rc) out->net_rc[net] = R.nrc;
+        if (out->wire_ptr) wires_of[net].swap(R.wires);
+        if (out->via_ptr) vias_of[net].swap(R.vias);
+    };
 
     double elapsed = 0.0;
-    std::vector<double> dummy;   // sink-delay sink when the caller passes none
-    Tree T;
-    NetState st;
-    for (int64_t oi = 0; oi < nrun; oi++) {
-        int64_t net = order[oi];
-        if (snap && oi > 0 && snap[net] != snap[order[oi - 1]]) flush();
-        NetView nv{nets->pin_ptr[net], nets->pin_ptr[net + 1], nets->seg_ptr[net], nets->seg_ptr[net + 1]};
-        if (nv.p1 <= nv.p0) { std::snprintf(out->err, 256, "net %lld: no pins", (long long)net); return -1; }
-        for (int64_t p = nv.p0; p < nv.p1; p++)
-            if (nets->pin_layer[p] >= L) { std::snprintf(out->err, 256, "net %lld: pin layer >= L", (long long)net); return -1; }
-        if (!build_tree(C, net, nv, T)) return -1;
-        const int64_t drv = nv.p0;
-        const size_t nn = T.x.size();
-        if (out->n_nodes) out->n_nodes[net] = (int32_t)nn;
-
-        net_weights_ur(C, nets, net, drv, T, st);
-        auto t0 = std::chrono::steady_clock::now();
-        // O6 bottom-up (children before parents)
-        net_dp(C, nets, drv, T, st);
-        // O7 backtrack (Alg. 4): root layer = driver pin layer (R13)
-        st.lay.assign(nn, -1); st.sb.assign(nn, -1); st.st.assign(nn, -1);
-        int root = T.pre[0];
-        st.lay[root] = nets->pin_layer[drv];
-        double cost = st.f[(size_t)root * L + st.lay[root]];
-        for (int n : T.pre) {
-            size_t idx = (size_t)n * L + st.lay[n];
-            st.sb[n] = st.cb[idx];
-            st.st[n] = st.ct[idx];
-            for (size_t i = 0; i < T.kids[n].size(); i++) st.lay[T.kids[n][i]] = st.entry[idx * 4 + i];
-        }
-        // O8 commit: +1 per unit edge on the chosen layer, +1 per via cut
-        for (int n : T.pre) {
-            if (T.par[n] >= 0) {
-                int j = st.lay[n], x = T.x[n], y = T.y[n], len = T.len[n];
-                for (int i = 0; i < len; i++) {
-                    int64_t idx;
-                    switch (T.edir[n]) {
-                        case DIR_E: idx = wire_index(C, j, x - len + i, y); break;
-                        case DIR_W: idx = wire_index(C, j, x + i, y); break;
-                        case DIR_N: idx = wire_index(C, j, x, y - len + i); break;
-                        default:    idx = wire_index(C, j, x, y + i); break;
-                    }
-                    if (snap) pend_w.push_back(idx);
-                    else C.wdem[idx] += 1;
-                }
-            }
-            for (int k = st.sb[n]; k < st.st[n]; k++) {
-                if (snap) pend_v.push_back(via_index(C, k, T.x[n], T.y[n]));
-                else C.vdem[via_index(C, k, T.x[n], T.y[n])] += 1;
+    const int threads = out->threads > 1 ? out->threads : 1;
+    if (threads == 1 || snap) {
+        // ---- mode 1: sequential, one net at a time in priority order, commit after each (c.2) ----
+        // batch recurrence: footprint = unit edges U node GCells; element spaces disjoint
+        std::vector<int32_t> last;
+        if (out->batch_of) last.assign((size_t)3 * C.X * C.Y, -1);
+        Tree T;
+        NetState st;
+        NetResult R;
+        std::vector<int64_t> fp;
+        for (int64_t oi = 0; oi < nrun; oi++) {
+            int64_t net = order[oi];
+            if (snap && oi > 0 && snap[net] != snap[order[oi - 1]]) flush();
+            if (!checked_tree(C, nets, net, T, out->err)) return -1;
+            if (out->n_nodes) out->n_nodes[net] = (int32_t)T.x.size();
+            solve_net(C, nets, net, T, st, want_sol, snap ? &pend_w : nullptr, snap ? &pend_v : nullptr, sd, R);
+            elapsed += R.seconds;
+            store(net, R);
+            if (out->batch_of) {
+                footprint(C, T, fp);
+                int32_t b = 0;
+                for (int64_t e : fp) b = std::max(b, last[e] + 1);
+                for (int64_t e : fp) last[e] = b;
+                out->batch_of[net] = b;
             }
         }
-        // O9 Elmore
-        double ncap = 0, nrc = 0;
-        double *sd = out->sink_delay;
-        if (!sd) { if (dummy.empty()) dummy.assign(nets->pin_ptr[NN], 0.0); sd = dummy.data(); }
-        elmore(C, nets, drv, T, st, sd, &ncap, &nrc);
-        auto t1 = std::chrono::steady_clock::now();
-        elapsed += std::chrono::duration<double>(t1 - t0).count();
-
-        if (out->net_cost) out->net_cost[net] = cost;
-        if (out->net_cap) out->net_cap[net] = ncap;
-        if (out->net_rc) out->net_rc[net] = nrc;
-        if (out->wire_ptr) {
-            auto &W = wires_of[net];
-            for (int n : T.pre) {
-                if (T.par[n] < 0) continue;
-                int p = T.par[n];
-                W.push_back({std::min(T.x[n], T.x[p]), std::min(T.y[n], T.y[p]), std::max(T.x[n], T.x[p]),
-                             std::max(T.y[n], T.y[p]), st.lay[n]});
-            }
-            std::sort(W.begin(), W.end());
-        }
-        if (out->via_ptr) {
-            auto &Vv = vias_of[net];
-            for (int n : T.pre)
-                if (st.st[n] > st.sb[n]) Vv.push_back({T.x[n], T.y[n], st.sb[n], st.st[n]});
-            std::sort(Vv.begin(), Vv.end());
-        }
-        if (out->batch_of) {
+        flush();
+    } else {
+        // ---- mode 2: the same nets, batch by batch; the nets of one
+        // conflict-free batch run concurrently on `threads` host threads.  Exact by c.2: nets of a
+        // batch have disjoint footprints, so each reads and commits only state no other net of
+        // the batch touches, and every net sees the commits of all earlier conflicting nets. ----
+        std::vector<int32_t> bat(nrun);
+        std::vector<int32_t> nodes_of(nrun);
+        std::vector<int64_t> fp_ptr(nrun + 1, 0);
+        std::vector<std::vector<int64_t>> fp_chunk(threads);
+        std::vector<int64_t> chunk_beg(threads + 1);
+        for (int t = 0; t <= threads; t++) chunk_beg[t] = nrun * t / threads;
+        volatile bool failed = false;
+        char errbuf[256] = {0};
+        // (a) trees -> footprints, in parallel (contiguous chunks of the priority order)
+#pragma omp parallel num_threads(threads)
+        {
+            int t = omp_get_thread_num();
+            Tree T;
             std::vector<int64_t> fp;
-            for (int64_t k : T.edges) fp.push_back(k);   // unit edges: 2*(y*X+x)+t
-            for (size_t n = 0; n < nn; n++) fp.push_back((int64_t)2 * C.X * C.Y + (int64_t)T.y[n] * C.X + T.x[n]);
-            int32_t b = 0;
-            for (int64_t e : fp) b = std::max(b, last[e] + 1);
-            for (int64_t e : fp) last[e] = b;
-            out->batch_of[net] = b;
+            char err[256];
+            for (int64_t oi = chunk_beg[t]; oi < chunk_beg[t + 1] && !failed; oi++) {
+                if (!checked_tree(C, nets, order[oi], T, err)) {
+#pragma omp critical
+                    { if (!failed) { failed = true; std::memcpy(errbuf, err, 256); } }
+                    break;
+                }
+                footprint(C, T, fp);
+                nodes_of[oi] = (int32_t)T.x.size();
+                fp_ptr[oi + 1] = (int64_t)fp.size();
+                fp_chunk[t].insert(fp_chunk[t].end(), fp.begin(), fp.end());
+            }
         }
+        if (failed) { std::memcpy(out->err, errbuf, 256); return -1; }
+        // (b) the sequential batch recurrence over the footprints, in priority order
+        {
+            std::vector<int32_t> last((size_t)3 * C.X * C.Y, -1);
+            int64_t k = 0;
+            for (int t = 0; t < threads; t++) {
+                const std::vector<int64_t> &F = fp_chunk[t];
+                int64_t pos = 0;
+                for (int64_t oi = chunk_beg[t]; oi < chunk_beg[t + 1]; oi++, k++) {
+                    int64_t cnt = fp_ptr[oi + 1];
+                    int32_t b = 0;
+                    for (int64_t i = 0; i < cnt; i++) b = std::max(b, last[F[pos + i]] + 1);
+                    for (int64_t i = 0; i < cnt; i++) last[F[pos + i]] = b;
+                    pos += cnt;
+                    bat[oi] = b;
+                }
+                std::vector<int64_t>().swap(fp_chunk[t]);
+            }
+        }
+        for (int64_t oi = 0; oi < nrun; oi++) {
+            if (out->batch_of) out->batch_of[order[oi]] = bat[oi];
+            if (out->n_nodes) out->n_nodes[order[oi]] = nodes_of[oi];
+        }
+        // (c) batches in order; inside a batch, nets in parallel
+        int32_t nb = 0;
+        for (int64_t oi = 0; oi < nrun; oi++) nb = std::max(nb, bat[oi] + 1);
+        std::vector<int64_t> bptr(nb + 1, 0), bnets(nrun);
+        for (int64_t oi = 0; oi < nrun; oi++) bptr[bat[oi] + 1]++;
+        for (int32_t b = 0; b < nb; b++) bptr[b + 1] += bptr[b];
+        {
+            std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+            for (int64_t oi = 0; oi < nrun; oi++) bnets[fill[bat[oi]]++] = order[oi];
+        }
+        auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel num_threads(threads)
+        {
+            Tree T;
+            NetState st;
+            NetResult R;
+            char err[256];
+            for (int32_t b = 0; b < nb; b++) {
+#pragma omp for schedule(dynamic, 64)
+                for (int64_t i = bptr[b]; i < bptr[b + 1]; i++) {
+                    int64_t net = bnets[i];
+                    if (!checked_tree(C, nets, net, T, err)) continue;   // cannot fail: checked in (a)
+                    solve_net(C, nets, net, T, st, want_sol, nullptr, nullptr, sd, R);
+                    store(net, R);
+                }   // implicit barrier: batch b is committed before b + 1 starts
+            }
+        }
+        elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
-    flush();
     out->elapsed_s = elapsed;
     out->nets_run = nrun;
     if (out->wire_ptr) {

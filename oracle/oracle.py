@@ -23,7 +23,7 @@ c_i32, c_i64, c_u8, c_f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8, ctyp
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-shared", "-fPIC",
+        subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-fopenmp", "-shared", "-fPIC",
                                "-o", _SO, _SRC])
     return _SO
 
@@ -51,7 +51,7 @@ class OOut(ctypes.Structure):
                 ("via_ptr", P(c_i64)), ("vias", P(c_i32)), ("wire_dem", P(c_i32)), ("via_dem", P(c_i32)),
                 ("sink_delay", P(c_f64)), ("net_cap", P(c_f64)), ("net_rc", P(c_f64)),
                 ("batch_of", P(c_i32)), ("n_nodes", P(c_i32)), ("elapsed_s", c_f64), ("nets_run", c_i64),
-                ("err", ctypes.c_char * 256), ("snap_batch", P(c_i32))]
+                ("err", ctypes.c_char * 256), ("snap_batch", P(c_i32)), ("threads", c_i32)]
 
 
 _lib = None
@@ -116,11 +116,13 @@ def _nets(d, keep):
 
 
 def run(d, solution: bool = True, grids: bool = True, timing: bool = True, batches: bool = True,
-        max_nets: int = 0, snap_batch=None) -> dict:
+        max_nets: int = 0, snap_batch=None, threads: int = 1) -> dict:
     """Sequential oracle over design ``d`` (gen.synth.Design).  Returns numpy arrays:
     net_cost, wire_ptr/wires, via_ptr/vias, wire_dem, via_dem, sink_delay, net_cap,
     net_rc, batch_of, n_nodes, elapsed_s, nets_run.  ``snap_batch`` (int32 per net):
-    paper-style snapshot batches (NEXT #1, reading R31) instead of sequential commits."""
+    paper-style snapshot batches (NEXT #1, reading R31) instead of sequential commits.
+    ``threads`` > 1: mode 2, the nets of each conflict-free batch on that many
+    host threads (OpenMP); exact by SURVEY §8(c) c.2, so every output equals mode 1's."""
     lib = _load()
     keep = []
     g = _grid(d, keep)
@@ -141,6 +143,7 @@ def run(d, solution: bool = True, grids: bool = True, timing: bool = True, batch
     o.max_wires = res["wires"].shape[0] if solution else 0
     o.max_vias = res["vias"].shape[0] if solution else 0
     o.max_nets_to_run = max_nets
+    o.threads = int(threads)
     if snap_batch is not None:
         snap_batch = np.ascontiguousarray(snap_batch, np.int32)
         keep.append(snap_batch)

@@ -638,6 +638,10 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     *out = nullptr;
     if (g->L < 2 || g->L > MAXL) return set_err(LA_EINVAL, "L must be in [2, 16]");
     if (g->X <= 1 || g->Y <= 1 || g->X > 65535 || g->Y > 65535) return set_err(LA_EINVAL, "X, Y must be in [2, 65535]");
+    // conflict-free batching sorts (element << 32 | rank) keys over 3 X Y footprint elements
+    // (unit H edges, unit V edges, GCells): the element id must fit in 32 bits
+    if ((uint64_t)3 * (uint64_t)g->X * (uint64_t)g->Y >= ((uint64_t)1 << 32))
+        return set_err(LA_EINVAL, "grid too large: 3 X Y must be < 2^32 (footprint element ids)");
     if (!g->dir || !g->routable || !g->r || !g->c || !g->vr || !g->ofw || !g->wire_cap || !g->via_cap)
         return set_err(LA_EINVAL, "null grid array");
     const int L = g->L;

@@ -83,3 +83,45 @@ def rebuild_demand(d: synth.Design, wires, vias):
     if d.via_dem0 is not None:
         vd += d.via_dem0
     return wd.astype(np.int32), vd.astype(np.int32)
+
+
+# Canonical outputs of one whole run (SURVEY §8(d) d.5 "parity at config 5 compares hashes"): the
+# arrays, their dtypes and byte order are fixed here so the oracle's golden hashes
+# (tools/oracle_golden.py) and the GPU run hash the same bytes.  Floating-point outputs are hashed
+# as their IEEE bit patterns.  No method arithmetic.
+HASH_KEYS = (("wire_ptr", "<i8"), ("wires", "<i4"), ("via_ptr", "<i8"), ("vias", "<i4"), ("wire_dem", "<i4"),
+             ("via_dem", "<i4"), ("batch_of", "<i4"), ("net_cost", "<f8"), ("sink_delay", "<f8"),
+             ("net_cap", "<f8"), ("net_rc", "<f8"))
+HASH_CHUNKS = 64
+
+
+def output_hashes(res) -> dict:
+    """SHA-256 of every canonical output array, plus per-chunk hashes (HASH_CHUNKS equal slices
+    along axis 0) so a mismatch can be localised without the oracle's arrays."""
+    import hashlib
+    out = {}
+    for k, dt in HASH_KEYS:
+        a = np.ascontiguousarray(np.asarray(res[k]).astype(dt, copy=False))
+        n = a.shape[0]
+        out[k] = {"sha256": hashlib.sha256(a.tobytes()).hexdigest(), "shape": list(a.shape),
+                  "chunks": [hashlib.sha256(a[n * i // HASH_CHUNKS: n * (i + 1) // HASH_CHUNKS].tobytes()).hexdigest()[:16]
+                             for i in range(HASH_CHUNKS)]}
+    return out
+
+
+def compare_hashes(got: dict, want: dict) -> list:
+    """Mismatch report: per array, the shape difference or the first differing chunk and its
+    element range."""
+    bad = []
+    for k, _ in HASH_KEYS:
+        g, w = got[k], want[k]
+        if g["sha256"] == w["sha256"]:
+            continue
+        if g["shape"] != w["shape"]:
+            bad.append(f"{k}: shape {g['shape']} != {w['shape']}")
+            continue
+        n = w["shape"][0]
+        first = next(i for i in range(HASH_CHUNKS) if g["chunks"][i] != w["chunks"][i])
+        bad.append(f"{k}: first differing chunk {first} = elements [{n * first // HASH_CHUNKS}, "
+                   f"{n * (first + 1) // HASH_CHUNKS})")
+    return bad

@@ -75,6 +75,7 @@ def _desc(la, d, **over):
     (dict(L=1), "L must be"),
     (dict(L=17), "L must be"),
     (dict(X=1), "X, Y"),
+    (dict(X=40000, Y=40000), "grid too large"),
     (dict(r=-np.ones(6)), "negative"),
     (dict(W_D=-1.0), "negative"),
     (dict(delta_lo=5, delta_hi=4), "delta_lo"),

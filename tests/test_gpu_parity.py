@@ -429,3 +429,23 @@ def test_assign_variants_bitwise(la, cfg, variant, monkeypatch):
     monkeypatch.setenv("GAPLA_ASSIGN_VARIANT", variant)
     d = synth.make_config(cfg)
     assert_parity(run_gpu(la, d), oracle.run(d), bitwise_fp=True)
+
+
+# --------------------------------------------------------------- full-size parity (hashes)
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_config_full_size_oracle_hashes(la, cfg):
+    """Configs 4 and 5 at full size in the bench's launch configuration (LayerAssigner.run =
+    la_assign_all + la_eval_timing, default schedule and variants) against the SHA-256 hashes of
+    the oracle's outputs (tests/golden/oracle_hashes_cfg{4,5}.json, written by
+    tools/oracle_golden.py from oracle/ only).  Every array bit for bit:
+    solution, both demand grids, batch ids, and the bit patterns of f_root, sink delays, net
+    caps and net RC sums.  A mismatch names the first differing 1/64 slice of each array."""
+    from helpers import compare_hashes, golden, output_hashes
+    want = golden(f"oracle_hashes_cfg{cfg}.json")
+    d = synth.make_config(cfg)
+    assert d.n_nets == want["n_nets"] and d.n_pins == want["n_pins"]
+    got = run_gpu(la, d)
+    assert got["n_batches"] == want["n_batches"]
+    bad = compare_hashes(output_hashes(got), want["hashes"])
+    assert not bad, "; ".join(bad)
