@@ -24,21 +24,23 @@ def nccl_dir() -> str:
     raise RuntimeError("NCCL headers (nvidia/nccl from the torch wheel) not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra: list | None = None, out: str | None = None) -> str:
+    """extra / out: tuning variants (extra nvcc flags, an alternate library name in lib/, loaded with GAPLA_SO)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "la_internal.h"), os.path.join(CSRC, "la_device.cuh"),
                    os.path.join(ROOT, "include", "la.h")]
-    if not force and os.path.exists(SO) and all(os.path.getmtime(SO) >= os.path.getmtime(d) for d in deps):
-        return SO
+    so = os.path.join(LIBDIR, out) if out else SO
+    if not force and os.path.exists(so) and all(os.path.getmtime(so) >= os.path.getmtime(d) for d in deps):
+        return so
     os.makedirs(LIBDIR, exist_ok=True)
     nccl = nccl_dir()
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
            "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-pthread", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"),
-           "-shared", "-o", SO, *srcs,
+           *(extra or []), "-shared", "-o", so, *srcs,
            "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nccl, "lib")]
     subprocess.check_call(cmd)
-    return SO
+    return so
 
 
 if __name__ == "__main__":

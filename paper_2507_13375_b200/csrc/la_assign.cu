@@ -701,6 +701,532 @@ __device__ __forceinline__ void run_net(const NetCtx &c, WarpScr &w, const Share
         for (int64_t e = a.succ_off[net] + tid; e < a.succ_off[net + 1]; e += nthr) atomicSub(a.wait + a.succ[e], 1);
 }
 
+// A global slot for a big net that does not fit shared memory: a small pool of slots, each
+// guarded by a lock word (the pool is sized by the host budget, not by the grid).
+__device__ __forceinline__ int gslot_acquire(const AssignLaunch &a, int hid) {
+    int s = hid % a.n_gslots;
+    unsigned ns = 64;
+    while (atomicCAS(a.glock + s, 0, 1) != 0) {
+        s = s + 1 == a.n_gslots ? 0 : s + 1;
+        __nanosleep(ns);
+        ns = min(ns * 2, 1024u);
+    }
+    __threadfence();
+    return s;
+}
+
+__device__ __forceinline__ void gslot_release(const AssignLaunch &a, int s) {
+    __threadfence();
+    atomicExch(a.glock + s, 0);
+}
+
+// ------------------------------------------------------------- group path --
+// Batch mode, every net that fits a warp's arena (DESIGN §5 "group path"): an 8-lane GROUP
+// runs one net and a warp runs up to four nets side by side (a host-packed "job").  Lane e of
+// a group owns entry layer slot e of the node being processed (Alg. 3 l.2-3: one thread per
+// (node, layer)); the group walks the net's nodes in forest order (children before parents).
+//
+// Candidate spans by son-layer combinations (exact).  For a node with sons s_1..s_k and entry
+// l, every choice of son layers (j_1..j_k) has a cover span S_c = [min(b0, j..), max(t0, j..)]
+// and the value v_c = ((V(S_c) + cost'(j_1)) + ...).  For every span S, v_c >= G'(S_c) (a son's
+// window minimum is <= its chosen value; rounded addition is monotone) and the combination of
+// S's own window argmins has a cover inside S, hence a value <= G'(S) (V is monotone under
+// inclusion because kappa >= 0).  So min_c v_c equals the minimum G' over all spans, bitwise, and
+// the key winner (G', t-b, b) of Alg. 3's enumeration is the cover of a minimum-value combination
+// with the smallest (t-b, b): the lanes enumerate combinations (LD per son: L-independent loops,
+// uniform across the warp's four groups), then take each son's lowest-layer window argmin on the
+// winning span (R21) and recompute G with cost (not cost') and K in son order (O6).  V(b, t)
+// comes from a per-node table the group builds first, row b summed ascending from b (R10, R23).
+// Nodes with three or more sons (rare) sweep the spans directly (group_sweep).
+struct NodeG {
+    double wd, ur;                    // W_D w_n (Eq. 5), ur (O3)
+    uint32_t xy;                      // x | y << 16
+    uint16_t len, sink0, nsink, height;
+    uint16_t kid[MAXKIDS];            // children (net-local), E W N S order
+    uint8_t edir, nkid, nl, nh, lay, sb, st;
+};
+static_assert(sizeof(NodeG) == 48, "NodeG layout");
+
+struct GLay {
+    int node, ac, kap, dec, sink, player, froot, vt, bytes;
+};
+
+// One net's DP state in a group's part of the warp arena: node records, (A, C) per (node,
+// entry slot) (gathered S first, then O5's A and capb of the parent edge), kappa per (node,
+// cut), decisions per (node, slot), sinks (C_q, weight), sink layers and the V(b, t) table of
+// the node being processed (triangular, row b from t = b) -- one per group of the team running
+// the net (nvt: 1 on the small-net path, 8 or 16 for a big net).
+__host__ __device__ inline int vt_elems(int L) { return L * (L + 1) / 2; }
+
+__host__ __device__ inline GLay group_layout(int nn, int ns, int L, int LD, int nvt = 1) {
+    GLay w;
+    int o = 0;
+    auto take = [&](int bytes) { int r = o; o += (bytes + 15) & ~15; return r; };
+    w.node = take(48 * nn);
+    w.ac = take(16 * nn * LD);
+    w.kap = take(8 * nn * (L - 1));
+    w.dec = take(4 * nn * LD);
+    w.sink = take(16 * ns);
+    w.player = take(ns);
+    w.froot = take(8);
+    w.vt = take(8 * vt_elems(L) * nvt);
+    w.bytes = o;
+    return w;
+}
+
+struct GNet {
+    NodeG *nd;
+    double2 *AC;
+    double *kap, *Vt, *froot;
+    uint32_t *dec;
+    double2 *sk;
+    uint8_t *pl;
+};
+
+__device__ __forceinline__ int vtri(int b, int t, int L) { return ((b * (2 * L + 1 - b)) >> 1) + (t - b); }
+
+// O5 cost'(l; s, j) of son s (A, C at its slot for layer j), +inf where the son is infeasible.
+__device__ __forceinline__ double cost_p(const double2 ac, double wdk, double vr, double urn) {
+    if (!(ac.x < dinf())) return dinf();
+    const double Bv = wdk * ac.y;                     // B = wd_s (Cw + D)
+    const double cost = ac.x + Bv * vr;
+    return cost + Bv * urn;
+}
+
+// Nodes with 3 or 4 sons: bottoms b in {b0} U {legal son layers < b0}, descending, tops t in
+// {t0} U {legal son layers > t0}, ascending; son k's window minimum is D_k over [b, b0-1]
+// (descending, <=: the lower layer wins ties) then the layers [b0, t] (ascending, strict <).
+// Returns the key (t-b) << 4 | b (bit 8: no feasible span) and the window argmins in *js.
+__device__ __noinline__ uint32_t group_sweep(const Shared &sh, const GNet &n, int i, int l, int b0, int t0, int L,
+                                             int LD, uint32_t *js) {
+    const NodeG &r = n.nd[i];
+    const int nk = r.nkid;
+    const double urn = r.ur;
+    const double *VRl = sh.T.VR + l * MAXL;
+    int kid[MAXKIDS], kdt[MAXKIDS];
+    double wdk[MAXKIDS];
+    uint32_t legal_any = 0;
+#pragma unroll
+    for (int k = 0; k < MAXKIDS; ++k) {
+        kid[k] = k < nk ? r.kid[k] : 0;
+        kdt[k] = k < nk ? (n.nd[kid[k]].edir <= 1 ? 0 : 1) : 2;
+        wdk[k] = n.nd[kid[k]].wd;
+        if (k < nk) legal_any |= sh.legal[kdt[k]];
+    }
+    double D[MAXKIDS];
+    uint32_t jD = 0;
+#pragma unroll
+    for (int k = 0; k < MAXKIDS; ++k) D[k] = dinf();
+    double bestG = dinf();
+    uint32_t bestK = 0x1ffu, bestJ = 0;
+    uint32_t rem = legal_any & ((1u << b0) - 1u);
+    int b = b0;
+    for (;;) {
+        double U[MAXKIDS];
+        uint32_t jU = jD;
+#pragma unroll
+        for (int k = 0; k < MAXKIDS; ++k) U[k] = D[k];
+#pragma unroll 1
+        for (int t = b0; t < L; ++t) {
+            const bool son_layer = (legal_any >> t) & 1;
+            if (son_layer) {
+                const int dtt = sh.dir[t], st = sh.lidx[t];
+                const double vr = VRl[t];
+#pragma unroll
+                for (int k = 0; k < MAXKIDS; ++k)
+                    if (kdt[k] == dtt) {
+                        const double cp = cost_p(n.AC[kid[k] * LD + st], wdk[k], vr, urn);
+                        if (cp < U[k]) {
+                            U[k] = cp;
+                            jU = (jU & ~(0xfu << (4 * k))) | ((uint32_t)t << (4 * k));
+                        }
+                    }
+            }
+            if (t >= t0 && (t == t0 || son_layer)) {
+                bool feas = true;
+                double g = n.Vt[vtri(b, t, L)];
+#pragma unroll
+                for (int k = 0; k < MAXKIDS; ++k)
+                    if (k < nk) {
+                        feas = feas && U[k] < dinf();
+                        g = g + U[k];
+                    }
+                const uint32_t key = (uint32_t)(((t - b) << 4) | b);
+                if (feas && (g < bestG || (g == bestG && key < bestK))) {
+                    bestG = g;
+                    bestK = key;
+                    bestJ = jU;
+                }
+            }
+        }
+        if (!rem) break;
+        b = 31 - __clz(rem);                        // next candidate bottom, descending
+        rem &= ~(1u << b);
+        const int dtb = sh.dir[b], sbb = sh.lidx[b];
+        const double vr = VRl[b];
+#pragma unroll
+        for (int k = 0; k < MAXKIDS; ++k)
+            if (kdt[k] == dtb) {
+                const double cp = cost_p(n.AC[kid[k] * LD + sbb], wdk[k], vr, urn);
+                if (cp < dinf() && cp <= D[k]) {
+                    D[k] = cp;
+                    jD = (jD & ~(0xfu << (4 * k))) | ((uint32_t)b << (4 * k));
+                }
+            }
+    }
+    *js = bestJ;
+    return bestK;
+}
+
+// Lowest-layer argmin of a son (row ac, weight w, direction d) over its legal layers in [b, t].
+__device__ __forceinline__ int son_argmin(const Shared &sh, const double2 *ac, double w, int d, const double *VRl,
+                                          double urn, int b, int t) {
+    double m = dinf();
+    int jm = 0;
+    const int nd = sh.ndir[d];
+#pragma unroll
+    for (int s = 0; s < MAXE; ++s) {
+        const int j = sh.lay_of[d][s];
+        if (s < nd && j >= b && j <= t) {
+            const double cp = cost_p(ac[s], w, VRl[j], urn);
+            if (cp < m) { m = cp; jm = j; }
+        }
+    }
+    return jm;
+}
+
+// Node i of the group's net, entry layer l (lane's slot e; the root: l = p_drv, slot 0).
+__device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, const GNet &n, int i, bool root,
+                                           int l, int e, int L, int LD, double *froot) {
+    const NodeG &r = n.nd[i];
+    const int nk = r.nkid;
+    // pin terms, sinks in input order (Alg. 3 l.4-7)
+    double F0 = 0.0, C0 = 0.0;
+#pragma unroll 1
+    for (int q = r.sink0; q < r.sink0 + r.nsink; ++q) {
+        const double2 c = n.sk[q];
+        F0 = F0 + c.y * (c.x * sh.T.VR[n.pl[q] * MAXL + l]);
+        C0 = C0 + c.x;
+    }
+    const int nl = r.nl, nh = r.nh;
+    const bool pins = nl != 255;
+    const int b0 = pins ? min(l, nl) : l, t0 = pins ? max(l, nh) : l;
+    const double *kp = n.kap + i * (L - 1);
+    const double *VRl = sh.T.VR + l * MAXL;
+    double Gv, K = 0.0;
+    int bw = b0, tw = t0;
+    uint32_t js = 0;
+    if (nk == 0) {
+        // leaf: G' = V(b, t) >= V(b0, t0) on every admissible span (kappa >= 0), so (b0, t0)
+        double V = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < L - 1; ++k)
+            if (k >= b0 && k < t0) V = V + kp[k];
+        Gv = V;
+    } else {
+        const double urn = r.ur;
+        uint32_t key = 0x1ffu;
+        const int k0 = r.kid[0], k1 = nk > 1 ? r.kid[1] : 0;
+        const int d0 = n.nd[k0].edir <= 1 ? 0 : 1, d1 = n.nd[k1].edir <= 1 ? 0 : 1;
+        const double w0 = n.nd[k0].wd, w1 = n.nd[k1].wd;
+        const double2 *ac0 = n.AC + k0 * LD, *ac1 = n.AC + k1 * LD;
+        if (nk == 1) {
+            // son-layer combinations (header), all slots at once: cost' per slot in registers,
+            // independent loads and evaluations, then a compare chain in ascending slot order
+            double c0[MAXE];
+            const int n0 = sh.ndir[d0];
+            double bestG = dinf();
+#pragma unroll
+            for (int s = 0; s < MAXE; ++s) {
+                const int j = sh.lay_of[d0][s];
+                c0[s] = s < n0 ? cost_p(ac0[s], w0, VRl[j], urn) : dinf();
+                const int bb = min(b0, j), tt = max(t0, j);
+                const double g = n.Vt[vtri(bb, tt, L)] + c0[s];
+                const uint32_t kk = (uint32_t)(((tt - bb) << 4) | bb);
+                if (c0[s] < dinf() && (g < bestG || (g == bestG && kk < key))) { bestG = g; key = kk; }
+            }
+            if (!(key & 0x100u)) {
+                bw = key & 0xf;
+                tw = bw + (int)((key >> 4) & 0xf);
+                double m = dinf();
+                int jm = 0;
+#pragma unroll
+                for (int s = 0; s < MAXE; ++s) {        // the son's lowest-layer window argmin (R21)
+                    const int j = sh.lay_of[d0][s];
+                    if (j >= bw && j <= tw && c0[s] < m) { m = c0[s]; jm = j; }
+                }
+                js = (uint32_t)jm;
+            }
+        } else if (nk == 2) {
+            // son-layer combinations; son 1's cost' per slot in registers, son 0 per outer step
+            double c1[MAXE];
+            const int n0 = sh.ndir[d0], n1 = sh.ndir[d1];
+#pragma unroll
+            for (int s = 0; s < MAXE; ++s) c1[s] = s < n1 ? cost_p(ac1[s], w1, VRl[sh.lay_of[d1][s]], urn) : dinf();
+            double bestG = dinf();
+#pragma unroll 1
+            for (int s0 = 0; s0 < n0; ++s0) {
+                const int j0 = sh.lay_of[d0][s0];
+                const double c0 = cost_p(ac0[s0], w0, VRl[j0], urn);
+                if (!(c0 < dinf())) continue;
+                const int bb = min(b0, j0), tt = max(t0, j0);
+#pragma unroll
+                for (int s1 = 0; s1 < MAXE; ++s1) {
+                    const int j1 = sh.lay_of[d1][s1];
+                    const int b = min(bb, j1), t = max(tt, j1);
+                    const double g = (n.Vt[vtri(b, t, L)] + c0) + c1[s1];
+                    const uint32_t kk = (uint32_t)(((t - b) << 4) | b);
+                    if (c1[s1] < dinf() && (g < bestG || (g == bestG && kk < key))) { bestG = g; key = kk; }
+                }
+            }
+            if (!(key & 0x100u)) {
+                bw = key & 0xf;
+                tw = bw + (int)((key >> 4) & 0xf);
+                js = (uint32_t)son_argmin(sh, ac0, w0, d0, VRl, urn, bw, tw);
+                double m = dinf();
+                int jm = 0;
+#pragma unroll
+                for (int s = 0; s < MAXE; ++s) {
+                    const int j = sh.lay_of[d1][s];
+                    if (j >= bw && j <= tw && c1[s] < m) { m = c1[s]; jm = j; }
+                }
+                js |= (uint32_t)jm << 4;
+            }
+        } else {
+            key = group_sweep(sh, n, i, l, b0, t0, L, LD, &js);
+            bw = key & 0xf;
+            tw = bw + (int)((key >> 4) & 0xf);
+        }
+        if (key & 0x100u) {                             // no feasible span (cannot happen when every
+            if (root) *froot = dinf();                  // direction has a routable layer; kept exact)
+            else n.AC[i * LD + e].x = dinf();
+            return;
+        }
+        Gv = n.Vt[vtri(bw, tw, L)];
+#pragma unroll
+        for (int k = 0; k < MAXKIDS; ++k)
+            if (k < nk) {
+                const int kk = r.kid[k];
+                const int j = (js >> (4 * k)) & 0xf;
+                const double2 ac = n.AC[kk * LD + sh.lidx[j]];
+                const double Bv = n.nd[kk].wd * ac.y;
+                Gv = Gv + (ac.x + Bv * VRl[j]);
+                K = K + ac.y;
+            }
+    }
+    const double f = F0 + Gv;
+    const double dlc = C0 + K;
+    n.dec[i * LD + e] = (uint32_t)(bw | (tw << 4)) | (js << 8);
+    if (root) {
+        *froot = f;
+        return;
+    }
+    double2 &o = n.AC[i * LD + e];
+    const double Sc = o.x;                              // congestion sum gathered up front
+    const double len = (double)r.len;
+    const double Rw = sh.T.r[l] * len;
+    const double Cw = sh.T.c[l] * len;
+    o.x = ((f + r.wd * (Rw * (0.5 * Cw + dlc))) + G.W_CAP * Cw) + (G.W_CONG * sh.T.ofw[l]) * Sc;
+    o.y = Cw + dlc;
+}
+
+__device__ __forceinline__ GNet group_net(char *base, const GLay &lay) {
+    GNet n;
+    n.nd = (NodeG *)(base + lay.node);
+    n.AC = (double2 *)(base + lay.ac);
+    n.kap = (double *)(base + lay.kap);
+    n.dec = (uint32_t *)(base + lay.dec);
+    n.sk = (double2 *)(base + lay.sink);
+    n.pl = (uint8_t *)(base + lay.player);
+    n.froot = (double *)(base + lay.froot);
+    n.Vt = (double *)(base + lay.vt);
+    return n;
+}
+
+// Gather (a3) by threads tid of nthr: node records, sinks, kappa per (node, cut) and the
+// congestion sum S per (non-root node, entry slot) -- all loads of the net in flight at once.
+__device__ __forceinline__ void group_gather(const GNet &n, const Shared &sh, const DevGrid &G, const DevForest &F,
+                                             int64_t n0, int nn, int ns, int q_base, int LD, int tid, int nthr) {
+    const int Lm1 = G.L - 1;
+    for (int i = tid; i < nn; i += nthr) {
+        const int64_t nid = n0 + i;
+        NodeG r;
+        r.wd = F.wd[nid];
+        r.ur = F.ur[nid];
+        r.xy = F.xy[nid];
+        r.len = (uint16_t)F.len[nid];
+        r.sink0 = (uint16_t)(F.sink0[nid] - q_base);
+        r.nsink = F.nsink[nid];
+        r.height = F.height[nid];
+        const int4 k4 = *reinterpret_cast<const int4 *>(F.kid + nid * 4);
+        r.kid[0] = (uint16_t)(k4.x - n0);
+        r.kid[1] = (uint16_t)(k4.y - n0);
+        r.kid[2] = (uint16_t)(k4.z - n0);
+        r.kid[3] = (uint16_t)(k4.w - n0);
+        r.edir = F.edir[nid];
+        r.nkid = F.nkid[nid];
+        r.nl = F.nl[nid];
+        r.nh = F.nh[nid];
+        r.lay = r.sb = r.st = 0;
+        n.nd[i] = r;
+    }
+    for (int q = tid; q < ns; q += nthr) {
+        n.pl[q] = F.p_layer[q_base + q];
+        n.sk[q] = make_double2(F.p_cap[q_base + q], F.p_w[q_base + q]);
+    }
+    for (int idx = tid; idx < nn * Lm1; idx += nthr) {
+        const int i = idx / Lm1, k = idx - i * Lm1;
+        const uint32_t xy = __ldg(F.xy + n0 + i);
+        n.kap[idx] = kappa_w(G, sh, __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k), k);
+    }
+    for (int idx = tid; idx < (nn - 1) * LD; idx += nthr) {
+        const int i = idx / LD, s = idx - i * LD;
+        const int64_t nid = n0 + i;
+        const int ed = __ldg(F.edir + nid);
+        const int dt = ed <= 1 ? 0 : 1;
+        if (s >= sh.ndir[dt]) continue;
+        double Sc = dinf();
+        if (sh.routable[sh.lay_of[dt][s]]) {
+            const uint32_t xy = __ldg(F.xy + nid);
+            Sc = run_sum(G, dt, s, xy & 0xffff, xy >> 16, ed, __ldg(F.len + nid));
+        }
+        n.AC[idx].x = Sc;
+    }
+}
+
+// V(b, t) table of node i by the 8 lanes of a group: row b summed ascending from b (R10, R23).
+__device__ __forceinline__ void group_vtable(const GNet &n, int i, int L, int gl) {
+    const double *kp = n.kap + i * (L - 1);
+    for (int b = gl; b < L; b += 8) {
+        double *row = n.Vt + vtri(b, b, L);
+        double V = 0.0;
+        row[0] = V;
+#pragma unroll 1
+        for (int t = b + 1; t < L; ++t) {
+            V = V + kp[t - 1];
+            row[t - b] = V;
+        }
+    }
+}
+
+// Node i by one group: lanes over the entry layers of its parent edge (the root: l = p_drv).
+__device__ __forceinline__ void group_step(const GNet &n, const Shared &sh, const DevGrid &G, int i, int nn, int pdrv,
+                                           int L, int LD, int gl) {
+    const bool root = i == nn - 1;
+    const int ed = n.nd[i].edir;
+    const int dt = ed <= 1 ? 0 : 1;
+    const int nE = root ? 1 : sh.ndir[dt];
+    if (gl < nE) {
+        const int l = root ? pdrv : sh.lay_of[dt][gl];
+        if (root || sh.routable[l]) group_node(sh, G, n, i, root, l, gl, L, LD, n.froot);
+    }
+}
+
+// Alg. 4 backtrack from the root (entry = driver pin layer, R13) by one thread: parents precede
+// children in reverse forest order.
+__device__ __forceinline__ void group_backtrack(const GNet &n, const Shared &sh, int nn, int pdrv, int LD) {
+    n.nd[nn - 1].lay = (uint8_t)pdrv;
+#pragma unroll 1
+    for (int i = nn - 1; i >= 0; --i) {
+        NodeG &r = n.nd[i];
+        const int slot = i == nn - 1 ? 0 : sh.lidx[r.lay];
+        const uint32_t d = n.dec[i * LD + slot];
+        r.sb = d & 0xf;
+        r.st = (d >> 4) & 0xf;
+        const uint32_t jj = d >> 8;
+#pragma unroll 1
+        for (int k = 0; k < r.nkid; ++k) n.nd[r.kid[k]].lay = (uint8_t)((jj >> (4 * k)) & 0xf);
+    }
+}
+
+// Decisions to HBM and the fused commit (O8), threads tid of nthr over the nodes.
+__device__ __forceinline__ void group_emit(const GNet &n, const DevGrid &G, const DevScratch &S, const AssignLaunch &a,
+                                           int64_t n0, int nn, int tid, int nthr) {
+    for (int i = tid; i < nn; i += nthr) {
+        const NodeG &r = n.nd[i];
+        S.lay[n0 + i] = r.lay;
+        S.sb[n0 + i] = r.sb;
+        S.st[n0 + i] = r.st;
+        if (a.commit) commit_node(G, r.xy, r.edir, r.len, r.lay, r.sb, r.st);
+    }
+}
+
+// One small net by one group (lanes gl = 0..7; nn = 0: no net): gather, nodes in forest order
+// (children before parents), backtrack, commit.  Called by all 32 lanes of the warp: the node
+// loop runs to the largest node count of the warp's nets with a full-warp reconvergence point
+// after every node, so the four groups execute each node step together (independent thread
+// scheduling would otherwise let them drift apart for good).
+__device__ __forceinline__ void run_net_group(char *base, const Shared &sh, const DevGrid &G, const DevForest &F,
+                                              const DevScratch &S, const AssignLaunch &a, int64_t net, int64_t n0,
+                                              int nn, int ns, int q_base, int gl) {
+    const int L = G.L, LD = a.LD;
+    const GNet n = group_net(base, group_layout(nn, ns, L, LD));
+    int64_t *tr = (a.trace && nn > 0) ? a.trace + 5 * net : nullptr;
+    if (tr && gl == 0) tr[0] = tr[1] = gtimer();
+    const int pdrv = nn > 0 ? F.net_pdrv[net] : 0;
+    group_gather(n, sh, G, F, n0, nn, ns, q_base, LD, gl, 8);
+    const int nmax = __reduce_max_sync(FULL_MASK, (unsigned)nn);
+    __syncwarp();
+    if (tr && gl == 0) tr[2] = gtimer();
+#pragma unroll 1
+    for (int i = 0; i < nmax; ++i) {
+        const bool act = i < nn;
+        if (act && n.nd[i].nkid > 0) group_vtable(n, i, L, gl);
+        __syncwarp();
+        if (act) group_step(n, sh, G, i, nn, pdrv, L, LD, gl);
+        __syncwarp();
+    }
+    if (gl == 0 && nn > 0) {
+        S.froot[net] = *n.froot;
+        group_backtrack(n, sh, nn, pdrv, LD);
+    }
+    __syncwarp();
+    group_emit(n, G, S, a, n0, nn, gl, 8);
+    if (tr && gl == 0) trace_end(tr);
+}
+
+// One big net by a team (a half-CTA or the CTA: nthr threads = nthr / 8 groups, named barrier
+// `bar`): gather, then each height level's nodes spread over the groups (one group per node, V
+// table per group), a team barrier between levels; backtrack by one thread; commit.
+__device__ __forceinline__ void run_net_team(char *base, const Shared &sh, const DevGrid &G, const DevForest &F,
+                                             const DevScratch &S, const AssignLaunch &a, int64_t net, int64_t n0,
+                                             int nn, int ns, int q_base, int tid, int nthr, int bar) {
+    const int L = G.L, LD = a.LD, T = nthr >> 3, gid = tid >> 3, gl = tid & 7;
+    GNet n = group_net(base, group_layout(nn, ns, L, LD, T));
+    n.Vt += gid * vt_elems(L);
+    int64_t *tr = a.trace ? a.trace + 5 * net : nullptr;
+    if (tr && tid == 0) tr[0] = tr[1] = gtimer();
+    const int pdrv = F.net_pdrv[net];
+    group_gather(n, sh, G, F, n0, nn, ns, q_base, LD, tid, nthr);
+    bar_sync(bar, nthr);
+    if (tr && tid == 0) tr[2] = gtimer();
+    const unsigned gm = 0xffu << (8 * ((threadIdx.x & 31) >> 3));
+    int lo = 0;
+    while (lo < nn) {
+        const int h = n.nd[lo].height;
+        int hi = lo + 1;
+        while (hi < nn && n.nd[hi].height == h) ++hi;
+#pragma unroll 1
+        for (int i = lo + gid; i < hi; i += T) {
+            if (n.nd[i].nkid > 0) {
+                group_vtable(n, i, L, gl);
+                __syncwarp(gm);
+            }
+            group_step(n, sh, G, i, nn, pdrv, L, LD, gl);
+            __syncwarp(gm);
+        }
+        bar_sync(bar, nthr);
+        lo = hi;
+    }
+    if (tid == 0) {
+        S.froot[net] = *n.froot;
+        group_backtrack(n, sh, nn, pdrv, LD);
+    }
+    bar_sync(bar, nthr);
+    group_emit(n, G, S, a, n0, nn, tid, nthr);
+    if (tr && tid == 0) trace_end(tr);
+}
+
 // ------------------------------------------------------------------ kernel --
 // Two register budgets of the same kernel: MINB = ASSIGN_CTAS_LAT (6 CTAs/SM, 80 registers) for
 // launches bound by their slowest net (fewer spills on the serial path), MINB = ASSIGN_CTAS_THR
@@ -709,8 +1235,11 @@ template <int MINB>
 __global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign(DevGrid G, DevForest F, DevScratch S, AssignLaunch a) {
     __shared__ Shared sh;
     __shared__ int64_t big_item[2];
+    __shared__ int big_gslot[2];
     extern __shared__ __align__(16) char dyn[];
     stage_tab(sh.T, G.tab);
+    if (threadIdx.x < 2 * MAXL) sh.lay_of[threadIdx.x / MAXL][threadIdx.x % MAXL] = 0;   // unused slots: layer 0
+    __syncthreads();
     if (threadIdx.x < MAXL) {
         const int l = threadIdx.x;
         sh.dir[l] = G.dir[l];
@@ -744,7 +1273,6 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign(DevGrid G, D
         const int htid = threadIdx.x & (gsz - 1), bar = split ? 1 + half : 0;
         const int nslots = split ? 2 : ASSIGN_WARPS;
         const int64_t n_work = a.big_end - a.big_beg;
-        char *gmine = a.gscratch ? a.gscratch + ((int64_t)blockIdx.x * 2 + half) * a.gslot_bytes : nullptr;
         for (;;) {
             bar_sync(bar, gsz);
             if (htid == 0) big_item[half] = (int64_t)atomicAdd(a.ticket + 1, 1ull);
@@ -758,9 +1286,21 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign(DevGrid G, D
             const int64_t net = rec.x, n0 = (uint32_t)rec.y;
             const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
             const NetLay lay = net_layout(nn, ns, L, LD);
-            char *base = lay.bytes <= nslots * slay.bytes ? dyn + (int64_t)half * nslots * slay.bytes : gmine;
+            char *base = dyn + (int64_t)half * nslots * slay.bytes;
+            const bool glob = lay.bytes > nslots * slay.bytes;
+            if (glob) {
+                // a pooled global slot, taken only once the net may start (dataflow: its
+                // predecessors are done), so a slot holder never waits on another net
+                if (htid == 0) {
+                    if (a.wait) wait_ready(a.wait, net);
+                    big_gslot[half] = gslot_acquire(a, blockIdx.x * 2 + half);
+                }
+                bar_sync(bar, gsz);
+                base = a.gscratch + (int64_t)big_gslot[half] * a.gslot_bytes;
+            }
             const NetCtx c{net_buf(base, lay), L, LD, nn};
             run_net<true>(c, w, sh, G, F, S, a, net, n0, q_base, ns, htid, gsz, bar);
+            if (glob && htid == 0) gslot_release(a, big_gslot[half]);
         }
     }
 
@@ -786,7 +1326,110 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign(DevGrid G, D
     }
 }
 
+// Batch mode kernel (la_assign_batch): every CTA first takes the batch's big nets (a half-CTA or
+// the whole CTA per net, wide-node DP as in k_assign), then each warp takes host-packed JOBS of
+// up to four nets that fit its arena, one 8-lane group per net (group path above).  Shared
+// memory: four warp arenas of a.warp_arena bytes; a big net uses its half's (or the CTA's)
+// arenas, with the wide-node scratch of its warps carved from the region's end.
+template <int MINB>
+__global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign_g(DevGrid G, DevForest F, DevScratch S,
+                                                                      AssignLaunch a) {
+    __shared__ Shared sh;
+    __shared__ int64_t big_item[2];
+    __shared__ int gslot_of[2];
+    extern __shared__ __align__(16) char dyn[];
+    stage_tab(sh.T, G.tab);
+    if (threadIdx.x < 2 * MAXL) sh.lay_of[threadIdx.x / MAXL][threadIdx.x % MAXL] = 0;   // unused slots: layer 0
+    __syncthreads();
+    if (threadIdx.x < MAXL) {
+        const int l = threadIdx.x;
+        sh.dir[l] = G.dir[l];
+        sh.routable[l] = G.routable[l];
+        sh.lidx[l] = (uint8_t)G.lidx[l];
+        if (l < G.L) sh.lay_of[G.dir[l]][G.lidx[l]] = (uint8_t)l;
+    }
+    if (threadIdx.x == 0) {
+        sh.ndir[0] = G.LH;
+        sh.ndir[1] = G.LV;
+        uint32_t m0 = 0, m1 = 0;
+        for (int l = 0; l < G.L; ++l)
+            if (G.routable[l]) (G.dir[l] == 0 ? m0 : m1) |= 1u << l;
+        sh.legal[0] = m0;
+        sh.legal[1] = m1;
+    }
+    __syncthreads();
+    const int L = G.L, LD = a.LD, WA = a.warp_arena;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    // ---------------- big nets: a team (half-CTA or CTA) per net, level-parallel groups ----------------
+    if (a.big_end > a.big_beg) {
+        const bool split = a.big_split != 0;
+        const int half = split ? warp >> 1 : 0, gsz = split ? 64 : 128, nw = gsz >> 5;
+        const int htid = threadIdx.x & (gsz - 1), bar = split ? 1 + half : 0;
+        char *region = dyn + (int64_t)half * 2 * WA;
+        const int cap = nw * WA;
+        const int64_t n_work = a.big_end - a.big_beg;
+        for (;;) {
+            bar_sync(bar, gsz);
+            if (htid == 0) big_item[half] = (int64_t)atomicAdd(a.ticket + 1, 1ull);
+            bar_sync(bar, gsz);
+            const int64_t wk = big_item[half];
+            if (wk >= n_work) break;
+            const int4 rec = a.big_pos[a.big_beg + wk];
+            const int64_t net = rec.x, n0 = (uint32_t)rec.y;
+            const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
+            char *base = region;
+            const bool glob = group_layout(nn, ns, L, LD, gsz >> 3).bytes > cap;
+            if (glob) {
+                if (htid == 0) gslot_of[half] = gslot_acquire(a, blockIdx.x * 2 + half);
+                bar_sync(bar, gsz);
+                base = a.gscratch + (int64_t)gslot_of[half] * a.gslot_bytes;
+            }
+            run_net_team(base, sh, G, F, S, a, net, n0, nn, ns, q_base, htid, gsz, bar);
+            if (glob && htid == 0) gslot_release(a, gslot_of[half]);
+        }
+    }
+
+    // ---------------- jobs: up to four nets per warp, one 8-lane group per net ----------------
+    char *arena = dyn + (int64_t)warp * WA;
+    const int g = lane >> 3, gl = lane & 7;
+    const int64_t n_work = a.job_end - a.job_beg;
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
+    tk = __shfl_sync(FULL_MASK, tk, 0);
+    for (;;) {
+        if ((int64_t)tk >= n_work) return;
+        const int4 job = a.jobs[a.job_beg + (int64_t)tk];   // {first small index, count, off1 | off2 << 16, off3}
+        unsigned long long tk_next = 0;
+        if (lane == 0) tk_next = atomicAdd(a.ticket, 1ull);
+        {
+            const bool have = g < job.y;
+            const int off = g == 0 ? 0 : g == 1 ? (job.z & 0xffff) : g == 2 ? ((uint32_t)job.z >> 16) : job.w;
+            const int4 rec = have ? a.small_pos[(int64_t)job.x + g] : make_int4(0, 0, 0, 0);
+            const int64_t net = rec.x, n0 = (uint32_t)rec.y;
+            const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
+            run_net_group(arena + off, sh, G, F, S, a, net, n0, nn, ns, q_base, gl);
+        }
+        __syncwarp();
+        tk = __shfl_sync(FULL_MASK, tk_next, 0);
+    }
+}
+
 }  // namespace
+
+size_t assign_group_net_bytes(int nodes, int sinks, int L, int LD) {
+    return (size_t)group_layout(nodes, sinks, L, LD).bytes;
+}
+
+size_t assign_team_net_bytes(int nodes, int sinks, int L, int LD) {   // a big net run by a whole CTA (16 groups)
+    return (size_t)group_layout(nodes, sinks, L, LD, 16).bytes;
+}
+
+size_t assign_warp_arena_bytes(int L, int LD) {
+    (void)L;
+    (void)LD;
+    return (size_t)G_WARP_ARENA;
+}
 
 size_t assign_smem_bytes(int L, int LD, int NS, int NP) {
     return (size_t)ASSIGN_WARPS * (net_layout(NS, NP, L, LD).bytes + scr_bytes(L, LD));
@@ -828,6 +1471,29 @@ static cudaError_t launch(const DevGrid &G, const DevForest &F, const DevScratch
         return cudaLaunchCooperativeKernel((const void *)k_assign<MINB>, dim3(grid), dim3(ASSIGN_WARPS * 32), args, smem, s);
     }
     k_assign<MINB><<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
+    return cudaGetLastError();
+}
+
+template <int MINB>
+static cudaError_t resident_g(size_t smem, int *per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(k_assign_g<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_assign_g<MINB>, ASSIGN_WARPS * 32, smem);
+}
+
+cudaError_t assign_g_resident_ctas(int L, int LD, int *per_sm_lat, int *per_sm_thr) {
+    const size_t smem = (size_t)ASSIGN_WARPS * assign_warp_arena_bytes(L, LD);
+    cudaError_t e = resident_g<G_CTAS_LAT>(smem, per_sm_lat);
+    if (e != cudaSuccess) return e;
+    return resident_g<G_CTAS_THR>(smem, per_sm_thr);
+}
+
+cudaError_t launch_assign_g(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
+                            bool throughput, cudaStream_t s) {
+    if ((a.job_end <= a.job_beg && a.big_end <= a.big_beg) || grid <= 0) return cudaSuccess;
+    const size_t smem = (size_t)ASSIGN_WARPS * a.warp_arena;
+    if (throughput) k_assign_g<G_CTAS_THR><<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
+    else k_assign_g<G_CTAS_LAT><<<(unsigned)grid, ASSIGN_WARPS * 32, smem, s>>>(G, F, S, a);
     return cudaGetLastError();
 }
 

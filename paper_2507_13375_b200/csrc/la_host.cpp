@@ -145,6 +145,16 @@ struct la_ctx {
     int32_t *d_succ = nullptr, *d_indeg = nullptr, *d_wait = nullptr;
     char *d_gscratch = nullptr;
     int64_t gslot_bytes = 0;
+    int32_t *d_glock = nullptr;               // lock per pooled global slot
+    int32_t n_gslots = 0;
+    int32_t warp_arena = 0;                   // k_assign_g shared memory per warp
+    int32_t grid_g = 0, grid_g_thr = 0;       // resident k_assign_g CTAs (latency / throughput variant)
+    bool group_path = true;                   // batch mode on k_assign_g (GAPLA_GROUP=0: k_assign)
+    std::vector<int4> h_jobs;                 // this rank's jobs (k_assign_g), batch by batch
+    std::vector<int64_t> batch_job0;          // [n_batches+1]
+    int4 *d_jobs = nullptr;
+    int64_t n_flow_big = 0, n_flow_small = 0; // dataflow role lists (k_assign's NS / NP roles)
+    int32_t n_big_ctas_flow = 0;              // big-net CTAs of the dataflow launch
     std::vector<int32_t> batch_of_net;        // input order
     std::vector<int32_t> h_big_pos, h_small_pos;
     DevForest F{};
@@ -172,7 +182,8 @@ struct la_ctx {
         cudaDeviceSynchronize();
         for (void *p : dev_allocs) dfree(p);
         void *gp[] = {d_wH, d_wV, d_via, d_wH0, d_wV0, d_via0, d_wcap, d_vcap, d_wire_off, d_Mpos, d_Mzero, d_tab,
-                      d_ticket, d_trace, d_eval, d_eval_lay, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch};
+                      d_ticket, d_trace, d_eval, d_eval_lay, d_succ_off, d_succ, d_indeg, d_wait, d_gscratch,
+                      d_glock};
         for (void *p : gp) if (p) dfree(p);
         if (comm) ncclCommDestroy(comm);
         for (auto &sp : spans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -901,7 +912,27 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     }
     if (const char *e = getenv("GAPLA_NS")) ctx->NS = std::max(1, std::min(1024, atoi(e)));   // tuning knobs
     if (const char *e = getenv("GAPLA_NP")) ctx->NP = std::max(1, std::min(4096, atoi(e)));
-    auto is_big = [&](int64_t net) { return nnodes_of(net) > ctx->NS || nsinks_of(net) > ctx->NP; };
+    // batch mode (k_assign_g): a net is "big" when its group-path state does not fit a warp's
+    // arena; the dataflow kernel (k_assign) re-classifies by its own slot (NS, NP)
+    ctx->warp_arena = (int32_t)assign_warp_arena_bytes(ctx->L, ctx->LD);
+    if (const char *e = getenv("GAPLA_GROUP")) ctx->group_path = atoi(e) != 0;
+    auto is_big_flow = [&](int64_t net) { return nnodes_of(net) > ctx->NS || nsinks_of(net) > ctx->NP; };
+    // small nets (one 8-lane group each, four per warp) up to nmax nodes; larger nets run
+    // level-parallel on a team of groups (DESIGN §5 "group path").  nmax is per batch: a batch
+    // with many nets per resident warp is throughput-bound and keeps nets up to group_nmax_thr
+    // nodes on the (more efficient) group path; a smaller batch is bound by its slowest net and
+    // sends nets above group_nmax_lat nodes to the (lower-latency) team path.
+    int64_t group_nmax_lat = 8, group_nmax_thr = 24;
+    if (const char *e = getenv("GAPLA_GROUP_NMAX")) group_nmax_lat = group_nmax_thr = std::max(1, std::min(65535, atoi(e)));
+    if (const char *e = getenv("GAPLA_GROUP_NMAX_LAT")) group_nmax_lat = std::max(1, std::min(65535, atoi(e)));
+    if (const char *e = getenv("GAPLA_GROUP_NMAX_THR")) group_nmax_thr = std::max(1, std::min(65535, atoi(e)));
+    std::vector<int32_t> nmax_of_batch;       // filled once the batches are known
+    auto is_big = [&](int64_t net, int32_t b) {
+        if (!ctx->group_path) return is_big_flow(net);
+        return nnodes_of(net) > nmax_of_batch[b] ||
+               assign_group_net_bytes((int)nnodes_of(net), (int)nsinks_of(net), ctx->L, ctx->LD) >
+                   (size_t)ctx->warp_arena;
+    };
     for (int64_t net = 0; net < N; net++)
         if (nnodes_of(net) >= 65535 || nsinks_of(net) >= 65535)
             return set_err(LA_EINVAL, "net " + std::to_string(net) + ": more than 65534 LA-tree nodes or sinks");
@@ -1034,6 +1065,18 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         ctx->batch_net0.assign(cnt.begin(), cnt.end());
         std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
         for (int64_t r = 0; r < N; r++) pos_net[cur[batch_of_rank[r]]++] = by_rank[r];
+        {
+            int lat = 0, thr = 0, n_sm = 0;
+            CK(assign_g_resident_ctas(ctx->L, ctx->LD, &lat, &thr));
+            CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device));
+            int64_t per_warp = 8;
+            if (const char *e = getenv("GAPLA_NMAX_NETS_PER_WARP")) per_warp = std::max(1, atoi(e));
+            const int64_t warps = (int64_t)std::max(1, thr * n_sm) * ASSIGN_WARPS;
+            nmax_of_batch.resize(std::max(nb, 1));
+            for (int32_t b = 0; b < nb; b++)
+                nmax_of_batch[b] = (int32_t)((cnt[b + 1] - cnt[b]) > per_warp * warps * ctx->world ? group_nmax_thr
+                                                                                                   : group_nmax_lat);
+        }
         // big nets (CTA path) first, then by node count descending, then rank: the longest nets
         // start first.  Key per position: !big | (65535 - nodes) | offset in the batch (rank order).
         std::atomic<int32_t> nxt{0};
@@ -1046,7 +1089,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                 kk.resize(p1 - p0);
                 for (int64_t p = p0; p < p1; p++) {
                     const int64_t net = pos_net[p];
-                    kk[p - p0] = ((uint64_t)(is_big(net) ? 0 : 1) << 63) | ((uint64_t)(65535 - nn_of[net]) << 40) |
+                    kk[p - p0] = ((uint64_t)(is_big(net, b) ? 0 : 1) << 63) | ((uint64_t)(65535 - nn_of[net]) << 40) |
                                  (uint64_t)(p - p0);
                 }
                 std::sort(kk.begin(), kk.end());
@@ -1069,7 +1112,10 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     ctx->batch_big0.assign(1, 0);
     ctx->batch_small0.assign(1, 0);
     std::vector<uint8_t> big_at(N);
-    par_for(N, nthr, [&](int64_t p) { big_at[p] = is_big(pos_net[p]) ? 1 : 0; });
+    par_for(N, nthr, [&](int64_t p) {
+        const int64_t net = pos_net[p];
+        big_at[p] = is_big(net, ctx->batch_of_net[net]) ? 1 : 0;
+    });
     for (int32_t b = 0; b < nb; b++) {
         for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++) {
             if (big_at[p]) {
@@ -1079,6 +1125,11 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                 max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
             } else {
                 small_pos.push_back((int32_t)p);
+                const int64_t net = pos_net[p];
+                if (is_big_flow(net)) {   // a big net of the dataflow kernel (k_assign)
+                    max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
+                    max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
+                }
             }
         }
         ctx->batch_big0.push_back((int64_t)big_pos.size());
@@ -1248,6 +1299,45 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         phase("  (pack_nets)");
         TRY(dev_upload(ctx, &ctx->d_big_pos, ib.data(), ib.size()));
         TRY(dev_upload(ctx, &ctx->d_small_pos, is.data(), is.size()));
+        // k_assign_g jobs (DESIGN §5 "group path"): this rank's share of each batch's small
+        // nets, in list order (nodes descending), up to four consecutive nets whose group
+        // states fit one warp arena together
+        {
+            int lat = 0, thr = 0;
+            CK(assign_g_resident_ctas(ctx->L, ctx->LD, &lat, &thr));
+            if (lat < 1 || thr < 1) return set_err(LA_ECUDA, "k_assign_g does not fit on an SM");
+            ctx->grid_g = lat * n_sm;
+            ctx->grid_g_thr = thr * n_sm;
+            ctx->h_jobs.clear();
+            ctx->batch_job0.assign(1, 0);
+            const int WA = ctx->warp_arena;
+            for (int32_t b = 0; b < nb && ctx->group_path; b++) {
+                const int64_t m0 = ctx->batch_small0[b], m1 = ctx->batch_small0[b + 1];
+                int64_t s0 = 0, s1 = 0;
+                la_shard_range(m1 - m0, ctx->world, ctx->rank, &s0, &s1);
+                int4 cur{0, 0, 0, 0};
+                int used = 0;
+                for (int64_t idx = m0 + s0; idx < m0 + s1; idx++) {
+                    const int32_t p = small_pos[idx];
+                    const int bytes = (int)assign_group_net_bytes((int)(node0[p + 1] - node0[p]),
+                                                                  (int)(sink0g[p + 1] - sink0g[p]), ctx->L, ctx->LD);
+                    if (cur.y == 4 || (cur.y > 0 && used + bytes > WA)) {
+                        ctx->h_jobs.push_back(cur);
+                        cur = int4{0, 0, 0, 0};
+                        used = 0;
+                    }
+                    if (cur.y == 0) cur.x = (int32_t)idx;
+                    else if (cur.y == 1) cur.z = used;
+                    else if (cur.y == 2) cur.z |= used << 16;
+                    else cur.w = used;
+                    cur.y++;
+                    used += bytes;
+                }
+                if (cur.y) ctx->h_jobs.push_back(cur);
+                ctx->batch_job0.push_back((int64_t)ctx->h_jobs.size());
+            }
+            if (ctx->group_path) TRY(dev_upload(ctx, &ctx->d_jobs, ctx->h_jobs.data(), ctx->h_jobs.size()));
+        }
         // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
         ctx->n_big_ctas = big_pos.empty() ? 0 : n_sm;
         if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas = std::max(0, atoi(e));
@@ -1256,12 +1346,22 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (const char *e = getenv("GAPLA_BIG_SPLIT")) ctx->big_split = atoi(e);
         CK(dmalloc(&ctx->d_wait, sizeof(int32_t) * std::max<int64_t>(N, 1)));
         if (N) CK(cudaMemcpyAsync(ctx->d_wait, ctx->d_indeg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
-        // a big net keeps its DP state in its CTA's shared memory, or in a per-CTA global slot
-        const size_t need = assign_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD);
+        // a big net keeps its DP state in its half-CTA's shared memory, or in a global slot taken
+        // from a pool: one slot per half-CTA up to a byte budget (GAPLA_GSLOT_MB, default 1024)
+        const size_t need = std::max(assign_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD),
+                                     assign_team_net_bytes((int)max_big_nodes, (int)max_big_sinks, ctx->L, ctx->LD));
         ctx->gslot_bytes = 0;
-        if (max_big_nodes > 0 && need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP)) {
+        if (max_big_nodes > 0 && (need > assign_cta_net_bytes(ctx->L, ctx->LD, ctx->NS, ctx->NP) ||
+                                  need > (size_t)2 * ctx->warp_arena)) {
             ctx->gslot_bytes = (int64_t)((need + 255) & ~(size_t)255);
-            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * std::max(ctx->grid, ctx->grid_thr) * 2));   // per half-CTA
+            int64_t budget = (int64_t)1024 << 20;
+            if (const char *e = getenv("GAPLA_GSLOT_MB")) budget = std::max<int64_t>(1, atoll(e)) << 20;
+            const int64_t halves = 2 * (int64_t)std::max(std::max(ctx->grid, ctx->grid_thr),
+                                                         std::max(ctx->grid_g, ctx->grid_g_thr));
+            ctx->n_gslots = (int32_t)std::max<int64_t>(1, std::min<int64_t>(halves, budget / ctx->gslot_bytes));
+            CK(dmalloc(&ctx->d_gscratch, (size_t)ctx->gslot_bytes * ctx->n_gslots));
+            CK(dmalloc(&ctx->d_glock, sizeof(int32_t) * ctx->n_gslots));
+            CK(cudaMemsetAsync(ctx->d_glock, 0, sizeof(int32_t) * ctx->n_gslots, ctx->stream));
         }
     }
     CK(cudaMemsetAsync(S.froot, 0, sizeof(double) * std::max<int64_t>(N, 1), ctx->stream));
@@ -1339,9 +1439,27 @@ static int launch_grid(const la_ctx *ctx, AssignLaunch &al, bool *thr) {
         return (int)std::min<int64_t>(gmax, std::max<int64_t>(nbig, (nsmall + npc - 1) / npc));
     }
     al.hybrid = 0;
-    al.n_big_ctas = (int32_t)std::min<int64_t>(ctx->n_big_ctas, nbig);
-    const int64_t small_ctas = std::min<int64_t>(gmax - ctx->n_big_ctas, (nsmall + npc - 1) / npc);
+    const int32_t nbc = al.wait ? ctx->n_big_ctas_flow : ctx->n_big_ctas;
+    al.n_big_ctas = (int32_t)std::min<int64_t>(nbc, nbig);
+    const int64_t small_ctas = std::min<int64_t>(gmax - nbc, (nsmall + npc - 1) / npc);
     return al.n_big_ctas + (int)small_ctas;
+}
+
+// Grid of one k_assign_g launch: enough CTAs for the big nets and the jobs (four warps per CTA),
+// at most the resident grid of the variant; the 7-CTA/SM variant for launches of many jobs per
+// resident warp (GAPLA_THR_JOBS_PER_WARP, default 4), the 6-CTA/SM one for tail-bound launches.
+static int launch_grid_g(const la_ctx *ctx, AssignLaunch &al, bool *thr) {
+    const int64_t nbig = al.big_end - al.big_beg, njobs = al.job_end - al.job_beg;
+    const bool busy = nbig + njobs > (int64_t)4 * ctx->grid_g * ASSIGN_WARPS;
+    al.big_split = ctx->big_split >= 0 ? ctx->big_split : (busy ? 1 : 0);
+    int64_t per_warp = 4;
+    if (const char *e = getenv("GAPLA_THR_JOBS_PER_WARP")) per_warp = std::max(1, atoi(e));
+    const bool wide = nbig + njobs > per_warp * ctx->grid_g * ASSIGN_WARPS;
+    *thr = ctx->assign_variant >= 0 ? ctx->assign_variant == 1 : wide;
+    const int gmax = *thr ? ctx->grid_g_thr : ctx->grid_g;
+    al.hybrid = 1;
+    al.n_big_ctas = 0;
+    return (int)std::min<int64_t>(gmax, std::max<int64_t>(nbig, (njobs + ASSIGN_WARPS - 1) / ASSIGN_WARPS));
 }
 
 static AssignLaunch assign_launch(const la_ctx *ctx) {
@@ -1350,6 +1468,10 @@ static AssignLaunch assign_launch(const la_ctx *ctx) {
     al.small_pos = ctx->d_small_pos;
     al.gscratch = ctx->d_gscratch;
     al.gslot_bytes = ctx->gslot_bytes;
+    al.glock = ctx->d_glock;
+    al.n_gslots = ctx->n_gslots;
+    al.jobs = ctx->d_jobs;
+    al.warp_arena = ctx->warp_arena;
     al.NS = ctx->NS;
     al.NP = ctx->NP;
     al.LD = ctx->LD;
@@ -1372,9 +1494,17 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     al.big_beg = r.big_beg; al.big_end = r.big_end; al.small_beg = r.small_beg; al.small_end = r.small_end;
     al.ticket = ctx->d_ticket + 2 * (1 + batch);
     bool thr = false;
-    const int grid = launch_grid(ctx, al, &thr);
+    int grid = 0;
     int pi = prof_begin(ctx, K_ASSIGN);
-    CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, thr, ctx->stream));
+    if (ctx->group_path) {
+        al.job_beg = ctx->batch_job0[batch];
+        al.job_end = ctx->batch_job0[batch + 1];
+        grid = launch_grid_g(ctx, al, &thr);
+        CK(launch_assign_g(ctx->G, ctx->F, ctx->S, al, grid, thr, ctx->stream));
+    } else {
+        grid = launch_grid(ctx, al, &thr);
+        CK(launch_assign(ctx->G, ctx->F, ctx->S, al, grid, thr, ctx->stream));
+    }
     prof_end(ctx, pi);
     if (grid > 0) ctx->stats.launches += 1;
     ctx->pending_commit = true;
@@ -1500,8 +1630,23 @@ static la_status build_flow_lists(la_ctx *ctx) {
     if (off[N])
         CK(cudaMemcpyAsync(succ.data(), ctx->d_succ, sizeof(int32_t) * off[N], cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    // the dataflow kernel's own roles: big = more than NS nodes or NP sinks (its warp slot)
     std::vector<uint8_t> big(N, 0);
-    for (int32_t p : ctx->h_big_pos) big[p] = 1;
+    std::vector<int32_t> fb, fs;
+    for (int64_t p = 0; p < N; p++) {
+        big[p] = (ctx->h_net_node0[p + 1] - ctx->h_net_node0[p] > ctx->NS ||
+                  ctx->h_net_sink0[p + 1] - ctx->h_net_sink0[p] > ctx->NP) ? 1 : 0;
+        (big[p] ? fb : fs).push_back((int32_t)p);
+    }
+    ctx->n_flow_big = (int64_t)fb.size();
+    ctx->n_flow_small = (int64_t)fs.size();
+    {   // big-net CTAs of the dataflow launch: one per SM by default (GAPLA_BIG_CTAS overrides)
+        int n_sm = 0;
+        CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device));
+        ctx->n_big_ctas_flow = fb.empty() ? 0 : n_sm;
+        if (const char *e = getenv("GAPLA_BIG_CTAS")) ctx->n_big_ctas_flow = std::max(0, atoi(e));
+        if (!fb.empty()) ctx->n_big_ctas_flow = std::max(1, std::min(ctx->n_big_ctas_flow, ctx->grid - 1));
+    }
     std::vector<int64_t> bl(N);
     for (int64_t p = N - 1; p >= 0; p--) {
         const int64_t nn = ctx->h_net_node0[p + 1] - ctx->h_net_node0[p];
@@ -1510,7 +1655,6 @@ static la_status build_flow_lists(la_ctx *ctx) {
         bl[p] = m + 8 + (big[p] ? nn / 4 : nn);
     }
     auto by_prio = [&](int32_t a, int32_t c) { return bl[a] != bl[c] ? bl[a] > bl[c] : a < c; };
-    std::vector<int32_t> fb = ctx->h_big_pos, fs = ctx->h_small_pos;
     const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     par_sort(fb, by_prio, nthr);
     par_sort(fs, by_prio, nthr);
@@ -1536,9 +1680,9 @@ la_status la_assign_all(la_ctx *ctx) {
         al.big_pos = ctx->d_flow_big_pos;
         al.small_pos = ctx->d_flow_small_pos;
         al.big_beg = 0;
-        al.big_end = (int64_t)ctx->h_big_pos.size();
+        al.big_end = ctx->n_flow_big;
         al.small_beg = 0;
-        al.small_end = (int64_t)ctx->h_small_pos.size();
+        al.small_end = ctx->n_flow_small;
         al.ticket = ctx->d_ticket;
         al.wait = ctx->d_wait;
         al.succ_off = ctx->d_succ_off;

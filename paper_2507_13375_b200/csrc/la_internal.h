@@ -94,6 +94,18 @@ constexpr int ASSIGN_WARPS = 4;
 #ifndef ASSIGN_CTAS_LAT
 #define ASSIGN_CTAS_LAT 6                   // k_assign CTAs per SM, latency-bound launches (80 registers)
 #endif
+// k_assign_g: 4 CTAs of 4 warps per SM (128 registers: the group path's per-slot cost' values
+// stay in registers) and a 13 KB shared-memory arena per warp (measured: 6-7 CTAs/SM spill and
+// run cfg5 at 103-119 ms, 5 at 94 ms, 4 at 87 ms, 3 at 99 ms; profiles/r02_*)
+#ifndef G_CTAS_LAT
+#define G_CTAS_LAT 4                        // k_assign_g CTAs per SM, latency-bound launches
+#endif
+#ifndef G_CTAS_THR
+#define G_CTAS_THR 4                        // k_assign_g CTAs per SM, throughput-bound launches
+#endif
+#ifndef G_WARP_ARENA
+#define G_WARP_ARENA 13312                  // k_assign_g shared-memory bytes per warp
+#endif
 #ifndef ASSIGN_CTAS_THR
 #define ASSIGN_CTAS_THR 7                   // k_assign CTAs per SM, throughput-bound launches (72 registers)
 #endif
@@ -132,8 +144,20 @@ struct AssignLaunch {
     int32_t LD;                               // max(#H layers, #V layers): layer slots per direction
     int32_t commit;                           // fuse the demand commit (K8) into the kernel
     int64_t *trace;                           // diagnostics: [n_nets][5] per-net timestamps, or nullptr
+    // k_assign_g (batch mode): jobs of up to four small nets, one 8-lane group per net
+    const int4 *jobs;                         // {first small_pos index, count, off1 | off2 << 16, off3}
+    int64_t job_beg, job_end;
+    int32_t warp_arena;                       // shared-memory bytes per warp (group arena)
+    int32_t *glock;                           // lock per pooled global slot of a big net
+    int32_t n_gslots;
 };
 size_t assign_smem_bytes(int L, int LD, int NS, int NP);
+size_t assign_group_net_bytes(int nodes, int sinks, int L, int LD);   // one net's state on the group path
+size_t assign_warp_arena_bytes(int L, int LD);                         // per-warp shared memory of k_assign_g
+size_t assign_team_net_bytes(int nodes, int sinks, int L, int LD);    // a big net's state on k_assign_g (upper bound)
+cudaError_t assign_g_resident_ctas(int L, int LD, int *per_sm_lat, int *per_sm_thr);
+cudaError_t launch_assign_g(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
+                            bool throughput, cudaStream_t s);
 size_t assign_net_bytes(int nodes, int sinks, int L, int LD);
 int assign_nets_per_cta();
 size_t assign_cta_net_bytes(int L, int LD, int NS, int NP);   // shared memory a big net may use

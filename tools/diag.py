@@ -121,10 +121,13 @@ if os.environ.get("DIAG_PERNET"):
     nv = np.diff(sol["via_ptr"])
     g = (t[:, 2] - t[:, 1]) / 1e3
     dp = (t[:, 3] - t[:, 2]) / 1e3
-    for w in sorted(set(nw.tolist()))[:12]:
-        m = nw == w
-        print(f"    {w:3d} wires: {m.sum():6d} nets gather {np.median(g[m]):7.1f} us  dp+commit p50 {np.median(dp[m]):7.1f} "
-              f"max {dp[m].max():7.1f} us", flush=True)
+    for lo, hi in ((1, 2), (2, 3), (3, 4), (4, 6), (6, 9), (9, 13), (13, 20), (20, 30), (30, 50), (50, 80), (80, 120),
+                   (120, 100000)):
+        m = (nw >= lo) & (nw < hi)
+        if not m.any():
+            continue
+        print(f"    wires [{lo:3d},{hi:3d}): {m.sum():7d} nets gather p50 {np.median(g[m]):7.1f} us  dp+commit p50 "
+              f"{np.median(dp[m]):7.1f} p90 {np.percentile(dp[m], 90):7.1f} max {dp[m].max():7.1f} us", flush=True)
     A.close()
 
 if os.environ.get("DIAG_NCU"):
