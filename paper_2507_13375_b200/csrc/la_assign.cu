@@ -895,9 +895,41 @@ __device__ __forceinline__ int son_argmin(const Shared &sh, const double2 *ac, d
     return jm;
 }
 
-// Node i of the group's net, entry layer l (lane's slot e; the root: l = p_drv, slot 0).
+// Reduction of a candidate (G', key) over the P parts of an entry (lanes part * 8 + e).
+template <int P>
+__device__ __forceinline__ void reduce_best(double &g, uint32_t &key) {
+    if constexpr (P > 1) {
+#pragma unroll
+        for (int o = 8; o < 8 * P; o <<= 1) {
+            const double og = __shfl_xor_sync(FULL_MASK, g, o);
+            const uint32_t ok = __shfl_xor_sync(FULL_MASK, key, o);
+            if (og < g || (og == g && ok < key)) { g = og; key = ok; }
+        }
+    }
+}
+
+// Reduction of a son's window argmin (value, layer) over the P parts: the lowest layer among the minima.
+template <int P>
+__device__ __forceinline__ void reduce_argmin(double &m, int &j) {
+    if constexpr (P > 1) {
+#pragma unroll
+        for (int o = 8; o < 8 * P; o <<= 1) {
+            const double om = __shfl_xor_sync(FULL_MASK, m, o);
+            const int oj = __shfl_xor_sync(FULL_MASK, j, o);
+            if (om < m || (om == m && oj < j)) { m = om; j = oj; }
+        }
+    }
+}
+
+// Node i, entry layer l (slot e; the root: l = p_drv, slot 0).  P = 1: one lane per entry (the
+// small-net path; the caller passes only active lanes).  P = 4: a whole warp per node (big nets),
+// lane = part * 8 + e; the parts split the son-layer slots of the combination search (slot s in
+// part s % P) and reduce by the same total orders, so the choice is the P = 1 one; every lane
+// calls (act = an entry of the node), part 0 writes.
+template <int P>
 __device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, const GNet &n, int i, bool root,
-                                           int l, int e, int L, int LD, double *froot) {
+                                           int l, int e, int part, bool act, int L, int LD, double *froot) {
+    constexpr int NSP = MAXE / P;                       // son-layer slots per part
     const NodeG &r = n.nd[i];
     const int nk = r.nkid;
     // pin terms, sinks in input order (Alg. 3 l.4-7)
@@ -931,32 +963,33 @@ __device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, c
         const double w0 = n.nd[k0].wd, w1 = n.nd[k1].wd;
         const double2 *ac0 = n.AC + k0 * LD, *ac1 = n.AC + k1 * LD;
         if (nk == 1) {
-            // son-layer combinations (header), all slots at once: cost' per slot in registers,
-            // independent loads and evaluations, then a compare chain in ascending slot order
-            double c0[MAXE];
+            // son-layer combinations (header): cost' per slot in registers, independent loads and
+            // evaluations, then a compare chain in ascending slot order
+            double c0[NSP];
             const int n0 = sh.ndir[d0];
             double bestG = dinf();
 #pragma unroll
-            for (int s = 0; s < MAXE; ++s) {
+            for (int k = 0; k < NSP; ++k) {
+                const int s = part + k * P;
                 const int j = sh.lay_of[d0][s];
-                c0[s] = s < n0 ? cost_p(ac0[s], w0, VRl[j], urn) : dinf();
+                c0[k] = s < n0 ? cost_p(ac0[s], w0, VRl[j], urn) : dinf();
                 const int bb = min(b0, j), tt = max(t0, j);
-                const double g = n.Vt[vtri(bb, tt, L)] + c0[s];
+                const double g = n.Vt[vtri(bb, tt, L)] + c0[k];
                 const uint32_t kk = (uint32_t)(((tt - bb) << 4) | bb);
-                if (c0[s] < dinf() && (g < bestG || (g == bestG && kk < key))) { bestG = g; key = kk; }
+                if (c0[k] < dinf() && (g < bestG || (g == bestG && kk < key))) { bestG = g; key = kk; }
             }
-            if (!(key & 0x100u)) {
-                bw = key & 0xf;
-                tw = bw + (int)((key >> 4) & 0xf);
-                double m = dinf();
-                int jm = 0;
+            reduce_best<P>(bestG, key);
+            bw = key & 0xf;
+            tw = bw + (int)((key >> 4) & 0xf);
+            double m = dinf();
+            int jm = MAXL;
 #pragma unroll
-                for (int s = 0; s < MAXE; ++s) {        // the son's lowest-layer window argmin (R21)
-                    const int j = sh.lay_of[d0][s];
-                    if (j >= bw && j <= tw && c0[s] < m) { m = c0[s]; jm = j; }
-                }
-                js = (uint32_t)jm;
+            for (int k = 0; k < NSP; ++k) {                 // the son's lowest-layer window argmin (R21)
+                const int j = sh.lay_of[d0][part + k * P];
+                if (j >= bw && j <= tw && c0[k] < m) { m = c0[k]; jm = j; }
             }
+            reduce_argmin<P>(m, jm);
+            js = (uint32_t)jm & 0xf;
         } else if (nk == 2) {
             // son-layer combinations; son 1's cost' per slot in registers, son 0 per outer step
             double c1[MAXE];
@@ -965,7 +998,7 @@ __device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, c
             for (int s = 0; s < MAXE; ++s) c1[s] = s < n1 ? cost_p(ac1[s], w1, VRl[sh.lay_of[d1][s]], urn) : dinf();
             double bestG = dinf();
 #pragma unroll 1
-            for (int s0 = 0; s0 < n0; ++s0) {
+            for (int s0 = part; s0 < n0; s0 += P) {
                 const int j0 = sh.lay_of[d0][s0];
                 const double c0 = cost_p(ac0[s0], w0, VRl[j0], urn);
                 if (!(c0 < dinf())) continue;
@@ -979,24 +1012,36 @@ __device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, c
                     if (c1[s1] < dinf() && (g < bestG || (g == bestG && kk < key))) { bestG = g; key = kk; }
                 }
             }
-            if (!(key & 0x100u)) {
-                bw = key & 0xf;
-                tw = bw + (int)((key >> 4) & 0xf);
-                js = (uint32_t)son_argmin(sh, ac0, w0, d0, VRl, urn, bw, tw);
-                double m = dinf();
-                int jm = 0;
+            reduce_best<P>(bestG, key);
+            bw = key & 0xf;
+            tw = bw + (int)((key >> 4) & 0xf);
+            double m = dinf();
+            int jm = MAXL;
 #pragma unroll
-                for (int s = 0; s < MAXE; ++s) {
-                    const int j = sh.lay_of[d1][s];
-                    if (j >= bw && j <= tw && c1[s] < m) { m = c1[s]; jm = j; }
+            for (int k = 0; k < NSP; ++k) {                 // son 0's window argmin over this part's slots
+                const int s = part + k * P;
+                const int j = sh.lay_of[d0][s];
+                if (s < n0 && j >= bw && j <= tw) {
+                    const double cp = cost_p(ac0[s], w0, VRl[j], urn);
+                    if (cp < m) { m = cp; jm = j; }
                 }
-                js |= (uint32_t)jm << 4;
             }
+            reduce_argmin<P>(m, jm);
+            js = (uint32_t)jm & 0xf;
+            m = dinf();
+            jm = 0;
+#pragma unroll
+            for (int s = 0; s < MAXE; ++s) {
+                const int j = sh.lay_of[d1][s];
+                if (j >= bw && j <= tw && c1[s] < m) { m = c1[s]; jm = j; }
+            }
+            js |= (uint32_t)jm << 4;
         } else {
             key = group_sweep(sh, n, i, l, b0, t0, L, LD, &js);
             bw = key & 0xf;
             tw = bw + (int)((key >> 4) & 0xf);
         }
+        if (!act || part != 0) return;
         if (key & 0x100u) {                             // no feasible span (cannot happen when every
             if (root) *froot = dinf();                  // direction has a routable layer; kept exact)
             else n.AC[i * LD + e].x = dinf();
@@ -1014,6 +1059,7 @@ __device__ __forceinline__ void group_node(const Shared &sh, const DevGrid &G, c
                 K = K + ac.y;
             }
     }
+    if (!act || part != 0) return;
     const double f = F0 + Gv;
     const double dlc = C0 + K;
     n.dec[i * LD + e] = (uint32_t)(bw | (tw << 4)) | (js << 8);
@@ -1109,17 +1155,19 @@ __device__ __forceinline__ void group_vtable(const GNet &n, int i, int L, int gl
     }
 }
 
-// Node i by one group: lanes over the entry layers of its parent edge (the root: l = p_drv).
+// Node i: P = 1, one group (lanes gl = entry slots); P = 4, a whole warp (lane = part * 8 + entry).
+template <int P>
 __device__ __forceinline__ void group_step(const GNet &n, const Shared &sh, const DevGrid &G, int i, int nn, int pdrv,
-                                           int L, int LD, int gl) {
+                                           int L, int LD, int lane) {
+    const int e = lane & 7, part = P > 1 ? (lane >> 3) : 0;
     const bool root = i == nn - 1;
     const int ed = n.nd[i].edir;
     const int dt = ed <= 1 ? 0 : 1;
     const int nE = root ? 1 : sh.ndir[dt];
-    if (gl < nE) {
-        const int l = root ? pdrv : sh.lay_of[dt][gl];
-        if (root || sh.routable[l]) group_node(sh, G, n, i, root, l, gl, L, LD, n.froot);
-    }
+    const int l = root ? pdrv : sh.lay_of[dt][e];
+    const bool act = e < nE && (root || sh.routable[l]);
+    if (P == 1 && !act) return;
+    group_node<P>(sh, G, n, i, root, act ? l : 0, e, part, act, L, LD, n.froot);
 }
 
 // Alg. 4 backtrack from the root (entry = driver pin layer, R13) by one thread: parents precede
@@ -1173,7 +1221,7 @@ __device__ __forceinline__ void run_net_group(char *base, const Shared &sh, cons
         const bool act = i < nn;
         if (act && n.nd[i].nkid > 0) group_vtable(n, i, L, gl);
         __syncwarp();
-        if (act) group_step(n, sh, G, i, nn, pdrv, L, LD, gl);
+        if (act) group_step<1>(n, sh, G, i, nn, pdrv, L, LD, gl);
         __syncwarp();
     }
     if (gl == 0 && nn > 0) {
@@ -1185,35 +1233,44 @@ __device__ __forceinline__ void run_net_group(char *base, const Shared &sh, cons
     if (tr && gl == 0) trace_end(tr);
 }
 
-// One big net by a team (a half-CTA or the CTA: nthr threads = nthr / 8 groups, named barrier
-// `bar`): gather, then each height level's nodes spread over the groups (one group per node, V
-// table per group), a team barrier between levels; backtrack by one thread; commit.
+// One big net by a team (a half-CTA or the CTA: nthr threads = nthr / 32 warps, named barrier
+// `bar`): gather, then each height level's nodes spread over the warps (a whole warp per node:
+// group_node<4>, V table per warp), a team barrier between levels; backtrack by one thread; commit.
 __device__ __forceinline__ void run_net_team(char *base, const Shared &sh, const DevGrid &G, const DevForest &F,
                                              const DevScratch &S, const AssignLaunch &a, int64_t net, int64_t n0,
                                              int nn, int ns, int q_base, int tid, int nthr, int bar) {
-    const int L = G.L, LD = a.LD, T = nthr >> 3, gid = tid >> 3, gl = tid & 7;
+    const int L = G.L, LD = a.LD, T = nthr >> 5, wid = tid >> 5, lane = tid & 31;
     GNet n = group_net(base, group_layout(nn, ns, L, LD, T));
-    n.Vt += gid * vt_elems(L);
+    n.Vt += wid * vt_elems(L);
     int64_t *tr = a.trace ? a.trace + 5 * net : nullptr;
     if (tr && tid == 0) tr[0] = tr[1] = gtimer();
     const int pdrv = F.net_pdrv[net];
     group_gather(n, sh, G, F, n0, nn, ns, q_base, LD, tid, nthr);
     bar_sync(bar, nthr);
     if (tr && tid == 0) tr[2] = gtimer();
-    const unsigned gm = 0xffu << (8 * ((threadIdx.x & 31) >> 3));
     int lo = 0;
     while (lo < nn) {
         const int h = n.nd[lo].height;
         int hi = lo + 1;
         while (hi < nn && n.nd[hi].height == h) ++hi;
 #pragma unroll 1
-        for (int i = lo + gid; i < hi; i += T) {
-            if (n.nd[i].nkid > 0) {
-                group_vtable(n, i, L, gl);
-                __syncwarp(gm);
+        for (int i = lo + wid; i < hi; i += T) {
+            if (n.nd[i].nkid > 0) {        // V(b, t) table of node i, lane b sums row b ascending (R10, R23)
+                if (lane < L) {
+                    const double *kp = n.kap + i * (L - 1);
+                    double *row = n.Vt + vtri(lane, lane, L);
+                    double V = 0.0;
+                    row[0] = V;
+#pragma unroll 1
+                    for (int t = lane + 1; t < L; ++t) {
+                        V = V + kp[t - 1];
+                        row[t - lane] = V;
+                    }
+                }
+                __syncwarp();
             }
-            group_step(n, sh, G, i, nn, pdrv, L, LD, gl);
-            __syncwarp(gm);
+            group_step<4>(n, sh, G, i, nn, pdrv, L, LD, lane);
+            __syncwarp();
         }
         bar_sync(bar, nthr);
         lo = hi;
@@ -1379,7 +1436,7 @@ __global__ void __launch_bounds__(ASSIGN_WARPS * 32, MINB) k_assign_g(DevGrid G,
             const int64_t net = rec.x, n0 = (uint32_t)rec.y;
             const int nn = rec.z & 0xffff, ns = (int)((uint32_t)rec.z >> 16), q_base = rec.w;
             char *base = region;
-            const bool glob = group_layout(nn, ns, L, LD, gsz >> 3).bytes > cap;
+            const bool glob = group_layout(nn, ns, L, LD, gsz >> 5).bytes > cap;
             if (glob) {
                 if (htid == 0) gslot_of[half] = gslot_acquire(a, blockIdx.x * 2 + half);
                 bar_sync(bar, gsz);
