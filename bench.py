@@ -123,17 +123,18 @@ def algorithmic_bytes(st, L, n_nets, via_cuts=None):
     return assign, commit, elmore
 
 
-def ncu_traffic(workload):
-    """dram bytes per k_assign launch from the committed ncu summary (profiles/), if it matches."""
+def ncu_summary(workload):
+    """The committed ncu summary of the k_assign launches (profiles/ncu_k_assign_summary.json) if it
+    matches the workload: dram bytes per launch, FP64-pipe activity, source files."""
     p = os.path.join(ROOT, "profiles", "ncu_k_assign_summary.json")
     try:
         with open(p) as f:
             j = json.load(f)
         if j.get("workload") == workload:
-            return j.get("dram_bytes_per_launch"), j.get("file")
+            return j
     except Exception:
         pass
-    return None, None
+    return {}
 
 
 # ------------------------------------------------------------------ reference arm (the CPU oracle)
@@ -277,16 +278,26 @@ def run_ours(args, rank, world, local_rank):
     a_bytes, c_bytes, e_bytes = algorithmic_bytes(st, d.L, d.n_nets, via_cuts)
     a_launch = prof["assign_launches"] / args.steps
     a_ms = prof["assign_ms"] / args.steps           # k_assign device time per step (this rank's shard)
-    a_bytes_rank = a_bytes / world
+    # at world 1 with conflict-free batches the demand commit (K8) runs inside the k_assign launches
+    # (fused red.relaxed reductions): its read-modify-write bytes are that kernel's too
+    fused = world == 1 and args.batching == "conflict-free"
+    a_bytes_rank = (a_bytes + (c_bytes if fused else 0)) / world
     achieved = a_bytes_rank / (a_ms / 1000.0) / 1e9 if a_ms > 0 else None
-    traffic_step, traffic_file = ncu_traffic(d.name)
-    roof = {"kernel": "k_assign (K4+K5: Alg. 3 DP + Alg. 4 backtrack)", "bound": "hbm",
-            "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    ncu = ncu_summary(d.name)
+    fp64_peak = la.la_fp64_peak(local_rank)         # FP64 vector pipe, lane ops/s (SURVEY d.3)
+    roof = {"kernel": ("k_assign_g (K4+K5 Alg. 3 DP + Alg. 4 backtrack" + (" + fused K8 commit)" if fused else ")")),
+            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None,
-            "traffic": traffic_step, "traffic_source": traffic_file,
+            "traffic": ncu.get("dram_bytes_per_launch"), "traffic_source": ncu.get("file"),
             "alg_bytes_per_launch": a_bytes_rank / max(a_launch, 1), "launches_per_step": a_launch,
+            "alg_bytes_includes": "K4/K5 per SURVEY d.4" + (" + K8 commit (8 B per unit edge and per via cut)"
+                                                             if fused else ""),
             "kernel_ms_per_step": a_ms, "kernel_share_of_step": a_ms / ms,
-            "peak_source": peak_src}
+            "peak_source": peak_src,
+            "fp64": {"peak_ops_per_s": fp64_peak, "peak_source": "measured (la_fp64_peak: DADD chains on every SM)",
+                     "pipe_active_frac": ncu.get("fp64_pipe_active_frac"),
+                     "pipe_active_source": ncu.get("fp64_source"),
+                     "issue_active_frac": ncu.get("issue_active_frac")}}
     step_bytes = a_bytes + c_bytes + e_bytes
     roof_step = {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / 1000.0) / 1e9,
                  "frac": step_bytes / (ms / 1000.0) / 1e9 / hbm,

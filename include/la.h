@@ -179,19 +179,23 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches);
 
 /* Alg. 3 + Alg. 4 for batch k on this rank's shard of the batch: bottom-up
  * candidate DP with look-ahead, then backtrack.  Enqueue only.
- * At world == 1 (conflict-free batches) the demand commit of batch k is FUSED into
- * this call's kernel (each net commits as soon as it is backtracked), so la_get_demand
- * between la_assign_batch(k) and la_commit_demand(k) already sees batch k's demand;
- * la_commit_demand(k) then only advances the batch state.  With world > 1 or snapshot
- * batches the commit happens in la_commit_demand (after the reconcile).
+ * With conflict-free batches the demand commit of this rank's nets of batch k is FUSED
+ * into this call's kernel (each net commits as soon as it is backtracked; nets of one
+ * batch never share a footprint element, so this cannot change another net's reads), so
+ * la_get_demand between la_assign_batch(k) and la_commit_demand(k) already sees those
+ * commits; la_commit_demand(k) adds the other ranks' nets (world > 1).  With snapshot
+ * batches every commit happens in la_commit_demand.
  * Errors: LA_ERANGE (k out of range), LA_ESTATE (k is not the next batch). */
 la_status la_assign_batch(la_ctx *ctx, int32_t batch);
 
 /* Commit batch k's chosen wires and via cuts into the demand grid (integer
- * atomics); with world > 1 first reconcile every rank's decisions for batch k
- * (NCCL all-reduce over the batch's packed decisions), so every replica applies
- * every commit.  Collective.  Enqueue only.
- * Errors: LA_ESTATE unless batch k was just assigned. */
+ * atomics).  On a context with an NCCL communicator (nccl_id given; world 1 included,
+ * which runs the same path on one GPU) first reconcile every rank's decisions and net
+ * costs for batch k (one sum all-reduce each over the batch's packed decisions, others'
+ * slots 0), so every replica holds every decision; then replay the OTHER ranks' nets
+ * (k_commit over the batch's node ranges outside this rank's two shards: its own nets
+ * committed inside la_assign_batch), or the whole batch with snapshot batches.
+ * Collective.  Enqueue only.  Errors: LA_ESTATE unless batch k was just assigned. */
 la_status la_commit_demand(la_ctx *ctx, int32_t batch);
 
 /* Host transport of the multi-GPU reconcile: a context created
@@ -261,7 +265,11 @@ la_status la_set_schedule(la_ctx *ctx, int32_t schedule);   /* LA_EINVAL for an 
  * (DESIGN §3 O9).  Outputs (any may be NULL): sink_delay[n_pins] in input pin
  * order (driver slots 0), net_cap[n_nets] (wire + sink C, fF), net_rc[n_nets]
  * (sum over resistors of R x downstream C, ps).  Requires every batch
- * committed.  Synchronises.  Collective. */
+ * committed.  Synchronises.  Collective.  With world > 1 each rank evaluates only
+ * the nets it assigned (its shards of every batch) and leaves the others' values 0;
+ * with NCCL the three arrays are then summed over the ranks (an all-gather: every
+ * value has exactly one nonzero contributor, x + 0 == x), so every rank returns the
+ * complete outputs; with the host transport the caller sums them. */
 la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, double *net_rc);
 
 /* The 3D solution in input net order (Alg. 2 output GRS-3D, l.344).  Pass
@@ -313,6 +321,12 @@ la_status la_get_trace(la_ctx *ctx, int64_t *out);
 /* Create an ncclUniqueId (128 bytes) on rank 0, to be broadcast to every rank
  * and passed as la_grid_desc.nccl_id. */
 la_status la_nccl_unique_id(void *out128);
+
+/* Measurement aid (bench.py): the FP64 vector pipe's peak on `device`, in
+ * lane operations per second (one DADD = 1 op), from a kernel of independent DADD chains on
+ * every SM (the DP's fp64 work is DADD / DMUL, no FMA: --fmad=false).  Synchronous; writes
+ * *ops_per_s; LA_ECUDA on a CUDA error. */
+la_status la_fp64_peak(int32_t device, double *ops_per_s);
 
 /* Wait for all enqueued work; surfaces asynchronous CUDA errors. */
 la_status la_sync(la_ctx *ctx);

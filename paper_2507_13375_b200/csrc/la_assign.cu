@@ -878,22 +878,6 @@ __device__ __noinline__ uint32_t group_sweep(const Shared &sh, const GNet &n, in
     return bestK;
 }
 
-// Lowest-layer argmin of a son (row ac, weight w, direction d) over its legal layers in [b, t].
-__device__ __forceinline__ int son_argmin(const Shared &sh, const double2 *ac, double w, int d, const double *VRl,
-                                          double urn, int b, int t) {
-    double m = dinf();
-    int jm = 0;
-    const int nd = sh.ndir[d];
-#pragma unroll
-    for (int s = 0; s < MAXE; ++s) {
-        const int j = sh.lay_of[d][s];
-        if (s < nd && j >= b && j <= t) {
-            const double cp = cost_p(ac[s], w, VRl[j], urn);
-            if (cp < m) { m = cp; jm = j; }
-        }
-    }
-    return jm;
-}
 
 // Reduction of a candidate (G', key) over the P parts of an entry (lanes part * 8 + e).
 template <int P>

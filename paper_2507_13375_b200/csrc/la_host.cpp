@@ -124,6 +124,9 @@ struct la_ctx {
     bool flow_dirty = false;                  // tickets / wait counters consumed since the last reset
     bool fuse_commit = true;
     bool host_xport = false;                  // world > 1 without NCCL: la_get_decisions / la_put_decisions
+    bool nccl = false;                        // an NCCL communicator (any world, 1 included): reconcile by all-reduce
+    int32_t *d_own_pos = nullptr;             // world > 1: this rank's nets (forest positions), every batch
+    int64_t n_own = 0;
     int32_t put_batch = -1;                   // host transport: batch whose reconciled decisions arrived
     int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
     unsigned long long *d_eval = nullptr;     // la_eval_overflow buffers (lazy)
@@ -806,7 +809,8 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     if (e != cudaSuccess) { delete ctx; return cuda_fail(nullptr, e, "snapshot initial state"); }
 
     ctx->host_xport = g->world > 1 && !g->nccl_id;   // ranks reconciled by the caller (la_get/put_decisions)
-    if (g->world > 1 && g->nccl_id) {
+    ctx->nccl = g->nccl_id != nullptr;                // world 1 with an id: the NCCL reconcile on one GPU
+    if (g->nccl_id) {
         ncclUniqueId id;
         std::memcpy(&id, g->nccl_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, g->world, id, g->rank);
@@ -1277,7 +1281,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
     TRY(dev_alloc(ctx, &S.net_cap, N)); TRY(dev_alloc(ctx, &S.net_rc, N));
-    if (ctx->world > 1) TRY(dev_alloc(ctx, &S.dec, NN));
+    if (ctx->world > 1 || ctx->nccl) TRY(dev_alloc(ctx, &S.dec, NN));
     phase("scratch alloc");
     // persistent k_assign grid, tickets, dataflow counters, big-net slots
     {
@@ -1337,6 +1341,21 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                 ctx->batch_job0.push_back((int64_t)ctx->h_jobs.size());
             }
             if (ctx->group_path) TRY(dev_upload(ctx, &ctx->d_jobs, ctx->h_jobs.data(), ctx->h_jobs.size()));
+        }
+        // world > 1: this rank's nets of every batch (its big and small shards), for la_eval_timing
+        if (ctx->world > 1) {
+            std::vector<int32_t> own;
+            for (int32_t b = 0; b < nb; b++) {
+                int64_t s0 = 0, s1 = 0;
+                const int64_t g0 = ctx->batch_big0[b], g1 = ctx->batch_big0[b + 1];
+                la_shard_range(g1 - g0, ctx->world, ctx->rank, &s0, &s1);
+                for (int64_t i = g0 + s0; i < g0 + s1; i++) own.push_back(big_pos[i]);
+                const int64_t m0 = ctx->batch_small0[b], m1 = ctx->batch_small0[b + 1];
+                la_shard_range(m1 - m0, ctx->world, ctx->rank, &s0, &s1);
+                for (int64_t i = m0 + s0; i < m0 + s1; i++) own.push_back(small_pos[i]);
+            }
+            ctx->n_own = (int64_t)own.size();
+            TRY(dev_upload(ctx, &ctx->d_own_pos, own.data(), std::max<size_t>(own.size(), 1)));
         }
         // big-net CTAs: one per SM by default (GAPLA_BIG_CTAS overrides), none without big nets
         ctx->n_big_ctas = big_pos.empty() ? 0 : n_sm;
@@ -1475,7 +1494,7 @@ static AssignLaunch assign_launch(const la_ctx *ctx) {
     al.NS = ctx->NS;
     al.NP = ctx->NP;
     al.LD = ctx->LD;
-    al.commit = (ctx->world == 1 && ctx->fuse_commit) ? 1 : 0;
+    al.commit = ctx->fuse_commit ? 1 : 0;   // this rank's nets commit inside k_assign (any world)
     al.trace = ctx->tracing ? ctx->d_trace : nullptr;
     return al;
 }
@@ -1487,7 +1506,7 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     if (ctx->pending_commit || batch != ctx->next_batch)
         return set_err(LA_ESTATE, "batches must be assigned in order, each committed before the next");
     const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
-    if (ctx->world > 1)   // other ranks' net costs arrive through the reconcile sum
+    if (ctx->world > 1 || ctx->nccl)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
     AssignLaunch al = assign_launch(ctx);
     const RankShare r = rank_share(ctx, batch);
@@ -1575,12 +1594,12 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
         return set_err(LA_ESTATE, "commit must follow the assignment of the same batch");
     const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
     const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
-    if (ctx->world > 1 && ctx->host_xport) {
+    if (ctx->host_xport) {
         // the caller summed every rank's packed decisions and net costs (la_put_decisions)
         if (ctx->put_batch != batch) return set_err(LA_ESTATE, "host transport: la_put_decisions must precede the commit");
         CK(launch_unpack_decisions(ctx->S, n0, n1, ctx->stream));
         ctx->stats.launches += 1;
-    } else if (ctx->world > 1) {
+    } else if (ctx->nccl) {
         // reconcile: every rank contributes its shard's packed decisions (others 0) -> sum
         int pr = prof_begin(ctx, K_RECONCILE);
         TRY(pack_shard(ctx, batch));
@@ -1592,11 +1611,37 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
         prof_end(ctx, pr);
         ctx->stats.launches += 2;
     }
-    if (!(ctx->world == 1 && ctx->fuse_commit)) {   // else already committed inside k_assign
+    // demand: this rank's nets were committed inside k_assign (fuse_commit); replay the others'
+    // decisions (integer adds: every replica ends identical).  Snapshot batches commit everything here.
+    std::vector<std::pair<int64_t, int64_t>> todo;
+    if (!ctx->fuse_commit) {
+        todo.push_back({n0, n1});
+    } else if (ctx->world > 1) {
+        const RankShare r = rank_share(ctx, batch);
+        auto first_node = [&](bool big, int64_t i, int64_t end) {   // node of list entry i, or of the list's end
+            const std::vector<int32_t> &lst = big ? ctx->h_big_pos : ctx->h_small_pos;
+            return i < end ? ctx->h_net_node0[lst[i]] : -1;
+        };
+        // the batch's positions: its big shards (rank 0..), then its small shards; own = two ranges
+        const int64_t ob0 = r.big_end > r.big_beg ? first_node(true, r.big_beg, r.big_end) : -1;
+        const int64_t ob1 = r.big_end > r.big_beg ? ctx->h_net_node0[ctx->h_big_pos[r.big_end - 1] + 1] : -1;
+        const int64_t os0 = r.small_end > r.small_beg ? first_node(false, r.small_beg, r.small_end) : -1;
+        const int64_t os1 = r.small_end > r.small_beg ? ctx->h_net_node0[ctx->h_small_pos[r.small_end - 1] + 1] : -1;
+        int64_t cur = n0;
+        for (auto own : {std::make_pair(ob0, ob1), std::make_pair(os0, os1)}) {
+            if (own.first < 0) continue;
+            if (own.first > cur) todo.push_back({cur, own.first});
+            cur = own.second;
+        }
+        if (n1 > cur) todo.push_back({cur, n1});
+    }
+    if (!todo.empty()) {
         int pc = prof_begin(ctx, K_COMMIT);
-        CK(launch_commit(ctx->G, ctx->F, ctx->S, n0, n1, ctx->stream));
+        for (auto &t : todo) {
+            CK(launch_commit(ctx->G, ctx->F, ctx->S, t.first, t.second, ctx->stream));
+            ctx->stats.launches += 1;
+        }
         prof_end(ctx, pc);
-        ctx->stats.launches += 1;
     }
     ctx->pending_commit = false;
     ctx->next_batch = batch + 1;
@@ -1672,7 +1717,7 @@ la_status la_assign_all(la_ctx *ctx) {
     // of resident warps (latency-bound), batch by batch otherwise (throughput-bound)
     const int32_t sched = ctx->schedule >= 0 ? ctx->schedule
                         : (ctx->n_nets <= (int64_t)ctx->grid * ASSIGN_WARPS ? LA_SCHED_DATAFLOW : LA_SCHED_BATCH);
-    if (ctx->world == 1 && ctx->fuse_commit && sched == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
+    if (ctx->world == 1 && !ctx->nccl && ctx->fuse_commit && sched == LA_SCHED_DATAFLOW && !ctx->pending_commit &&
         ctx->next_batch == 0 && !ctx->flow_dirty) {
         // one persistent launch over every net, in bottom-level priority order
         TRY(build_flow_lists(ctx));
@@ -1813,11 +1858,31 @@ static la_status require_done(la_ctx *ctx) {
 
 la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, double *net_rc) {
     TRY(require_done(ctx));
+    const bool shard = ctx->world > 1;
     if (ctx->n_pins) CK(cudaMemsetAsync(ctx->S.sink_delay, 0, sizeof(double) * ctx->n_pins, ctx->stream));
+    if (shard && ctx->n_nets) {   // other ranks' nets stay 0 here: the outputs are summed over ranks
+        CK(cudaMemsetAsync(ctx->S.net_cap, 0, sizeof(double) * ctx->n_nets, ctx->stream));
+        CK(cudaMemsetAsync(ctx->S.net_rc, 0, sizeof(double) * ctx->n_nets, ctx->stream));
+    }
     int pe = prof_begin(ctx, K_ELMORE);
-    CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_nets, ctx->stream));
+    if (shard) CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_own, ctx->d_own_pos, ctx->stream));
+    else CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_nets, nullptr, ctx->stream));
     prof_end(ctx, pe);
     ctx->stats.launches += 1;
+    if (ctx->nccl) {
+        // allgather of disjoint outputs as one sum (every value has exactly one nonzero contributor)
+        int pr = prof_begin(ctx, K_RECONCILE);
+        if (ctx->n_pins)
+            NK(ncclAllReduce(ctx->S.sink_delay, ctx->S.sink_delay, (size_t)ctx->n_pins, ncclFloat64, ncclSum, ctx->comm,
+                             ctx->stream));
+        if (ctx->n_nets) {
+            NK(ncclAllReduce(ctx->S.net_cap, ctx->S.net_cap, (size_t)ctx->n_nets, ncclFloat64, ncclSum, ctx->comm,
+                             ctx->stream));
+            NK(ncclAllReduce(ctx->S.net_rc, ctx->S.net_rc, (size_t)ctx->n_nets, ncclFloat64, ncclSum, ctx->comm,
+                             ctx->stream));
+        }
+        prof_end(ctx, pr);
+    }
     if (sink_delay && ctx->n_pins)
         CK(cudaMemcpyAsync(sink_delay, ctx->S.sink_delay, sizeof(double) * ctx->n_pins, cudaMemcpyDeviceToHost, ctx->stream));
     if (net_cap && ctx->n_nets)
@@ -2090,6 +2155,14 @@ la_status la_nccl_unique_id(void *out128) {
     ncclResult_t r = ncclGetUniqueId(&id);
     if (r != ncclSuccess) return set_err(LA_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
     std::memcpy(out128, &id, sizeof(id));
+    return LA_OK;
+}
+
+la_status la_fp64_peak(int32_t device, double *ops_per_s) {
+    if (!ops_per_s) return set_err(LA_EINVAL, "null argument");
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = gapla::fp64_peak(ops_per_s);
+    if (e != cudaSuccess) return set_err(LA_ECUDA, std::string("la_fp64_peak: ") + cudaGetErrorString(e));
     return LA_OK;
 }
 

@@ -164,13 +164,16 @@ size_t assign_cta_net_bytes(int L, int LD, int NS, int NP);   // shared memory a
 cudaError_t assign_resident_ctas(int L, int LD, int NS, int NP, int *per_sm_lat, int *per_sm_thr, int *n_sm);
 cudaError_t launch_assign(const DevGrid &G, const DevForest &F, const DevScratch &S, const AssignLaunch &a, int grid,
                           bool throughput, cudaStream_t s);
+cudaError_t fp64_peak(double *ops_per_s);   // la_fp64_peak (la_kernels.cu), current device
 cudaError_t launch_permute_forest(const DevForest &F, const ForestSrc &src, cudaStream_t s);
 cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t node_beg,
                           int64_t node_end, cudaStream_t s);
 cudaError_t launch_pack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);
 cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);
+// k_elmore over the nets [net_beg, net_end) of `list` (forest positions), or over the positions
+// [net_beg, net_end) themselves when list is null.
 cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
-                          int64_t net_end, cudaStream_t s);
+                          int64_t net_end, const int32_t *list, cudaStream_t s);
 
 // Evaluator (la_kernels.cu): histogram of (layer, c == 0, clamp(d - c)) over one packed
 // plane with `slots` layers per element group (slot -> layer via layer_of), exact

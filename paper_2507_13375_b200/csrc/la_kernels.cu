@@ -117,13 +117,14 @@ __global__ void k_unpack_dec(DevScratch S, int64_t node_beg, int64_t node_end) {
 constexpr int ELMORE_THREADS = 128;
 
 __global__ void __launch_bounds__(ELMORE_THREADS) k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg,
-                                                          int64_t net_end) {
+                                                          int64_t net_end, const int32_t *list) {
     __shared__ TechTab T;
     __shared__ double Tks[MAXL][ELMORE_THREADS];   // T(n, k) of the current node, one column per thread
     stage_tab(T, G.tab);
     __syncthreads();
-    const int64_t net = net_beg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (net >= net_end) return;
+    const int64_t idx = net_beg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= net_end) return;
+    const int64_t net = list ? (int64_t)list[idx] : idx;      // this rank's nets (multi-GPU) or all
     const int64_t n0 = F.net_node0[net], n1 = F.net_node0[net + 1];
     // bottom-up: Cdown(n) = C0 + ((Cw1 + Cd1) + ...); rc(n) = F0u + ((c1 + c2) + ...)
     for (int64_t n = n0; n < n1; ++n) {
@@ -309,11 +310,47 @@ cudaError_t launch_permute_forest(const DevForest &F, const ForestSrc &src, cuda
     return cudaGetLastError();
 }
 
+// FP64 pipe peak (la_fp64_peak): 8 independent DADD chains per thread; a lane DADD = 1 op.
+__global__ void __launch_bounds__(256) k_fp64_peak(double *out, int iters, double step) {
+    double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        a0 = a0 + step; a1 = a1 + step; a2 = a2 + step; a3 = a3 + step;
+        a4 = a4 + step; a5 = a5 + step; a6 = a6 + step; a7 = a7 + step;
+    }
+    const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == -1.0) out[0] = r;                       // keeps the chains live
+}
+
+cudaError_t fp64_peak(double *ops_per_s) {
+    int dev = 0, n_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    double *d = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&d, 8);
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreate(&a);
+    if (e == cudaSuccess) e = cudaEventCreate(&b);
+    const int iters = 1 << 14, grid = n_sm * 8, threads = 256;
+    float ms = 0.f;
+    for (int rep = 0; rep < 3 && e == cudaSuccess; ++rep) {   // the last of three timed runs
+        cudaEventRecord(a);
+        k_fp64_peak<<<grid, threads>>>(d, iters, 1e-300);
+        cudaEventRecord(b);
+        e = cudaEventSynchronize(b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    }
+    if (e == cudaSuccess) *ops_per_s = (double)grid * threads * 8.0 * iters / (ms * 1e-3);
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    if (d) cudaFree(d);
+    return e;
+}
+
 cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
-                          int64_t net_end, cudaStream_t s) {
+                          int64_t net_end, const int32_t *list, cudaStream_t s) {
     int64_t n = net_end - net_beg;
     if (n <= 0) return cudaSuccess;
-    k_elmore<<<nblk(n, ELMORE_THREADS), ELMORE_THREADS, 0, s>>>(G, F, S, net_beg, net_end);
+    k_elmore<<<nblk(n, ELMORE_THREADS), ELMORE_THREADS, 0, s>>>(G, F, S, net_beg, net_end, list);
     return cudaGetLastError();
 }
 

@@ -112,6 +112,7 @@ def _load():
         "la_set_profiling": ([c_void_p, c_i32], c_i32),
         "la_get_profile": ([c_void_p, P(la_profile), c_i32], c_i32),
         "la_nccl_unique_id": ([c_void_p], c_i32),
+        "la_fp64_peak": ([c_i32, P(c_f64)], c_i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -125,7 +126,7 @@ EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand"
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
            "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches",
-           "la_paper_batches", "la_batch_extent", "la_get_decisions", "la_put_decisions")
+           "la_paper_batches", "la_batch_extent", "la_get_decisions", "la_put_decisions", "la_fp64_peak")
 
 
 def _check(st):
@@ -279,6 +280,13 @@ def la_get_stats(ctx) -> dict:
 
 def la_sync(ctx):
     _check(_lib.la_sync(ctx))
+
+
+def la_fp64_peak(device: int = 0) -> float:
+    """FP64 vector-pipe peak of the device, lane ops per second (measurement aid)."""
+    v = c_f64(0.0)
+    _check(_lib.la_fp64_peak(int(device), ctypes.byref(v)))
+    return v.value
 
 
 def la_destroy(ctx):

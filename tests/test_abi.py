@@ -23,7 +23,7 @@ def la():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "la.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(la_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(la_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(la):

@@ -363,9 +363,16 @@ def test_sharded_path_host_transport(la, world, cfg, n):
         for A in ranks:
             la.la_put_decisions(A.ctx, k, dec, cost)
             A.commit_demand(k)
+    # la_eval_timing is sharded too: each rank evaluates the nets it assigned (others 0); the
+    # caller's element-wise sum is the all-gather (one nonzero contributor per value)
+    timing = [A.eval_timing() for A in ranks]
+    for k in ("sink_delay", "net_cap", "net_rc"):
+        nz = np.sum([t[k] != 0 for t in timing], axis=0)
+        assert np.all(nz <= 1), f"{k}: a value evaluated by two ranks"
+    summed = {k: np.sum([t[k] for t in timing], axis=0) for k in ("sink_delay", "net_cap", "net_rc")}
     outs = []
     for A in ranks:
-        out = A.eval_timing()
+        out = dict(summed)
         out.update(A.solution())
         wd, vd = A.demand()
         out.update(wire_dem=wd, via_dem=vd, batch_of=A.batches())
@@ -374,6 +381,27 @@ def test_sharded_path_host_transport(la, world, cfg, n):
     ref = oracle.run(d)
     for out in outs:
         assert_parity(out, ref, bitwise_fp=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,n,sched", [(2, None, "batch"), (1, None, "auto"), (3, 150_000, "batch")])
+def test_nccl_reconcile_one_gpu(la, cfg, n, sched):
+    """The NCCL branch of la_commit_demand and la_eval_timing on one GPU: a world-1 context with an
+    ncclUniqueId packs its decisions, all-reduces them (and the net costs, then the timing outputs)
+    through a real NCCL communicator and unpacks them; the result must equal the oracle bit for bit
+    and the reconcile must have run (profile)."""
+    d = synth.make_config(cfg, n_nets=n)
+    A = la.LayerAssigner(d, device=0, rank=0, world=1, nccl_id=la.la_nccl_unique_id())
+    A.load()
+    if sched == "batch":
+        A.set_schedule(la.LA_SCHED_BATCH)
+    A.profiling(True)
+    A.profile(reset=True)
+    got = A.run()
+    prof = A.profile(reset=True)
+    A.close()
+    assert prof["reconcile_ms"] > 0.0
+    assert_parity(got, oracle.run(d), bitwise_fp=True)
 
 
 def test_new_call_order_errors(la):
