@@ -360,12 +360,14 @@ cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch
 // k_eval_plane (PAPER Eq. (2)/(3) l.174-182): one pass over a packed
 // demand plane (the element of slot s of group i is words[i * slots + s]).  Every word gives
 // d - c (w >> 1) and the zero-capacity flag (w & 1); counts per (layer, flag, d - c) go to a
-// shared-memory window of d - c (warp-aggregated with __match_any_sync), the rest straight
-// to the global bins; max(0, d - c) is summed exactly per layer.  HBM-bound: 4 B per element,
+// shared-memory window of d - c (EV_COPIES copies, one per lane & 3, plain shared atomics), the
+// rest straight to the global bins; max(0, d - c) is summed exactly per layer.  HBM-bound: 4 B per element,
 // read once with 16-byte loads; grid = a multiple of the SM count.
 namespace gapla {
 namespace {
-constexpr int EV_LO = -64, EV_W = 128;             // shared window of d - c
+constexpr int EV_LO = -48, EV_W = 64;              // shared window of d - c
+constexpr int EV_COPIES = 4;                        // histogram copies (lane & 3): lanes of one warp that
+                                                    // hold the same layer slot mostly hit different copies
 constexpr int EV_THREADS = 512;
 
 __device__ __forceinline__ void eval_word(int32_t w, int slot, uint32_t (*sh)[2][EV_W], unsigned long long *shleg,
@@ -373,9 +375,7 @@ __device__ __forceinline__ void eval_word(int32_t w, int slot, uint32_t (*sh)[2]
     const int d = w >> 1, f = w & 1;
     if (d > 0) atomicAdd(&shleg[slot], (unsigned long long)d);
     if (d >= EV_LO && d < EV_LO + EV_W) {
-        const unsigned key = ((unsigned)slot << 8) | ((unsigned)f << 7) | (unsigned)(d - EV_LO);
-        const unsigned peers = __match_any_sync(__activemask(), key);
-        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&sh[slot][f][d - EV_LO], __popc(peers));
+        atomicAdd(&sh[slot][f][d - EV_LO], 1u);
     } else {
         const int dc = min(max(d, dlo), dhi);
         if (dc != d) atomicAdd(E.oob, 1ull);
@@ -386,11 +386,12 @@ __device__ __forceinline__ void eval_word(int32_t w, int slot, uint32_t (*sh)[2]
 __global__ void __launch_bounds__(EV_THREADS) k_eval_plane(const int32_t *__restrict__ words, int64_t n, int slots,
                                                            const int8_t *__restrict__ layer_of, EvalDev E, int dlo,
                                                            int dhi) {
-    __shared__ uint32_t sh[MAXL][2][EV_W];
+    __shared__ uint32_t shc[EV_COPIES][MAXL][2][EV_W];
     __shared__ unsigned long long shleg[MAXL];
-    for (int i = threadIdx.x; i < MAXL * 2 * EV_W; i += blockDim.x) (&sh[0][0][0])[i] = 0;
+    for (int i = threadIdx.x; i < EV_COPIES * MAXL * 2 * EV_W; i += blockDim.x) (&shc[0][0][0][0])[i] = 0;
     if (threadIdx.x < MAXL) shleg[threadIdx.x] = 0;
     __syncthreads();
+    uint32_t (*sh)[2][EV_W] = shc[threadIdx.x & (EV_COPIES - 1)];
     const int nbins = dhi - dlo + 1;
     const int64_t n4 = n / 4;
     const int4 *w4 = reinterpret_cast<const int4 *>(words);
@@ -417,7 +418,9 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_plane(const int32_t *__rest
     __syncthreads();
     for (int i = threadIdx.x; i < slots * 2 * EV_W; i += blockDim.x) {
         const int s = i / (2 * EV_W), f = (i / EV_W) & 1, b = i % EV_W;
-        const uint32_t c = sh[s][f][b];
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < EV_COPIES; ++k) c += shc[k][s][f][b];
         const int d = EV_LO + b;
         if (c) atomicAdd(&E.hist[((int)layer_of[s] * 2 + f) * nbins + (min(max(d, dlo), dhi) - dlo)], (unsigned long long)c);
         if (c && (d < dlo || d > dhi)) atomicAdd(E.oob, (unsigned long long)c);
@@ -425,25 +428,29 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_plane(const int32_t *__rest
     if (threadIdx.x < slots && shleg[threadIdx.x]) atomicAdd(&E.legacy[layer_of[threadIdx.x]], shleg[threadIdx.x]);
 }
 
-// k_eval_nodes: unit wire edges per layer (len of every parent run on its layer) and via cuts.
+// k_eval_nodes: unit wire edges per layer (len of every parent run on its layer) and via cuts;
+// per-thread counters in registers (layer index unrolled), one warp reduction per layer at the end.
 __global__ void __launch_bounds__(256) k_eval_nodes(DevForest F, DevScratch S, EvalDev E) {
-    __shared__ unsigned long long wl[MAXL];
-    __shared__ unsigned long long vc;
-    if (threadIdx.x < MAXL) wl[threadIdx.x] = 0;
-    if (threadIdx.x == 0) vc = 0;
-    __syncthreads();
+    uint32_t wl[MAXL];
+#pragma unroll
+    for (int l = 0; l < MAXL; ++l) wl[l] = 0;
     unsigned long long myv = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.n_nodes; i += stride) {
         const int l = S.lay[i];
-        if (F.edir[i] != NO_DIR) atomicAdd(&wl[l], (unsigned long long)F.len[i]);
+        const uint32_t len = F.edir[i] != NO_DIR ? (uint32_t)F.len[i] : 0u;
+#pragma unroll
+        for (int k = 0; k < MAXL; ++k) wl[k] += k == l ? len : 0u;
         myv += (unsigned)(S.st[i] - S.sb[i]);
     }
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) {
+        unsigned long long v = wl[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&E.wl[k], v);
+    }
     for (int o = 16; o > 0; o >>= 1) myv += __shfl_xor_sync(FULL_MASK, myv, o);
-    if ((threadIdx.x & 31) == 0 && myv) atomicAdd(&vc, myv);
-    __syncthreads();
-    if (threadIdx.x < MAXL && wl[threadIdx.x]) atomicAdd(&E.wl[threadIdx.x], wl[threadIdx.x]);
-    if (threadIdx.x == 0 && vc) atomicAdd(E.vcuts, vc);
+    if ((threadIdx.x & 31) == 0 && myv) atomicAdd(E.vcuts, myv);
 }
 }  // namespace
 
