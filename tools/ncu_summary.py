@@ -15,6 +15,7 @@ import sys
 from collections import defaultdict
 
 src, workload, out = sys.argv[1], sys.argv[2], sys.argv[3]
+full = sys.argv[4] if len(sys.argv) > 4 else None     # optional ncu --set full report of one k_assign launch
 rows = []
 with open(src) as f:
     lines = [l for l in f if l.startswith('"')]
@@ -43,11 +44,20 @@ for k, p in sorted(per.items(), key=lambda kv: -kv[1]["ms"]):
                           "dram_bytes_per_launch": (p["dram_bytes"] / n) if "dram_bytes" in p else None}
 with open(out, "w") as f:
     json.dump(summ, f, indent=1)
-ka = summ["kernels"].get("k_assign")
+ka = summ["kernels"].get("k_assign_g") or summ["kernels"].get("k_assign")
 if ka and ka["dram_bytes_per_launch"] is not None:
+    j = {"workload": workload, "file": os.path.basename(out),
+         "dram_bytes_per_launch": ka["dram_bytes_per_launch"], "launches": ka["launches"],
+         "note": "ncu serialised cold-cache launches of one bench step; mean over the step's launches"}
+    if full:
+        import subprocess
+        raw = subprocess.run(["ncu", "-i", full, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(raw.splitlines()))
+        h, v = rr[0], rr[2]
+        get = lambda m: float(v[h.index(m)]) / 100.0 if m in h else None
+        j["fp64_pipe_active_frac"] = get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+        j["issue_active_frac"] = get("smsp__issue_active.avg.pct_of_peak_sustained_active")
+        j["fp64_source"] = os.path.basename(full) + " (ncu --set full, one mid-step launch)"
     with open(os.path.join(os.path.dirname(out), "ncu_k_assign_summary.json"), "w") as f:
-        json.dump({"workload": workload, "file": os.path.basename(out),
-                   "dram_bytes_per_launch": ka["dram_bytes_per_launch"], "launches": ka["launches"],
-                   "note": "ncu serialised cold-cache launches of one bench step; mean over the step's launches"},
-                  f, indent=1)
+        json.dump(j, f, indent=1)
 print(json.dumps(summ, indent=1))

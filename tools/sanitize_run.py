@@ -85,13 +85,37 @@ def sc_host_transport():
             la.la_put_decisions(A.ctx, k, dec, cost)
             A.commit_demand(k)
     ref = oracle.run(d)
+    timing = [A.eval_timing() for A in ranks]          # each rank evaluates its own nets; the sum is the all-gather
+    summed = {k: np.sum([t[k] for t in timing], axis=0) for k in ("sink_delay", "net_cap", "net_rc")}
     for A in ranks:
-        out = A.eval_timing()
+        out = dict(summed)
         out.update(A.solution())
         wd, vd = A.demand()
         out.update(wire_dem=wd, via_dem=vd)
         check(out, ref, f"cfg1 host transport rank {A.grid_desc.rank}")
         A.close()
+
+
+def sc_nccl_one_gpu():
+    d = synth.make_config(2, n_nets=6000)
+    A = la.LayerAssigner(d, device=0, rank=0, world=1, nccl_id=la.la_nccl_unique_id())
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    out = A.run()
+    A.close()
+    check(out, oracle.run(d), "cfg2[6000] NCCL reconcile, world 1")
+
+
+def sc_group_paths():
+    # k_assign_g: the group path with every job size and the team path (half-CTA and whole-CTA
+    # teams, group/team split at small and large node counts)
+    d = synth.make_config(3, n_nets=5000)
+    ref = oracle.run(d)
+    for env in ({"GAPLA_GROUP_NMAX": "4"}, {"GAPLA_GROUP_NMAX": "64"}, {"GAPLA_BIG_SPLIT": "0"}, {"GAPLA_BIG_SPLIT": "1"}):
+        os.environ.update(env)
+        check(run(d, la.LA_SCHED_BATCH), ref, f"cfg3[5000] batch {env}")
+        for k in env:
+            del os.environ[k]
 
 
 SCENARIOS = {k[3:]: v for k, v in globals().items() if k.startswith("sc_")}
