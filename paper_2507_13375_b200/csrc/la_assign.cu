@@ -1104,10 +1104,35 @@ __device__ __forceinline__ void group_gather(const GNet &n, const Shared &sh, co
         n.pl[q] = F.p_layer[q_base + q];
         n.sk[q] = make_double2(F.p_cap[q_base + q], F.p_w[q_base + q]);
     }
-    for (int idx = tid; idx < nn * Lm1; idx += nthr) {
-        const int i = idx / Lm1, k = idx - i * Lm1;
-        const uint32_t xy = __ldg(F.xy + n0 + i);
-        n.kap[idx] = kappa_w(G, sh, __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k), k);
+    if (nthr >= 16) {
+        // a team (big net, latency-bound): chunks of 4 items per thread, the chunk's via words all
+        // in flight before the dependent Eq. (3) table lookups
+        const int nk_items = nn * Lm1;
+#pragma unroll 1
+        for (int base = 0; base < nk_items; base += 4 * nthr) {
+            int32_t wv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int idx = base + tid + u * nthr;
+                wv[u] = 0;
+                if (idx < nk_items) {
+                    const int i = idx / Lm1, k = idx - i * Lm1;
+                    const uint32_t xy = __ldg(F.xy + n0 + i);
+                    wv[u] = __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int idx = base + tid + u * nthr;
+                if (idx < nk_items) n.kap[idx] = kappa_w(G, sh, wv[u], idx % Lm1);
+            }
+        }
+    } else {
+        for (int idx = tid; idx < nn * Lm1; idx += nthr) {
+            const int i = idx / Lm1, k = idx - i * Lm1;
+            const uint32_t xy = __ldg(F.xy + n0 + i);
+            n.kap[idx] = kappa_w(G, sh, __ldcg(G.via + ((int64_t)(xy >> 16) * G.X + (xy & 0xffff)) * Lm1 + k), k);
+        }
     }
     for (int idx = tid; idx < (nn - 1) * LD; idx += nthr) {
         const int i = idx / LD, s = idx - i * LD;
@@ -1227,7 +1252,7 @@ __device__ __forceinline__ void run_net_team(char *base, const Shared &sh, const
     GNet n = group_net(base, group_layout(nn, ns, L, LD, T));
     n.Vt += wid * vt_elems(L);
     int64_t *tr = a.trace ? a.trace + 5 * net : nullptr;
-    if (tr && tid == 0) tr[0] = tr[1] = gtimer();
+    if (tr && tid == 0) tr[0] = gtimer();
     const int pdrv = F.net_pdrv[net];
     group_gather(n, sh, G, F, n0, nn, ns, q_base, LD, tid, nthr);
     bar_sync(bar, nthr);
@@ -1259,11 +1284,31 @@ __device__ __forceinline__ void run_net_team(char *base, const Shared &sh, const
         bar_sync(bar, nthr);
         lo = hi;
     }
+    if (tr && tid == 0) tr[1] = gtimer();             // team nets: [1] = end of the level loop
+    // Alg. 4, level-parallel from the root: the nodes of one height level take their entry layer
+    // from their parents (a level above) and set their sons'
     if (tid == 0) {
         S.froot[net] = *n.froot;
-        group_backtrack(n, sh, nn, pdrv, LD);
+        n.nd[nn - 1].lay = (uint8_t)pdrv;
     }
     bar_sync(bar, nthr);
+    for (int hi = nn; hi > 0;) {
+        const int h = n.nd[hi - 1].height;
+        int l0 = hi - 1;
+        while (l0 > 0 && n.nd[l0 - 1].height == h) --l0;
+        for (int i = l0 + tid; i < hi; i += nthr) {
+            NodeG &r = n.nd[i];
+            const int slot = i == nn - 1 ? 0 : sh.lidx[r.lay];
+            const uint32_t d = n.dec[i * LD + slot];
+            r.sb = d & 0xf;
+            r.st = (d >> 4) & 0xf;
+            const uint32_t jj = d >> 8;
+#pragma unroll 1
+            for (int k = 0; k < r.nkid; ++k) n.nd[r.kid[k]].lay = (uint8_t)((jj >> (4 * k)) & 0xf);
+        }
+        bar_sync(bar, nthr);
+        hi = l0;
+    }
     group_emit(n, G, S, a, n0, nn, tid, nthr);
     if (tr && tid == 0) trace_end(tr);
 }

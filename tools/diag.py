@@ -217,3 +217,29 @@ if os.environ.get("DIAG_NODEKIND"):
         print(f"    wires [{lo},{hi}): total {tot[m].mean() / 1e3:.2f} one-son {t[m, 1].mean() / 1e3:.2f} "
               f"other {t[m, 4].mean() / 1e3:.2f}", flush=True)
     A.close()
+
+if os.environ.get("DIAG_TEAM"):
+    # team-path nets (k_assign_g big nets): per size band, take -> gather end -> level loop end -> commit end
+    import numpy as np
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    A.reset()
+    la.la_set_tracing(A.ctx, True)
+    A.assign_all()
+    A.sync()
+    t = la.la_get_trace(A.ctx, d.n_nets)
+    sol = A.solution()
+    nw = np.diff(sol["wire_ptr"])
+    team = t[:, 1] > t[:, 2]            # team nets stamp [1] after the level loop; group nets [1] = [0]
+    g = (t[:, 2] - t[:, 0]) / 1e3
+    lv = (t[:, 1] - t[:, 2]) / 1e3
+    tl = (t[:, 3] - t[:, 1]) / 1e3
+    print(f"  team nets: {int(team.sum())} of {d.n_nets}")
+    for lo, hi in ((1, 13), (13, 20), (20, 30), (30, 50), (50, 80), (80, 120), (120, 200), (200, 100000)):
+        m = team & (nw >= lo) & (nw < hi)
+        if m.any():
+            print(f"    wires [{lo:3d},{hi:3d}): {m.sum():6d} nets gather p50 {np.median(g[m]):7.1f} us  levels p50 "
+                  f"{np.median(lv[m]):7.1f} p90 {np.percentile(lv[m], 90):7.1f}  backtrack+commit p50 {np.median(tl[m]):6.1f} us",
+                  flush=True)
+    A.close()
