@@ -243,3 +243,28 @@ if os.environ.get("DIAG_TEAM"):
                   f"{np.median(lv[m]):7.1f} p90 {np.percentile(lv[m], 90):7.1f}  backtrack+commit p50 {np.median(tl[m]):6.1f} us",
                   flush=True)
     A.close()
+
+if os.environ.get("DIAG_TIMELINE"):
+    # per batch: when team nets and group nets are taken / finish, relative to the batch's first take
+    import numpy as np
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.set_schedule(la.LA_SCHED_BATCH)
+    A.reset()
+    la.la_set_tracing(A.ctx, True)
+    A.assign_all()
+    A.sync()
+    t = la.la_get_trace(A.ctx, d.n_nets)
+    bo = A.batches()
+    team = t[:, 1] > t[:, 2]
+    nb = int(bo.max()) + 1
+    print(f"  {'batch':>5} {'nets':>7} {'team':>6} {'span':>7} | team take p50/max  end max | group take max  end p99 max  (us)")
+    for b in list(range(0, nb, max(1, nb // 16))):
+        m = bo == b
+        t0 = t[m, 0].min()
+        tm, gm = m & team, m & ~team
+        def q(x, p): return (np.percentile(x, p) - t0) / 1e3 if len(x) else float("nan")
+        print(f"  {b:5d} {int(m.sum()):7d} {int(tm.sum()):6d} {(t[m, 3].max() - t0) / 1e3:7.0f} | "
+              f"{q(t[tm, 0], 50):7.0f} {q(t[tm, 0], 100):7.0f} {q(t[tm, 3], 100):7.0f} | "
+              f"{q(t[gm, 0], 100):7.0f} {q(t[gm, 3], 99):7.0f} {q(t[gm, 3], 100):7.0f}", flush=True)
+    A.close()
