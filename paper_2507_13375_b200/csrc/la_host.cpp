@@ -131,6 +131,9 @@ struct la_ctx {
     int64_t *d_trace = nullptr;               // la_set_tracing: [n_nets][5] (forest order)
     unsigned long long *d_eval = nullptr;     // la_eval_overflow buffers (lazy)
     int8_t *d_eval_lay = nullptr;             // [3][MAXL] slot -> layer for the H, V and via planes
+    bool eval0_done = false;                  // Σ(d - c) per layer of the initial planes (la_eval_overflow)
+    std::vector<long long> eval0_wire, eval0_via;
+    int64_t eval0_oob = 0;
     std::vector<int64_t> batch_big0, batch_small0;   // [n_batches+1] per-batch ranges of the role lists
     // role lists as packed per-net records (position, node0, nodes | sinks << 16, sink0): one
     // 16-byte load per net instead of a chain of dependent loads in k_assign
@@ -2078,23 +2081,72 @@ la_status la_eval_overflow(la_ctx *ctx, la_eval *out) {
         CK(cudaMemcpyAsync(ctx->d_eval_lay, lay, sizeof(lay), cudaMemcpyHostToDevice, ctx->stream));
     }
     unsigned long long *b = ctx->d_eval;
+    const int64_t nH = (int64_t)(ctx->X - 1) * ctx->Y * ctx->LH, nV = (int64_t)ctx->X * (ctx->Y - 1) * ctx->LV;
+    // Per-layer wirelength and the via-cut count follow from the plane histograms: every committed
+    // unit wire edge (via cut) adds 1 to one word, so on each layer Σ(d - c) grows by exactly its
+    // wirelength.  Σ(d - c) of the initial state comes from one histogram pass over the pristine
+    // planes, once per context; a value clamped to [δ_lo, δ_hi] (R20) in either pass makes the sums
+    // inexact, and then the node pass (k_eval_nodes) counts them instead.
+    auto plane_sums = [&](const unsigned long long *hh, int nlay, std::vector<long long> &sum) {
+        sum.assign(MAXL, 0);
+        for (int l = 0; l < nlay; l++)
+            for (int f = 0; f < 2; f++)
+                for (int i = 0; i < nbins; i++) sum[l] += (long long)hh[((size_t)l * 2 + f) * nbins + i] * (dlo + i);
+    };
+    if (!ctx->eval0_done) {
+        CK(cudaMemsetAsync(b, 0, sizeof(unsigned long long) * nwords, ctx->stream));
+        EvalDev E0{b, b + 2 * nh, b + 2 * nh + 2 * MAXL, b + 2 * nh + 2 * MAXL + 1, b + 2 * nh + 3 * MAXL + 1};
+        EvalDev V0 = E0;
+        V0.hist = b + nh;
+        V0.legacy = b + 2 * nh + MAXL;
+        CK(launch_eval_plane(ctx->d_wH0, nH, ctx->LH, ctx->d_eval_lay, E0, dlo, dhi, ctx->stream));
+        CK(launch_eval_plane(ctx->d_wV0, nV, ctx->LV, ctx->d_eval_lay + MAXL, E0, dlo, dhi, ctx->stream));
+        CK(launch_eval_plane(ctx->d_via0, ctx->n_via_api, L - 1, ctx->d_eval_lay + 2 * MAXL, V0, dlo, dhi, ctx->stream));
+        std::vector<unsigned long long> h0(nwords);
+        CK(cudaMemcpyAsync(h0.data(), b, sizeof(unsigned long long) * nwords, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        plane_sums(h0.data(), L, ctx->eval0_wire);
+        plane_sums(h0.data() + nh, L - 1, ctx->eval0_via);
+        ctx->eval0_oob = (int64_t)h0[2 * nh + 2 * MAXL];
+        ctx->eval0_done = true;
+    }
     CK(cudaMemsetAsync(b, 0, sizeof(unsigned long long) * nwords, ctx->stream));
     EvalDev Ew{b, b + 2 * nh, b + 2 * nh + 2 * MAXL, b + 2 * nh + 2 * MAXL + 1, b + 2 * nh + 3 * MAXL + 1};
     EvalDev Ev = Ew;
     Ev.hist = b + nh;
     Ev.legacy = b + 2 * nh + MAXL;
-    const int64_t nH = (int64_t)(ctx->X - 1) * ctx->Y * ctx->LH, nV = (int64_t)ctx->X * (ctx->Y - 1) * ctx->LV;
     int pe = prof_begin(ctx, K_EVAL);
     CK(launch_eval_plane(ctx->d_wH, nH, ctx->LH, ctx->d_eval_lay, Ew, dlo, dhi, ctx->stream));
     CK(launch_eval_plane(ctx->d_wV, nV, ctx->LV, ctx->d_eval_lay + MAXL, Ew, dlo, dhi, ctx->stream));
     CK(launch_eval_plane(ctx->d_via, ctx->n_via_api, L - 1, ctx->d_eval_lay + 2 * MAXL, Ev, dlo, dhi, ctx->stream));
-    CK(launch_eval_nodes(ctx->F, ctx->S, Ew, ctx->stream));
     prof_end(ctx, pe);
-    ctx->stats.launches += 4;
+    ctx->stats.launches += 3;
     std::vector<unsigned long long> h(nwords);
     CK(cudaMemcpyAsync(h.data(), b, sizeof(unsigned long long) * nwords, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->stats.d2h_bytes += (int64_t)(8 * nwords);
+    const bool from_planes = h[2 * nh + 2 * MAXL] == 0 && ctx->eval0_oob == 0;
+    if (from_planes) {
+        std::vector<long long> sw, sv;
+        plane_sums(h.data(), L, sw);
+        plane_sums(h.data() + nh, L - 1, sv);
+        long long vc = 0;
+        for (int l = 0; l < MAXL; l++) {
+            h[2 * nh + 2 * MAXL + 1 + l] = (unsigned long long)(sw[l] - ctx->eval0_wire[l]);
+            vc += sv[l] - ctx->eval0_via[l];
+        }
+        h[2 * nh + 3 * MAXL + 1] = (unsigned long long)vc;
+    } else {   // a clamped value: count wirelength and via cuts from the nodes
+        unsigned long long *nb = b + 2 * nh + 2 * MAXL + 1;
+        CK(cudaMemsetAsync(nb, 0, sizeof(unsigned long long) * (MAXL + 1), ctx->stream));
+        int pn = prof_begin(ctx, K_EVAL);
+        CK(launch_eval_nodes(ctx->F, ctx->S, Ew, ctx->stream));
+        prof_end(ctx, pn);
+        ctx->stats.launches += 1;
+        CK(cudaMemcpyAsync(h.data() + 2 * nh + 2 * MAXL + 1, nb, sizeof(unsigned long long) * (MAXL + 1),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     // Eq. (3): per layer, bins in a fixed order (c > 0 then c == 0, d - c ascending), then layers ascending
     auto tof = [&](const unsigned long long *hist, int nlay) {
         double t = 0.0;

@@ -429,20 +429,34 @@ __global__ void __launch_bounds__(EV_THREADS) k_eval_plane(const int32_t *__rest
 }
 
 // k_eval_nodes: unit wire edges per layer (len of every parent run on its layer) and via cuts;
-// per-thread counters in registers (layer index unrolled), one warp reduction per layer at the end.
+// four nodes per thread and iteration (32-bit loads of the byte arrays, one 16-byte load of the
+// lengths), per-thread counters in registers (layer index unrolled), one warp reduction per layer.
 __global__ void __launch_bounds__(256) k_eval_nodes(DevForest F, DevScratch S, EvalDev E) {
     uint32_t wl[MAXL];
 #pragma unroll
     for (int l = 0; l < MAXL; ++l) wl[l] = 0;
     unsigned long long myv = 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.n_nodes; i += stride) {
-        const int l = S.lay[i];
-        const uint32_t len = F.edir[i] != NO_DIR ? (uint32_t)F.len[i] : 0u;
+    auto node = [&](int l, int ed, int len, int b, int t) {
+        const uint32_t w = ed != NO_DIR ? (uint32_t)len : 0u;
 #pragma unroll
-        for (int k = 0; k < MAXL; ++k) wl[k] += k == l ? len : 0u;
-        myv += (unsigned)(S.st[i] - S.sb[i]);
+        for (int k = 0; k < MAXL; ++k) wl[k] += k == l ? w : 0u;
+        myv += (unsigned)(t - b);
+    };
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = F.n_nodes / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint32_t l4 = reinterpret_cast<const uint32_t *>(S.lay)[i];
+        const uint32_t e4 = reinterpret_cast<const uint32_t *>(F.edir)[i];
+        const uint32_t b4 = reinterpret_cast<const uint32_t *>(S.sb)[i];
+        const uint32_t t4 = reinterpret_cast<const uint32_t *>(S.st)[i];
+        const int4 len = reinterpret_cast<const int4 *>(F.len)[i];
+        node(l4 & 0xff, e4 & 0xff, len.x, b4 & 0xff, t4 & 0xff);
+        node((l4 >> 8) & 0xff, (e4 >> 8) & 0xff, len.y, (b4 >> 8) & 0xff, (t4 >> 8) & 0xff);
+        node((l4 >> 16) & 0xff, (e4 >> 16) & 0xff, len.z, (b4 >> 16) & 0xff, (t4 >> 16) & 0xff);
+        node(l4 >> 24, e4 >> 24, len.w, b4 >> 24, t4 >> 24);
     }
+    for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.n_nodes; i += stride)
+        node(S.lay[i], F.edir[i], F.len[i], S.sb[i], S.st[i]);
 #pragma unroll
     for (int k = 0; k < MAXL; ++k) {
         unsigned long long v = wl[k];

@@ -284,6 +284,7 @@ def test_evaluator_parity(la, cfg, n):
     A.load()
     A.assign_all()
     ev = A.eval_overflow()
+    assert A.eval_overflow() == ev          # second call: cached initial-state sums
     A.close()
     ref = oracle.run(d)
     ex = oracle.evaluate(d, ref["wire_dem"], ref["via_dem"], ref["wires"], ref["vias"])
@@ -293,6 +294,27 @@ def test_evaluator_parity(la, cfg, n):
     assert ev["wirelength"] == ex["wirelength"]
     for k in ("tof_wire", "tof_via", "wire_cap"):
         assert abs(ev[k] - ex[k]) <= 1e-12 * abs(ex[k]), (k, ev[k], ex[k])
+
+
+def test_evaluator_clamped_domain(la):
+    """la_eval_overflow when d - c leaves the table domain [δ_lo, δ_hi] (R20): the per-layer
+    wirelength and via cuts can then no longer come from the plane histograms' Σ(d - c) (clamped
+    bins), so the library counts them from the nodes; they must still equal the oracle's, and
+    repeated calls (the initial-state sums are cached) must agree."""
+    d = synth.make_config(1)
+    d.delta_lo, d.delta_hi = -3, 1
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    A.assign_all()
+    ev = A.eval_overflow()
+    ev2 = A.eval_overflow()
+    A.close()
+    ref = oracle.run(d)
+    ex = oracle.evaluate(d, ref["wire_dem"], ref["via_dem"], ref["wires"], ref["vias"])
+    assert ev["out_of_domain"] > 0
+    for k in ("legacy_wire", "legacy_via", "via_cuts"):
+        assert ev[k] == ex[k] == ev2[k], k
+    assert ev["wirelength"] == ex["wirelength"] == ev2["wirelength"]
 
 
 @pytest.mark.parametrize("variant", ["no_lookahead", "no_timing", "heavy_timing"])
