@@ -125,6 +125,12 @@ struct la_ctx {
     bool fuse_commit = true;
     bool host_xport = false;                  // world > 1 without NCCL: la_get_decisions / la_put_decisions
     bool nccl = false;                        // an NCCL communicator (any world, 1 included): reconcile by all-reduce
+    // la_get_solution: decisions copied to the host and the per-net counts, kept between the count
+    // query and the fill call until the next assignment or reset
+    bool sol_valid = false;
+    std::vector<uint8_t> sol_lay, sol_sb, sol_st;
+    std::vector<double> sol_froot;
+    std::vector<int64_t> sol_nw, sol_nv, sol_pos_of;
     int32_t *d_own_pos = nullptr;             // world > 1: this rank's nets (forest positions), every batch
     int64_t n_own = 0;
     int32_t put_batch = -1;                   // host transport: batch whose reconciled decisions arrived
@@ -273,6 +279,88 @@ void par_for(int64_t n, unsigned nthr, F f) {
         th.emplace_back([&, t] { for (int64_t i = n * t / nthr; i < n * (t + 1) / nthr; i++) f(i); });
     for (int64_t i = 0; i < n / nthr; i++) f(i);
     for (auto &x : th) x.join();
+}
+
+// Host <-> device copies of pageable host memory, pipelined: the ranges are cut into pieces that
+// worker threads copy into pinned double buffers (a process-wide pool, allocated on first use and
+// kept like the device pool) while the DMA of the previous piece runs on the worker's own stream.
+// Returns once every piece has landed.  (A pageable cudaMemcpyAsync stages through one driver
+// buffer serially: ~7 GB/s measured for the forest upload.)
+struct Xfer {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+constexpr int PIN_WORKERS = 8;
+constexpr size_t PIN_PIECE = (size_t)16 << 20;
+struct PinnedPool {
+    std::mutex m;
+    char *buf[PIN_WORKERS][2] = {};
+    bool ok = false;
+};
+PinnedPool g_pin;
+
+cudaError_t copy_many(const std::vector<Xfer> &xs, int device, cudaMemcpyKind kind) {
+    std::lock_guard<std::mutex> lock(g_pin.m);
+    if (!g_pin.ok) {
+        for (int w = 0; w < PIN_WORKERS; w++)
+            for (int b = 0; b < 2; b++) {
+                cudaError_t e = cudaHostAlloc((void **)&g_pin.buf[w][b], PIN_PIECE, cudaHostAllocPortable);
+                if (e != cudaSuccess) return e;
+            }
+        g_pin.ok = true;
+    }
+    struct Piece { const Xfer *x; size_t off, len; };
+    std::vector<Piece> pieces;
+    for (const Xfer &x : xs)
+        for (size_t off = 0; off < x.bytes; off += PIN_PIECE) pieces.push_back({&x, off, std::min(PIN_PIECE, x.bytes - off)});
+    if (pieces.empty()) return cudaSuccess;
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{(int)cudaSuccess};
+    const bool h2d = kind == cudaMemcpyHostToDevice;
+    auto worker = [&](int w) {
+        cudaError_t e = cudaSetDevice(device);
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        for (int b = 0; b < 2 && e == cudaSuccess; b++) e = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming);
+        bool used[2] = {false, false};
+        const Piece *pend[2] = {nullptr, nullptr};   // D2H: piece waiting in buffer b
+        int b = 0;
+        for (size_t i; e == cudaSuccess && (i = next.fetch_add(1)) < pieces.size(); b ^= 1) {
+            const Piece &pc = pieces[i];
+            if (used[b]) {
+                e = cudaEventSynchronize(ev[b]);
+                if (e == cudaSuccess && !h2d && pend[b])
+                    std::memcpy((char *)pend[b]->x->dst + pend[b]->off, g_pin.buf[w][b], pend[b]->len);
+            }
+            if (e != cudaSuccess) break;
+            if (h2d) {
+                std::memcpy(g_pin.buf[w][b], (const char *)pc.x->src + pc.off, pc.len);
+                e = cudaMemcpyAsync((char *)pc.x->dst + pc.off, g_pin.buf[w][b], pc.len, kind, st);
+            } else {
+                e = cudaMemcpyAsync(g_pin.buf[w][b], (const char *)pc.x->src + pc.off, pc.len, kind, st);
+                pend[b] = &pc;
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(ev[b], st);
+            used[b] = true;
+        }
+        for (int k = 0; k < 2 && e == cudaSuccess; k++)
+            if (used[k]) {
+                e = cudaEventSynchronize(ev[k]);
+                if (e == cudaSuccess && !h2d && pend[k])
+                    std::memcpy((char *)pend[k]->x->dst + pend[k]->off, g_pin.buf[w][k], pend[k]->len);
+            }
+        for (int k = 0; k < 2; k++) if (ev[k]) cudaEventDestroy(ev[k]);
+        if (st) cudaStreamDestroy(st);
+        if (e != cudaSuccess) err.store((int)e);
+    };
+    const int nw = (int)std::min<size_t>(PIN_WORKERS, pieces.size());
+    std::vector<std::thread> th;
+    for (int w = 1; w < nw; w++) th.emplace_back(worker, w);
+    worker(0);
+    for (auto &t : th) t.join();
+    return (cudaError_t)err.load();
 }
 
 // Run f(t, begin, end) on nthr threads over contiguous blocks [n*t/nthr, n*(t+1)/nthr).
@@ -934,11 +1022,16 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (const char *e = getenv("GAPLA_GROUP_NMAX_LAT")) group_nmax_lat = std::max(1, std::min(65535, atoi(e)));
     if (const char *e = getenv("GAPLA_GROUP_NMAX_THR")) group_nmax_thr = std::max(1, std::min(65535, atoi(e)));
     std::vector<int32_t> nmax_of_batch;       // filled once the batches are known
+    // nets whose group-path state exceeds a warp arena, once per net (in parallel)
+    std::vector<uint8_t> over_arena(N, 0);
+    if (ctx->group_path)
+        par_for(N, nthr, [&](int64_t net) {
+            over_arena[net] = assign_group_net_bytes((int)nnodes_of(net), (int)nsinks_of(net), ctx->L, ctx->LD) >
+                              (size_t)ctx->warp_arena;
+        });
     auto is_big = [&](int64_t net, int32_t b) {
         if (!ctx->group_path) return is_big_flow(net);
-        return nnodes_of(net) > nmax_of_batch[b] ||
-               assign_group_net_bytes((int)nnodes_of(net), (int)nsinks_of(net), ctx->L, ctx->LD) >
-                   (size_t)ctx->warp_arena;
+        return nnodes_of(net) > nmax_of_batch[b] || over_arena[net] != 0;
     };
     for (int64_t net = 0; net < N; net++)
         if (nnodes_of(net) >= 65535 || nsinks_of(net) >= 65535)
@@ -1132,16 +1225,16 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
                 max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
             } else {
                 small_pos.push_back((int32_t)p);
-                const int64_t net = pos_net[p];
-                if (is_big_flow(net)) {   // a big net of the dataflow kernel (k_assign)
-                    max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
-                    max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
-                }
             }
         }
         ctx->batch_big0.push_back((int64_t)big_pos.size());
         ctx->batch_small0.push_back((int64_t)small_pos.size());
     }
+    for (int64_t net = 0; net < N; net++)   // the dataflow kernel's (k_assign) big nets: input order, sequential
+        if (is_big_flow(net)) {
+            max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
+            max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
+        }
     phase("role lists");
     // dataflow DAG in forest order (snapshot batches: none -- every net has 0 predecessors)
     if (snapshot) {
@@ -1208,6 +1301,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
 
     ForestSrc src{};
     std::vector<void *> raw;                                // input-order device copies, freed below
+    std::vector<Xfer> xfers;                                // their uploads (pipelined, below)
     auto raw_up = [&](auto member, const std::vector<int64_t> &base, int per, auto **dst) -> cudaError_t {
         using T = typename std::remove_reference<decltype(chunks[0].acc.*member)>::type::value_type;
         T *d = nullptr;
@@ -1217,8 +1311,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         for (int64_t c = 0; c < nchunks; c++) {
             const auto &v = chunks[c].acc.*member;
             if (v.empty()) continue;
-            e = cudaMemcpyAsync(d + base[c] * per, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx->stream);
-            if (e != cudaSuccess) return e;
+            xfers.push_back({d + base[c] * per, v.data(), sizeof(T) * v.size()});
             ctx->stats.h2d_bytes += (int64_t)(sizeof(T) * v.size());
         }
         *dst = d;
@@ -1232,6 +1325,8 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     CK(raw_up(&BuiltNet::wd, cnode, 1, &src.wd)); CK(raw_up(&BuiltNet::ur, cnode, 1, &src.ur));
     CK(raw_up(&BuiltNet::p_layer, csink, 1, &src.p_layer)); CK(raw_up(&BuiltNet::p_cap, csink, 1, &src.p_cap));
     CK(raw_up(&BuiltNet::p_w, csink, 1, &src.p_w)); CK(raw_up(&BuiltNet::p_orig, csink, 1, &src.p_orig));
+    CK(cudaStreamSynchronize(ctx->stream));                 // the allocations above precede the copies
+    CK(copy_many(xfers, ctx->device, cudaMemcpyHostToDevice));
     int64_t *d_srcn = nullptr, *d_srcs = nullptr, *d_dsts = nullptr;
     CK(dmalloc(&d_srcn, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcn);
     CK(dmalloc(&d_srcs, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcs);
@@ -1511,6 +1606,7 @@ la_status la_assign_batch(la_ctx *ctx, int32_t batch) {
     const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
     if (ctx->world > 1 || ctx->nccl)   // other ranks' net costs arrive through the reconcile sum
         CK(cudaMemsetAsync(ctx->S.froot + b0, 0, sizeof(double) * (b1 - b0), ctx->stream));
+    ctx->sol_valid = false;
     AssignLaunch al = assign_launch(ctx);
     const RankShare r = rank_share(ctx, batch);
     al.big_beg = r.big_beg; al.big_end = r.big_end; al.small_beg = r.small_beg; al.small_end = r.small_end;
@@ -1595,6 +1691,7 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
     TRY(check_ready(ctx));
     if (!ctx->pending_commit || batch != ctx->next_batch)
         return set_err(LA_ESTATE, "commit must follow the assignment of the same batch");
+    ctx->sol_valid = false;
     const int64_t b0 = ctx->batch_net0[batch], b1 = ctx->batch_net0[batch + 1];
     const int64_t n0 = ctx->h_net_node0[b0], n1 = ctx->h_net_node0[b1];
     if (ctx->host_xport) {
@@ -1724,6 +1821,7 @@ la_status la_assign_all(la_ctx *ctx) {
         ctx->next_batch == 0 && !ctx->flow_dirty) {
         // one persistent launch over every net, in bottom-level priority order
         TRY(build_flow_lists(ctx));
+        ctx->sol_valid = false;
         AssignLaunch al = assign_launch(ctx);
         al.big_pos = ctx->d_flow_big_pos;
         al.small_pos = ctx->d_flow_small_pos;
@@ -1902,20 +2000,21 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
                           int64_t *via_ptr, int32_t *vias, double *net_cost) {
     TRY(require_done(ctx));
     const int64_t N = ctx->n_nets, NN = ctx->n_nodes;
-    std::vector<uint8_t> lay(NN), sb(NN), st(NN);
-    std::vector<double> froot(N);
-    if (NN) {
-        CK(cudaMemcpyAsync(lay.data(), ctx->S.lay, NN, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(sb.data(), ctx->S.sb, NN, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(st.data(), ctx->S.st, NN, cudaMemcpyDeviceToHost, ctx->stream));
-    }
-    if (N) CK(cudaMemcpyAsync(froot.data(), ctx->S.froot, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<uint8_t> &lay = ctx->sol_lay, &sb = ctx->sol_sb, &st = ctx->sol_st;
+    std::vector<double> &froot = ctx->sol_froot;
+    std::vector<int64_t> &nw = ctx->sol_nw, &nv = ctx->sol_nv, &pos_of = ctx->sol_pos_of;
+    if (!ctx->sol_valid) {
+    lay.resize(NN); sb.resize(NN); st.resize(NN);
+    froot.resize(N);
     CK(cudaStreamSynchronize(ctx->stream));
+    CK(copy_many({{lay.data(), ctx->S.lay, (size_t)NN}, {sb.data(), ctx->S.sb, (size_t)NN}, {st.data(), ctx->S.st, (size_t)NN},
+                  {froot.data(), ctx->S.froot, sizeof(double) * N}}, ctx->device, cudaMemcpyDeviceToHost));
     ctx->stats.d2h_bytes += 3 * NN + 8 * N;
     // per input net: counts (threads over positions)
-    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-    std::vector<int64_t> nw(N + 1, 0), nv(N + 1, 0);
-    std::vector<int64_t> pos_of(N);
+    nw.assign(N + 1, 0);
+    nv.assign(N + 1, 0);
+    pos_of.resize(N);
     std::vector<int64_t> vc_part(nthr + 1, 0);
     {
         std::vector<std::thread> th;
@@ -1942,6 +2041,8 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     for (unsigned t = 0; t < nthr; t++) vcuts += vc_part[t];
     ctx->stats.via_cuts = vcuts;
     for (int64_t i = 0; i < N; i++) { nw[i + 1] += nw[i]; nv[i + 1] += nv[i]; }
+    ctx->sol_valid = true;
+    }
     if (n_wires) *n_wires = nw[N];
     if (n_vias) *n_vias = nv[N];
     if (wire_ptr) std::memcpy(wire_ptr, nw.data(), sizeof(int64_t) * (N + 1));
@@ -2014,6 +2115,7 @@ la_status la_get_batches(la_ctx *ctx, int32_t *batch_of) {
 
 la_status la_reset(la_ctx *ctx) {
     TRY(check_ready(ctx));
+    ctx->sol_valid = false;
     size_t bH = sizeof(int32_t) * (size_t)(ctx->X - 1) * ctx->Y * ctx->LH;
     size_t bV = sizeof(int32_t) * (size_t)ctx->X * (ctx->Y - 1) * ctx->LV;
     size_t bVia = sizeof(int32_t) * (size_t)ctx->n_via_api;
