@@ -729,6 +729,66 @@ bool checked_tree(Ctx &C, const ONets *nets, int64_t net, Tree &T, char *err) {
     return ok;
 }
 
+// Per-direction average unit R / C of the pre-assignment parasitics (PAPER §III-B l.283-285:
+// "For horizontal (vertical) wire connections, we calculate resistance (capacitance) using the
+// average per-unit-length resistance (capacitance) of all horizontal (vertical) wires";
+// reading R44: the plain mean over the routable layers of that direction, summed in ascending l).
+double dir_mean(const OGrid *g, const double *v, int d) {
+    double s = 0.0;
+    int cnt = 0;
+    for (int l = 0; l < g->L; l++)
+        if (g->routable[l] && g->dir[l] == d) { s = s + v[l]; cnt++; }
+    return cnt ? s / (double)cnt : 0.0;
+}
+
+// Pre-assignment timing of ONE net on its 2D LA tree with the pi-model (PAPER §III-B l.283-286,
+// Alg. 1 inputs r_avg / c_avg l.240-241; reading R44), written as the
+// definition of the Elmore delay:
+//   edge into node n (n != root): R_n = r_dir(n) * len_n, C_n = c_dir(n) * len_n (dir: E/W = H);
+//   pi-model node capacitance Cnode(u) = sum of u's sink pin caps (input order; the driver pin
+//     has none) + C_u / 2 (u != root) + sum over u's sons s of C_s / 2 (child order);
+//   Elmore delay of node v = sum over the edges n on the path root -> v of
+//     R_n * (sum of Cnode(u) over the nodes u of subtree(n)), subtree membership tested by
+//     walking u's ancestors (no recursion);
+//   sink delay = the delay of its node; net load cap = sum of Cnode(u) over all nodes.
+void pre_timing_net(const ONets *N, int64_t drv, const Tree &T, const double rd[2], const double cd[2],
+                    double *sink_delay, double *net_cap) {
+    const int nn = (int)T.x.size();
+    std::vector<double> Rn(nn, 0.0), Cn(nn, 0.0), Cnode(nn, 0.0), down(nn, 0.0), D(nn, 0.0);
+    for (int n = 0; n < nn; n++)
+        if (T.par[n] >= 0) {
+            const int t = edge_dir_type(T.edir[n]);
+            Rn[n] = rd[t] * (double)T.len[n];
+            Cn[n] = cd[t] * (double)T.len[n];
+        }
+    for (int u = 0; u < nn; u++) {
+        double c = 0.0;
+        for (int64_t q : T.pins[u]) if (q != drv) c = c + N->pin_cap[q];
+        if (T.par[u] >= 0) c = c + 0.5 * Cn[u];
+        for (int s : T.kids[u]) c = c + 0.5 * Cn[s];
+        Cnode[u] = c;
+    }
+    double tot = 0.0;
+    for (int u = 0; u < nn; u++) tot = tot + Cnode[u];
+    for (int a = 0; a < nn; a++) {             // down(a) = sum of Cnode over subtree(a), by membership
+        double s = 0.0;
+        for (int u = 0; u < nn; u++) {
+            int w = u;
+            while (w >= 0 && w != a) w = T.par[w];
+            if (w == a) s = s + Cnode[u];
+        }
+        down[a] = s;
+    }
+    for (int v = 0; v < nn; v++) {             // D(v) = sum over the path root -> v of R_n * down(n)
+        double d = 0.0;
+        for (int w = v; T.par[w] >= 0; w = T.par[w]) d = d + Rn[w] * down[w];
+        D[v] = d;
+    }
+    for (int n = 0; n < nn; n++)
+        for (int64_t q : T.pins[n]) sink_delay[q] = (q == drv) ? 0.0 : D[n];
+    *net_cap = tot;
+}
+
 // footprint(j) = unit 2D edges of its route U GCells of its LA nodes; element spaces disjoint
 // (SURVEY §8(c) c.2).
 void footprint(const Ctx &C, const Tree &T, std::vector<int64_t> &fp) {
@@ -740,6 +800,25 @@ void footprint(const Ctx &C, const Tree &T, std::vector<int64_t> &fp) {
 }  // namespace
 
 extern "C" {
+
+// Pre-assignment pi-model timing of every net (pre_timing_net above).  r_h / r_v / c_h / c_v:
+// per-direction unit R (kOhm) / C (fF); NaN = the mean over that direction's routable layers
+// (dir_mean).  Outputs sink_delay[n_pins] (driver slots 0, ps) and net_cap[n_nets] (fF).
+int oracle_pre_timing(const OGrid *g, const ONets *nets, double r_h, double r_v, double c_h, double c_v,
+                      double *sink_delay, double *net_cap, char *err) {
+    Ctx C;
+    C.g = g; C.nets = nets; C.X = g->X; C.Y = g->Y; C.L = g->L;
+    char buf[256] = {0};
+    C.err = buf;
+    const double rd[2] = {std::isnan(r_h) ? dir_mean(g, g->r, 0) : r_h, std::isnan(r_v) ? dir_mean(g, g->r, 1) : r_v};
+    const double cd[2] = {std::isnan(c_h) ? dir_mean(g, g->c, 0) : c_h, std::isnan(c_v) ? dir_mean(g, g->c, 1) : c_v};
+    for (int64_t net = 0; net < nets->n_nets; net++) {
+        Tree T;
+        if (!checked_tree(C, nets, net, T, err)) return -1;
+        pre_timing_net(nets, nets->pin_ptr[net], T, rd, cd, sink_delay, net_cap + net);
+    }
+    return 0;
+}
 
 int oracle_run(const OGrid *g, const ONets *nets, OOut *out) {
     Ctx C;

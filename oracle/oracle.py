@@ -71,6 +71,9 @@ def _load():
         _lib.oracle_net_dp.argtypes = [P(OGrid), P(ONets), c_i64, c_i32, P(c_i32), P(c_f64), P(c_f64), P(c_f64),
                                        P(c_f64), P(c_f64), P(c_i32), P(c_i32), P(c_i32), ctypes.c_char_p]
         _lib.oracle_net_dp.restype = ctypes.c_int
+        _lib.oracle_pre_timing.argtypes = [P(OGrid), P(ONets), c_f64, c_f64, c_f64, c_f64, P(c_f64), P(c_f64),
+                                           ctypes.c_char_p]
+        _lib.oracle_pre_timing.restype = ctypes.c_int
     return _lib
 
 
@@ -225,6 +228,26 @@ def net_dp(d, net: int) -> dict:
         raise OracleError(err.value.decode())
     k = cnt.value
     return dict(ur=ur[:k], wd=wd[:k], f=f[:k], dlc=dlc[:k], gp=gp[:k], cb=cb[:k], ct=ct[:k], entry=entry[:k])
+
+
+def pre_timing(d, r_h: float = float("nan"), r_v: float = float("nan"), c_h: float = float("nan"),
+               c_v: float = float("nan")):
+    """Pre-assignment pi-model timing on the 2D LA trees (PAPER §III-B l.283-286, Alg. 1 inputs
+    r_avg / c_avg l.240-241; reading R44): per-direction unit R / C (NaN =
+    mean over that direction's routable layers), definitional Elmore (la_oracle.cpp
+    pre_timing_net).  Returns (sink_delay[n_pins] ps, driver slots 0; net_cap[n_nets] fF)."""
+    lib = _load()
+    keep = []
+    g = _grid(d, keep)
+    n = _nets(d, keep)
+    delay = np.zeros(int(d.pin_ptr[-1]), np.float64)
+    cap = np.zeros(d.n_nets, np.float64)
+    err = ctypes.create_string_buffer(256)
+    rc = lib.oracle_pre_timing(ctypes.byref(g), ctypes.byref(n), r_h, r_v, c_h, c_v, _ptr(delay, c_f64),
+                               _ptr(cap, c_f64), err)
+    if rc != 0:
+        raise OracleError(err.value.decode())
+    return delay, cap
 
 
 def evaluate(d, wire_dem, via_dem, wires, vias) -> dict:
