@@ -45,6 +45,7 @@ def parse():
                     help="conflict-free batches (exact sequential semantics, default) or the paper's Alg. 1 "
                          "snapshot batches (NEXT #1/#2, synthetic criticality)")
     ap.add_argument("--max-batch", type=int, default=1 << 18, help="Alg. 1 GetBatches size cap (paper batching)")
+    ap.add_argument("--no-pre", action="store_true", help="skip the NEXT #2 measurements (pre-timing, Alg. 1)")
     ap.add_argument("--ncu-pass", action="store_true",
                     help="setup + 1 warm step, then ONE step between cudaProfilerStart/Stop (for ncu)")
     return ap.parse_args()
@@ -194,6 +195,44 @@ def cpu_baseline_mode2(d, seconds, rate1):
                        f"DP+backtrack+commit+Elmore, tree build excluded")}
 
 
+def pre_assignment(args, A, d, la, crit, st, hbm):
+    """SURVEY §8(f) NEXT #2, outside the step: the pre-assignment pi-model timing on the 2D trees
+    (la_pre_timing, k_pre_timing) and Alg. 1 lines 3-10 (la_paper_batches), each timed W + K times
+    with CUDA events on the library stream.  Algorithmic bytes:
+      k_pre_timing: 30 per node (kid 16, len 4, sink0 4, height 2, nsink 2, nkid 1, edir 1)
+                    + 24 per sink (cap, input index, delay out) + 24 per net (node range, id, cap out)
+      Alg. 1 kernels: 24 per net (pin_ptr, seg_ptr, criticality, batch id out) + 8 per pin (slack)
+                    + 16 per segment (x1 y1 x2 y2); the two radix passes are implementation traffic."""
+    n_pins = int(d.pin_ptr[-1])
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            A.profiling(True)
+            A.profile(reset=True)
+        la.la_pre_timing(A.ctx, n_pins, d.n_nets)
+    p1 = A.profile(reset=True)
+    pt_ms = p1["pretime_ms"] / max(p1["pretime_launches"], 1)
+    pt_bytes = 30 * st["n_nodes"] + 24 * st["n_sinks"] + 24 * d.n_nets
+    nb_paper = None
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            A.profile(reset=True)
+        _, nb_paper = la.la_paper_batches(A.ctx, d, crit, 0.7, 3, args.max_batch)
+    p2 = A.profile(reset=True)
+    A.profiling(False)
+    calls = max(p2["order_calls"], 1)
+    ok_ms, oc_ms = p2["order_kernel_ms"] / calls, p2["order_ms"] / calls
+    or_bytes = 24 * d.n_nets + 8 * n_pins + 16 * int(d.seg_ptr[-1])
+    return {"pre_timing": {"kernel": "k_pre_timing (pi-model Elmore on the 2D trees, per-direction r_avg/c_avg)",
+                           "bound": "hbm", "ms": pt_ms, "alg_bytes": pt_bytes,
+                           "achieved": pt_bytes / (pt_ms / 1e3) / 1e9 if pt_ms else None, "peak": hbm,
+                           "unit": "GB/s", "frac": pt_bytes / (pt_ms / 1e3) / 1e9 / hbm if pt_ms else None},
+            "paper_batches": {"kernels": "k_crit_max, k_order_keys, 2 x CUB radix SortPairs, scans, k_batch_*",
+                              "bound": "hbm", "kernel_ms": ok_ms, "call_ms_with_h2d": oc_ms, "alg_bytes": or_bytes,
+                              "achieved": or_bytes / (ok_ms / 1e3) / 1e9 if ok_ms else None, "peak": hbm,
+                              "unit": "GB/s", "frac": or_bytes / (ok_ms / 1e3) / 1e9 / hbm if ok_ms else None,
+                              "batches": nb_paper, "max_batch": args.max_batch}}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, rank, world, local_rank):
     import numpy as np
@@ -223,10 +262,11 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     snap = None
-    if args.batching == "paper":
-        snap, _ = la.la_paper_batches(d, synth.criticality(d), 0.7, 3, args.max_batch)
     t_setup = time.perf_counter()
     A = la.LayerAssigner(d, device=local_rank, rank=rank, world=world, nccl_id=nid, stream=stream.cuda_stream)
+    crit = synth.criticality(d) if (args.batching == "paper" or not args.no_pre) else None
+    if args.batching == "paper":
+        snap, _ = la.la_paper_batches(A.ctx, d, crit, 0.7, 3, args.max_batch)   # Alg. 1 l.3-10 on the GPU
     nb = A.load(snapshot_batches=snap)
     setup_s = time.perf_counter() - t_setup
     st0 = A.stats()
@@ -323,6 +363,7 @@ def run_ours(args, rank, world, local_rank):
     # st, edir (u8) and len (i32) per node as well
     ev_bytes = 4 * (int(sum(d.wire_layer_sizes())) + d.X * d.Y * (d.L - 1)) + \
         (8 * st["n_nodes"] if ev_res["out_of_domain"] else 0)
+    pre = None if args.no_pre else pre_assignment(args, A, d, la, crit, st, hbm)
     A.close()
     evaluator = {"kernel": "k_eval_plane x3 (NEXT #3: Eq. (3)/(2) overflow; wirelength and via cuts from the "
                            "same histograms)",
@@ -382,7 +423,7 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"dp{world}: nets of every conflict-free batch sharded over {world} GPU(s)",
                        "l2": f"inputs > L2: {(4 * (st['via_state_words'] + st['wire_state_words']) + 50 * st['n_nodes']) / 1e9:.2f} GB touched per step",
                        "setup_s": setup_s, "load_ms": st0["load_ms"], "batching_ms": st0["batch_ms"]},
-            "roofline": roof, "roofline_step": roof_step, "evaluator": evaluator,
+            "roofline": roof, "roofline_step": roof_step, "evaluator": evaluator, "pre_assignment": pre,
             "cpu_baseline": cpu, "cpu_baseline_mode2": cpu2, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(out), flush=True)

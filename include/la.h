@@ -128,6 +128,9 @@ typedef struct {
     double assign_ms, commit_ms, elmore_ms, reconcile_ms;
     int64_t eval_launches;
     double eval_ms;
+    int64_t pretime_launches, order_calls;   /* la_pre_timing kernels; la_paper_batches calls          */
+    double pretime_ms, order_ms;             /* order_ms: the whole call (host->device copies included) */
+    double order_kernel_ms;                  /* la_paper_batches' kernels and sorts alone                */
 } la_profile;
 
 /* Evaluation of a 3D solution (la_eval_overflow).
@@ -236,10 +239,11 @@ la_status la_assign_all(la_ctx *ctx);
  * descriptor's is reported by la_load_nets (LA_EINVAL). */
 la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t n_nets);
 
-/* Alg. 1 lines 3-10 (PAPER §III-A l.213-262): critical-net-analysis
- * based ordering and batching, given what Alg. 1 lines 1-2 (STA) produce.  Inputs: the net
- * descriptor (its pin slacks and wns), criticality[n_nets] = number of critical paths through
- * each net (l.208), alpha (semi-critical ratio, 0.7, l.216-218) and th (3, l.215).  Steps:
+/* Alg. 1 lines 3-10 on the GPU (PAPER §III-A l.213-262):
+ * critical-net-analysis based ordering and batching, given what Alg. 1 lines 1-2 (STA)
+ * produce.  Inputs: the net descriptor (its pin slacks, segments and wns), criticality[n_nets]
+ * = number of critical paths through each net (l.208), alpha (semi-critical ratio, 0.7,
+ * l.216-218) and th (3, l.215).  Steps:
  *   Divide (l.3): critical nets N_c: criticality > th; semi-critical N_s: the rest with net
  *     slack (minimum over the net's sink slacks, l.217) < alpha * wns; non-critical N_n.
  *   PartitionAndSort(N_c) (l.4, l.228): bands [C, C], [C/2, C), [C/4, C/2), ... of
@@ -248,14 +252,36 @@ la_status la_set_snapshot_batches(la_ctx *ctx, const int32_t *batch_of, int64_t 
  *   PartitionAndSort(N_s) (l.5, l.229, reading R33): bands slack == wns, then
  *     (f_{k-1} wns, f_k wns] with f_k = 1 - 0.01 k^2 (1, 0.99, 0.96, 0.91, ...; reading R42)
  *     down to alpha * wns; inside a band net slack ascending, net index.
- *   Sort(N_n) (l.6, l.230 "congestion-driven"; reading R43): 2D wirelength ascending, index.
+ *   Sort(N_n) (l.6, l.230 "congestion-driven"; reading R43): 2D wirelength (sum of the
+ *     segments' lengths) ascending, index.
  *   GetBatches (l.7-9, reading R31): every band (and N_n) cut in its order into batches of
  *     at most max_batch nets; Concat (l.10): N_c's, then N_s's, then N_n's.
- * Output: batch_of[n_nets] (input order), *n_batches; feed them to la_set_snapshot_batches.
- * Host code, multithreaded sorts; no context needed.  Errors: LA_EINVAL on NULL arrays,
- * alpha <= 0, max_batch < 1 or a negative criticality. */
-la_status la_paper_batches(const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
+ * Runs on ctx's device and stream (any state after la_init_grid; the context's nets are not
+ * used or changed): the descriptor's pin_ptr, pin_slack, seg_ptr, seg_xy and criticality are
+ * copied to the device, per-net keys and bands are formed by hand-written kernels, two stable
+ * radix passes (CUB) order the nets and a scan forms the batches.  Output: batch_of[n_nets]
+ * (input order, caller-owned host memory), *n_batches; feed them to la_set_snapshot_batches.
+ * Errors: LA_EINVAL on NULL arrays, alpha <= 0, th < 0, max_batch < 1, a negative criticality
+ * or n_nets >= 2^31; LA_ECUDA (poisons the context). */
+la_status la_paper_batches(la_ctx *ctx, const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
                            int64_t max_batch, int32_t *batch_of, int32_t *n_batches);
+
+/* Pre-assignment timing on the 2D LA trees (PAPER §III-B l.283-286:
+ * "For horizontal (vertical) wire connections, we calculate resistance (capacitance) using
+ * the average per-unit-length resistance (capacitance) of all horizontal (vertical) wires ...
+ * the widely adopted pi-model"; Alg. 1 inputs r_avg, c_avg l.240-241; reading R44).  Every
+ * LA-tree edge of direction t and length len is a pi section R = r_t len, C = c_t len (C/2 at
+ * each end); sinks hang on their node through zero-resistance edges (l.284).  Outputs (either
+ * may be NULL): sink_delay[n_pins] = the Elmore wire delay from the driver's node to the
+ * sink's node (ps, input pin order, driver slots 0) and net_cap[n_nets] = the net's total load
+ * capacitance (wires + sinks, fF) — the parasitics the STA of Alg. 1 line 1 consumes (the STA
+ * is out of scope).  r_h, r_v (kOhm per GCell), c_h, c_v (fF per GCell): per-direction unit
+ * values; NaN = the mean of r (c) over the routable layers of that direction (R44).
+ * Requires la_load_nets (runs on the resident forest; independent of the batching and of any
+ * assignment).  Synchronises.  Not collective: every rank evaluates every net.  Errors:
+ * LA_ESTATE before la_load_nets, LA_EINVAL for a negative unit value. */
+la_status la_pre_timing(la_ctx *ctx, double r_h, double r_v, double c_h, double c_v, double *sink_delay,
+                        double *net_cap);
 
 /* Schedule used by la_assign_all on one rank; automatic until set. */
 enum { LA_SCHED_DATAFLOW = 0, LA_SCHED_BATCH = 1 };

@@ -165,6 +165,8 @@ struct la_ctx {
     std::vector<int4> h_jobs;                 // this rank's jobs (k_assign_g), batch by batch
     std::vector<int64_t> batch_job0;          // [n_batches+1]
     int4 *d_jobs = nullptr;
+    int4 *d_chunks = nullptr;                 // chunks of the tree passes (build_chunks), in dev_allocs
+    int64_t n_chunks = 0;
     int64_t n_flow_big = 0, n_flow_small = 0; // dataflow role lists (k_assign's NS / NP roles)
     int32_t n_big_ctas_flow = 0;              // big-net CTAs of the dataflow launch
     std::vector<int32_t> batch_of_net;        // input order
@@ -244,7 +246,8 @@ la_status dev_upload(la_ctx *ctx, T **dst, const T *src, size_t n) {
     return LA_OK;
 }
 
-enum { K_ASSIGN = 0, K_COMMIT = 1, K_ELMORE = 2, K_RECONCILE = 3, K_EVAL = 4 };
+enum { K_ASSIGN = 0, K_COMMIT = 1, K_ELMORE = 2, K_RECONCILE = 3, K_EVAL = 4, K_PRETIME = 5, K_ORDER = 6,
+       K_ORDER_KERNELS = 7 };
 
 // Profiling brackets: record a CUDA event before / after a launch on the context stream.
 int prof_begin(la_ctx *ctx, int kind) {
@@ -1850,82 +1853,115 @@ la_status la_assign_all(la_ctx *ctx) {
     return LA_OK;
 }
 
-la_status la_paper_batches(const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
+la_status la_paper_batches(la_ctx *ctx, const la_net_desc *n, const int32_t *criticality, double alpha, int32_t th,
                            int64_t max_batch, int32_t *batch_of, int32_t *n_batches) {
+    if (!ctx) return set_err(LA_EINVAL, "null context");
+    if (ctx->poisoned) return set_err(LA_ESTATE, "context poisoned by an earlier CUDA/NCCL error");
     if (!n || !criticality || !batch_of || !n_batches) return set_err(LA_EINVAL, "null argument");
-    if (!(alpha > 0.0) || max_batch < 1) return set_err(LA_EINVAL, "alpha must be > 0 and max_batch >= 1");
+    if (!(alpha > 0.0) || max_batch < 1 || th < 0) return set_err(LA_EINVAL, "alpha must be > 0, th >= 0, max_batch >= 1");
     const int64_t N = n->n_nets;
-    if (N > 0 && (!n->pin_ptr || !n->pin_slack || !n->seg_ptr)) return set_err(LA_EINVAL, "bad net descriptor");
-    const double wns = n->wns;
-    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-    std::vector<double> slack(N);
-    std::vector<int64_t> wl(N);
-    par_for(N, nthr, [&](int64_t j) {
-        double m = std::numeric_limits<double>::infinity();
-        for (int64_t p = n->pin_ptr[j] + 1; p < n->pin_ptr[j + 1]; p++) m = std::min(m, n->pin_slack[p]);   // sinks
-        slack[j] = m;
-        int64_t w = 0;
-        for (int64_t s = n->seg_ptr[j]; s < n->seg_ptr[j + 1]; s++) {
-            const int32_t *q = n->seg_xy + 4 * s;
-            w += std::abs(q[2] - q[0]) + std::abs(q[3] - q[1]);
-        }
-        wl[j] = w;
-    });
+    if (N < 0 || N >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "net count out of range");
+    if (N > 0 && (!n->pin_ptr || !n->pin_slack || !n->seg_ptr || !n->seg_xy)) return set_err(LA_EINVAL, "bad net descriptor");
     for (int64_t j = 0; j < N; j++)
         if (criticality[j] < 0) return set_err(LA_EINVAL, "negative criticality");
-    // Divide (l.3): band key per net; (class, band) sorts the subsets in Concat order
-    int32_t C = 0;
-    for (int64_t j = 0; j < N; j++) if (criticality[j] > th) C = std::max(C, criticality[j]);
-    struct Item { int32_t cls, band; int64_t key1; double key2; int64_t idx; };
-    std::vector<Item> it(N);
-    par_for(N, nthr, [&](int64_t j) {
-        Item &x = it[j];
-        x.idx = j;
-        if (criticality[j] > th) {                               // N_c: bands [C/2^k, C/2^(k-1)), [C, C] first
-            x.cls = 0;
-            int b = 0;
-            if (criticality[j] < C) {
-                b = 1;
-                while ((double)criticality[j] < (double)C / std::ldexp(1.0, b)) b++;
-            }
-            x.band = b;
-            x.key1 = -(int64_t)criticality[j];
-            x.key2 = slack[j];
-        } else if (wns < 0.0 && slack[j] < alpha * wns) {       // N_s: bands of net slack (R33, R42)
-            x.cls = 1;
-            int b = 0;
-            if (!(slack[j] <= wns)) {
-                b = 1;
-                while (b < 10 && !(slack[j] <= (1.0 - 0.01 * b * b) * wns)) b++;
-            }
-            x.band = b;
-            x.key1 = 0;
-            x.key2 = slack[j];
-        } else {                                                 // N_n: congestion-driven (R43)
-            x.cls = 2;
-            x.band = 0;
-            x.key1 = wl[j];
-            x.key2 = 0.0;
+    *n_batches = 0;
+    if (N == 0) return LA_OK;
+    const int64_t NP = n->pin_ptr[N], NSG = n->seg_ptr[N];
+    CK(cudaSetDevice(ctx->device));
+    // inputs to the device (freed on return: this call keeps no state in the context)
+    int64_t *d_pp = nullptr, *d_sp = nullptr;
+    double *d_sl = nullptr;
+    int32_t *d_xy = nullptr, *d_cr = nullptr, *d_out = nullptr;
+    auto release = [&] { for (void *p : {(void *)d_pp, (void *)d_sp, (void *)d_sl, (void *)d_xy, (void *)d_cr, (void *)d_out}) dfree(p); };
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((e = dmalloc(&d_pp, 8 * (N + 1))) || (e = dmalloc(&d_sp, 8 * (N + 1))) || (e = dmalloc(&d_sl, 8 * NP)) ||
+            (e = dmalloc(&d_xy, 16 * NSG)) || (e = dmalloc(&d_cr, 4 * N)) || (e = dmalloc(&d_out, 4 * N)))
+            break;
+        const int pe = prof_begin(ctx, K_ORDER);
+        if ((e = copy_many({{d_pp, n->pin_ptr, 8 * (size_t)(N + 1)}, {d_sp, n->seg_ptr, 8 * (size_t)(N + 1)},
+                            {d_sl, n->pin_slack, 8 * (size_t)NP}, {d_xy, n->seg_xy, 16 * (size_t)NSG},
+                            {d_cr, criticality, 4 * (size_t)N}}, ctx->device, cudaMemcpyHostToDevice)))
+            break;
+        ctx->stats.h2d_bytes += 16 * (N + 1) + 8 * NP + 16 * NSG + 4 * N;
+        const int pk = prof_begin(ctx, K_ORDER_KERNELS);
+        OrderIn in{N, d_pp, d_sp, d_sl, d_xy, d_cr, n->wns, alpha, th, max_batch};
+        int32_t nb = 0;
+        if ((e = gpu_paper_batches(in, d_out, &nb, ctx->stream, &ctx->stats.launches))) break;
+        prof_end(ctx, pk);
+        if ((e = cudaMemcpyAsync(batch_of, d_out, 4 * N, cudaMemcpyDeviceToHost, ctx->stream))) break;
+        prof_end(ctx, pe);
+        if ((e = cudaStreamSynchronize(ctx->stream))) break;
+        ctx->stats.d2h_bytes += 4 * N;
+        *n_batches = nb;
+    } while (0);
+    release();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "la_paper_batches");
+    return LA_OK;
+}
+
+// Chunks of the tree passes (la_order.cu): consecutive forest positions packed into runs of at
+// most CHUNK_NODES nodes / CHUNK_SINKS sinks / 32 nets; a net beyond that is a chunk of its own.
+static la_status build_chunks(la_ctx *ctx) {
+    if (ctx->d_chunks) return LA_OK;
+    const int64_t N = ctx->n_nets;
+    std::vector<int4> ch;
+    ch.reserve((size_t)(N / 6 + 16));
+    int64_t p = 0;
+    while (p < N) {
+        const int64_t q0 = ctx->h_net_sink0[p];
+        int64_t nodes = 0, sinks = 0, k = 0;
+        while (p + k < N && k < 32) {
+            const int64_t a = ctx->h_net_node0[p + k + 1] - ctx->h_net_node0[p + k];
+            const int64_t b = ctx->h_net_sink0[p + k + 1] - ctx->h_net_sink0[p + k];
+            if (nodes + a > CHUNK_NODES || sinks + b > CHUNK_SINKS) break;
+            nodes += a;
+            sinks += b;
+            k++;
         }
-    });
-    par_sort(it, [](const Item &a, const Item &b) {
-        if (a.cls != b.cls) return a.cls < b.cls;
-        if (a.band != b.band) return a.band < b.band;
-        if (a.key1 != b.key1) return a.key1 < b.key1;
-        if (a.key2 != b.key2) return a.key2 < b.key2;
-        return a.idx < b.idx;
-    }, nthr);
-    // GetBatches (l.7-9) + Concat (l.10)
-    int32_t nb = 0;
-    int64_t in_batch = 0;
-    for (int64_t i = 0; i < N; i++) {
-        const bool new_subset = i > 0 && (it[i].cls != it[i - 1].cls || it[i].band != it[i - 1].band);
-        if (i == 0) nb = 1;
-        else if (new_subset || in_batch == max_batch) { nb++; in_batch = 0; }
-        batch_of[it[i].idx] = nb - 1;
-        in_batch++;
+        if (k == 0) {   // one net beyond a chunk
+            k = 1;
+            sinks = ctx->h_net_sink0[p + 1] - q0;
+        }
+        ch.push_back(make_int4((int)p, (int)k, (int)q0, (int)std::min<int64_t>(sinks, INT32_MAX)));
+        p += k;
     }
-    *n_batches = nb;
+    ctx->n_chunks = (int64_t)ch.size();
+    TRY(dev_upload(ctx, &ctx->d_chunks, ch.data(), ch.size()));
+    return LA_OK;
+}
+
+la_status la_pre_timing(la_ctx *ctx, double r_h, double r_v, double c_h, double c_v, double *sink_delay,
+                        double *net_cap) {
+    TRY(check_ready(ctx));
+    if (!(std::isnan(r_h) || r_h >= 0) || !(std::isnan(r_v) || r_v >= 0) || !(std::isnan(c_h) || c_h >= 0) ||
+        !(std::isnan(c_v) || c_v >= 0))
+        return set_err(LA_EINVAL, "negative unit R / C");
+    CK(cudaSetDevice(ctx->device));
+    TRY(build_chunks(ctx));
+    // per-direction averages over the routable layers (R44): plain mean, ascending l
+    PreRC P{};
+    const double give_r[2] = {r_h, r_v}, give_c[2] = {c_h, c_v};
+    for (int t = 0; t < 2; t++) {
+        double sr = 0.0, sc = 0.0;
+        int cnt = 0;
+        for (int l = 0; l < ctx->L; l++)
+            if (ctx->routable[l] && ctx->dir[l] == t) { sr = sr + ctx->r[l]; sc = sc + ctx->c[l]; cnt++; }
+        P.rd[t] = std::isnan(give_r[t]) ? (cnt ? sr / (double)cnt : 0.0) : give_r[t];
+        P.cd[t] = std::isnan(give_c[t]) ? (cnt ? sc / (double)cnt : 0.0) : give_c[t];
+    }
+    if (ctx->n_pins) CK(cudaMemsetAsync(ctx->S.sink_delay, 0, sizeof(double) * ctx->n_pins, ctx->stream));
+    const int pe = prof_begin(ctx, K_PRETIME);
+    CK(launch_pre_timing(ctx->F, ctx->d_chunks, ctx->n_chunks, P, ctx->S.Cd, ctx->S.Tin, ctx->S.sink_delay,
+                         ctx->S.net_cap, ctx->stream));
+    prof_end(ctx, pe);
+    ctx->stats.launches += 1;
+    if (sink_delay && ctx->n_pins)
+        CK(cudaMemcpyAsync(sink_delay, ctx->S.sink_delay, sizeof(double) * ctx->n_pins, cudaMemcpyDeviceToHost, ctx->stream));
+    if (net_cap && ctx->n_nets)
+        CK(cudaMemcpyAsync(net_cap, ctx->S.net_cap, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stats.d2h_bytes += (sink_delay ? 8 * ctx->n_pins : 0) + (net_cap ? 8 * ctx->n_nets : 0);
     return LA_OK;
 }
 
@@ -2157,6 +2193,9 @@ la_status la_get_profile(la_ctx *ctx, la_profile *out, int32_t reset) {
             case K_COMMIT: ctx->acc.commit_ms += ms; ctx->acc.commit_launches++; break;
             case K_ELMORE: ctx->acc.elmore_ms += ms; ctx->acc.elmore_launches++; break;
             case K_EVAL: ctx->acc.eval_ms += ms; ctx->acc.eval_launches++; break;
+            case K_PRETIME: ctx->acc.pretime_ms += ms; ctx->acc.pretime_launches++; break;
+            case K_ORDER: ctx->acc.order_ms += ms; ctx->acc.order_calls++; break;
+            case K_ORDER_KERNELS: ctx->acc.order_kernel_ms += ms; break;
             default: ctx->acc.reconcile_ms += ms; ctx->acc.reconcile_calls++; break;
         }
         ctx->ev_pool.push_back(sp.a);

@@ -175,6 +175,29 @@ cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64
 cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
                           int64_t net_end, const int32_t *list, cudaStream_t s);
 
+// Chunked tree passes (la_order.cu): a chunk is a run of consecutive forest positions
+// {first position, count, first sink, sink count} run by one warp — whole nets with at most
+// CHUNK_NODES nodes and CHUNK_SINKS sinks together (lane = node), or one bigger net alone.
+constexpr int CHUNK_NODES = 32;
+constexpr int CHUNK_SINKS = 64;
+// Pre-assignment pi-model parasitics per direction (0 = H, 1 = V): unit R (kOhm), unit C (fF).
+struct PreRC { double rd[2], cd[2]; };
+// Cd / Dg: per-node scratch [n_nodes] for nets beyond a chunk.
+cudaError_t launch_pre_timing(const DevForest &F, const int4 *chunks, int64_t n_chunks, const PreRC &P, double *Cd,
+                              double *Dg, double *sink_delay, double *net_cap, cudaStream_t s);
+// Alg. 1 lines 3-10 (la_order.cu): device inputs; batch_of [n_nets] device output.
+struct OrderIn {
+    int64_t n_nets;
+    const int64_t *pin_ptr, *seg_ptr;
+    const double *pin_slack;
+    const int32_t *seg_xy, *crit;
+    double wns, alpha;
+    int32_t th;
+    int64_t max_batch;
+};
+cudaError_t gpu_paper_batches(const OrderIn &in, int32_t *batch_of, int32_t *n_batches, cudaStream_t s,
+                              int64_t *launches);
+
 // Evaluator (la_kernels.cu): histogram of (layer, c == 0, clamp(d - c)) over one packed
 // plane with `slots` layers per element group (slot -> layer via layer_of), exact
 // legacy sum of max(0, d - c) per layer, and the out-of-domain count.

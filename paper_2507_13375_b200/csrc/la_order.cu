@@ -1,0 +1,345 @@
+// The step before the hot path, on the GPU:
+//
+//   k_pre_timing      pre-assignment timing on the 2D LA trees with the pi model and the
+//                     per-direction average unit R / C (PAPER §III-B l.283-286; Alg. 1 inputs
+//                     r_avg, c_avg l.240-241; reading R44): sink wire delays and net load caps,
+//                     the parasitics the STA of Alg. 1 line 1 consumes (the STA itself is out of
+//                     scope).
+//   k_order_keys ..   Alg. 1 lines 3-10 (PAPER §III-A l.213-262; readings R31, R33, R42, R43):
+//   k_batch_ids       Divide, PartitionAndSort(N_c), PartitionAndSort(N_s), Sort(N_n),
+//                     GetBatches, Concat; two stable CUB radix passes (a library sort
+//                     primitive) order the nets, hand-written kernels form the keys and batches.
+//
+// Compiled with --fmad=false: every fp64 expression is evaluated as written (the band bounds
+// C / 2^k and (1 - 0.01 k k) WNS must be the oracle's doubles bit for bit).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include "la_device.cuh"
+#include "la_internal.h"
+
+namespace gapla {
+namespace {
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ pre-timing ----
+// A warp per CHUNK of consecutive forest positions (DESIGN §5 "Chunked tree passes"): either
+// several whole nets with at most 32 nodes and 64 sinks together — lane = node, every node and
+// sink field loaded once with coalesced loads, the recursion run in height steps out of shared
+// memory — or one bigger net, walked in windows of 32 nodes with its per-node values in global
+// scratch (bottom-up forward, top-down backward).
+constexpr int PT_WARPS = 8;
+
+__device__ __forceinline__ int dtype_of(int edir) { return edir <= 1 ? 0 : 1; }   // E / W = H
+
+__device__ void pre_small(const DevForest &F, const PreRC &P, int64_t pb, int np, int64_t n0, int nn, int64_t q0,
+                          int nq, double *sCd, double *sD, double *sR, double *sC, double *sQ, double *sink_delay,
+                          double *net_cap) {
+    const int lane = threadIdx.x & 31;
+    const bool act = lane < nn;
+    int4 kid = make_int4(-1, -1, -1, -1);
+    int nk = 0, h = 0, s0 = 0, ns = 0;
+    double R = 0.0, C = 0.0;
+    int e = 0;
+    int64_t nid = 0;
+    if (lane < np) {
+        e = (int)(F.net_node0[pb + lane + 1] - n0) - 1;   // local id of net lane's root (last node)
+        nid = F.net_id[pb + lane];
+    }
+    for (int k = lane; k < nq; k += 32) sQ[k] = F.p_cap[q0 + k];
+    const unsigned roots = __reduce_or_sync(FULL_MASK, lane < np ? 1u << e : 0u);
+    const bool root = (roots >> lane) & 1u;
+    if (act) {
+        const int64_t n = n0 + lane;
+        kid = reinterpret_cast<const int4 *>(F.kid)[n];
+        nk = F.nkid[n];
+        h = F.height[n];
+        s0 = (int)(F.sink0[n] - q0);
+        ns = F.nsink[n];
+        if (!root) {
+            const int t = dtype_of(F.edir[n]);
+            const double len = (double)F.len[n];
+            R = P.rd[t] * len;
+            C = P.cd[t] * len;
+        }
+    }
+    sR[lane] = R;
+    sC[lane] = C;
+    const int hmax = __reduce_max_sync(FULL_MASK, act ? h : 0);
+    const int kl[4] = {kid.x - (int)n0, kid.y - (int)n0, kid.z - (int)n0, kid.w - (int)n0};
+    __syncwarp();
+    // bottom-up: Cdn(n) = sum of its sink caps + sum over sons s of (C_s + Cdn(s))
+    for (int hh = 0; hh <= hmax; ++hh) {
+        if (act && h == hh) {
+            double c0 = 0.0;
+            for (int k = 0; k < ns; ++k) c0 = c0 + sQ[s0 + k];
+            double K = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < nk) K = K + (sC[kl[i]] + sCd[kl[i]]);
+            sCd[lane] = c0 + K;
+        }
+        __syncwarp();
+    }
+    // top-down: D(s) = D(n) + R_s (C_s / 2 + Cdn(s)); D(root) = 0
+    if (root) sD[lane] = 0.0;
+    __syncwarp();
+    for (int hh = hmax; hh >= 0; --hh) {
+        if (act && h == hh) {
+            const double D = sD[lane];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < nk) sD[kl[i]] = D + sR[kl[i]] * (0.5 * sC[kl[i]] + sCd[kl[i]]);
+            for (int k = 0; k < ns; ++k) sQ[s0 + k] = D;   // the sink caps are no longer needed
+        }
+        __syncwarp();
+    }
+    for (int k = lane; k < nq; k += 32) sink_delay[F.p_orig[q0 + k]] = sQ[k];
+    if (lane < np) net_cap[nid] = sCd[e];
+    __syncwarp();
+}
+
+__device__ void pre_big(const DevForest &F, const PreRC &P, int64_t n0, int nn, int64_t nid, double *Cd,
+                        double *Dg, double *sink_delay, double *net_cap) {
+    const int lane = threadIdx.x & 31;
+    auto RC = [&](int64_t s, double &R, double &C) {
+        const int t = dtype_of(F.edir[s]);
+        const double len = (double)F.len[s];
+        R = P.rd[t] * len;
+        C = P.cd[t] * len;
+    };
+    for (int wb = 0; wb < nn; wb += 32) {   // bottom-up, windows forward (children before parents)
+        const bool act = wb + lane < nn;
+        const int64_t n = n0 + wb + lane;
+        const int h = act ? F.height[n] : 0;
+        const int hlo = __reduce_min_sync(FULL_MASK, act ? h : 0x7fffffff);
+        const int hhi = __reduce_max_sync(FULL_MASK, act ? h : 0);
+        for (int hh = hlo; hh <= hhi; ++hh) {
+            if (act && h == hh) {
+                double c0 = 0.0;
+                const int64_t q = F.sink0[n];
+                for (int k = 0; k < F.nsink[n]; ++k) c0 = c0 + F.p_cap[q + k];
+                double K = 0.0;
+                for (int i = 0; i < F.nkid[n]; ++i) {
+                    const int64_t s = F.kid[n * 4 + i];
+                    double R, C;
+                    RC(s, R, C);
+                    K = K + (C + Cd[s]);
+                }
+                Cd[n] = c0 + K;
+            }
+            __syncwarp();
+        }
+    }
+    const int64_t rt = n0 + nn - 1;
+    if (lane == 0) {
+        Dg[rt] = 0.0;
+        net_cap[nid] = Cd[rt];
+    }
+    __syncwarp();
+    for (int wb = ((nn - 1) / 32) * 32; wb >= 0; wb -= 32) {   // top-down, windows backward
+        const bool act = wb + lane < nn;
+        const int64_t n = n0 + wb + lane;
+        const int h = act ? F.height[n] : 0;
+        const int hlo = __reduce_min_sync(FULL_MASK, act ? h : 0x7fffffff);
+        const int hhi = __reduce_max_sync(FULL_MASK, act ? h : 0);
+        for (int hh = hhi; hh >= hlo; --hh) {
+            if (act && h == hh) {
+                const double D = Dg[n];
+                for (int i = 0; i < F.nkid[n]; ++i) {
+                    const int64_t s = F.kid[n * 4 + i];
+                    double R, C;
+                    RC(s, R, C);
+                    Dg[s] = D + R * (0.5 * C + Cd[s]);
+                }
+                const int64_t q = F.sink0[n];
+                for (int k = 0; k < F.nsink[n]; ++k) sink_delay[F.p_orig[q + k]] = D;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(PT_WARPS * 32) k_pre_timing(DevForest F, const int4 *__restrict__ chunks,
+                                                             int64_t n_chunks, PreRC P, double *Cd, double *Dg,
+                                                             double *sink_delay, double *net_cap) {
+    __shared__ double sCd[PT_WARPS][32], sD[PT_WARPS][32], sR[PT_WARPS][32], sC[PT_WARPS][32];
+    __shared__ double sQ[PT_WARPS][CHUNK_SINKS];
+    const int w = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * PT_WARPS;
+    for (int64_t ci = (int64_t)blockIdx.x * PT_WARPS + w; ci < n_chunks; ci += nw) {
+        const int4 ch = chunks[ci];
+        const int64_t pb = ch.x, q0 = ch.z;
+        const int np = ch.y, nq = ch.w;
+        const int64_t n0 = F.net_node0[pb];
+        const int64_t nn = F.net_node0[pb + np] - n0;
+        if (nn <= CHUNK_NODES && nq <= CHUNK_SINKS)
+            pre_small(F, P, pb, np, n0, (int)nn, q0, nq, sCd[w], sD[w], sR[w], sC[w], sQ[w], sink_delay, net_cap);
+        else
+            pre_big(F, P, n0, (int)nn, F.net_id[pb], Cd, Dg, sink_delay, net_cap);
+    }
+}
+
+// ---------------------------------------------------------- Alg. 1 l.3-10 --
+// Per net: net slack (minimum over its sinks, l.217), 2D wirelength (sum of its segments'
+// lengths), the class (Divide, l.3: 0 = N_c, 1 = N_s, 2 = N_n), the band and the two sort keys:
+//   key1: N_c / N_s: net slack as an order-preserving 64-bit integer; N_n: wirelength;
+//   key2: class << 48 | band << 32 | (N_c: INT32_MAX - criticality, so criticality descends).
+// Two stable radix passes (key1, then key2) over the identity permutation order the nets by
+// (class, band, -criticality, slack or wirelength, index) — the oracle's sort keys.
+__device__ __forceinline__ uint64_t ordered_bits(double v) {
+    if (v == 0.0) v = 0.0;                 // -0 and +0 compare equal: one key
+    const uint64_t b = (uint64_t)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void k_crit_max(const int32_t *__restrict__ crit, int64_t n, int32_t th, int32_t *__restrict__ cmax) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int32_t c = (j < n && crit[j] > th) ? crit[j] : 0;
+    c = __reduce_max_sync(FULL_MASK, c);
+    if ((threadIdx.x & 31) == 0 && c > 0) atomicMax(cmax, c);
+}
+
+__global__ void k_order_keys(OrderIn in, const int32_t *__restrict__ cmax, uint64_t *__restrict__ key1,
+                             uint64_t *__restrict__ key2, int32_t *__restrict__ idx) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= in.n_nets) return;
+    double m = dinf();
+    for (int64_t p = in.pin_ptr[j] + 1; p < in.pin_ptr[j + 1]; ++p) {   // sinks: pin 0 is the driver
+        const double s = in.pin_slack[p];
+        m = (s < m) ? s : m;
+    }
+    const int32_t c = in.crit[j];
+    uint64_t k1, k2;
+    if (c > in.th) {                                   // N_c: [C, C], [C/2, C), [C/4, C/2), ...
+        const int32_t C = *cmax;
+        uint64_t b = 0;
+        if (c < C) {   // th >= 0 (la_paper_batches), so c >= 1 and b <= 31: C / 2^b is exact
+            b = 1;
+            while ((double)c < (double)C / (double)(1ull << b)) ++b;
+        }
+        k1 = ordered_bits(m);
+        k2 = (0ull << 48) | (b << 32) | (uint64_t)(uint32_t)(0x7fffffff - c);
+    } else if (in.wns < 0.0 && m < in.alpha * in.wns) {   // N_s: slack == WNS, (f_{k-1} WNS, f_k WNS]
+        uint64_t b = 0;
+        if (!(m <= in.wns)) {
+            b = 1;
+            while (b < 10 && !(m <= (1.0 - 0.01 * (double)b * (double)b) * in.wns)) ++b;
+        }
+        k1 = ordered_bits(m);
+        k2 = (1ull << 48) | (b << 32);
+    } else {                                           // N_n: congestion-driven, 2D wirelength (R43)
+        int64_t wl = 0;
+        for (int64_t s = in.seg_ptr[j]; s < in.seg_ptr[j + 1]; ++s) {
+            const int4 q = reinterpret_cast<const int4 *>(in.seg_xy)[s];
+            wl += abs(q.z - q.x) + abs(q.w - q.y);
+        }
+        k1 = (uint64_t)wl;
+        k2 = 2ull << 48;
+    }
+    key1[j] = k1;
+    key2[j] = k2;
+    idx[j] = (int32_t)j;
+}
+
+__global__ void k_gather_key(const uint64_t *__restrict__ key, const int32_t *__restrict__ idx, int64_t n,
+                             uint64_t *__restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = key[idx[i]];
+}
+
+// GetBatches + Concat: a subset starts where (class, band) changes; a batch starts at a subset
+// start and every max_batch nets after it.  subset_start = running max of the subsets' starts.
+__global__ void k_subset_heads(const uint64_t *__restrict__ k2s, int64_t n, int64_t *__restrict__ head_at) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    head_at[i] = (i == 0 || (k2s[i] >> 32) != (k2s[i - 1] >> 32)) ? i : 0;
+}
+
+__global__ void k_batch_flags(const int64_t *__restrict__ sub0, int64_t n, int64_t max_batch,
+                              int32_t *__restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = ((i - sub0[i]) % max_batch) == 0 ? 1 : 0;
+}
+
+__global__ void k_batch_scatter(const int32_t *__restrict__ incl, const int32_t *__restrict__ idx, int64_t n,
+                                int32_t *__restrict__ batch_of) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) batch_of[idx[i]] = incl[i] - 1;
+}
+
+struct MaxI64 {
+    __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
+
+#define OCK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
+
+}  // namespace
+
+cudaError_t launch_pre_timing(const DevForest &F, const int4 *chunks, int64_t n_chunks, const PreRC &P, double *Cd,
+                              double *Dg, double *sink_delay, double *net_cap, cudaStream_t s) {
+    if (n_chunks == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    OCK(cudaGetDevice(&dev));
+    OCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int per_sm = 1;
+    OCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pre_timing, PT_WARPS * 32, 0));
+    const int64_t want = (n_chunks + PT_WARPS - 1) / PT_WARPS;
+    const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
+    k_pre_timing<<<grid, PT_WARPS * 32, 0, s>>>(F, chunks, n_chunks, P, Cd, Dg, sink_delay, net_cap);
+    return cudaGetLastError();
+}
+
+cudaError_t gpu_paper_batches(const OrderIn &in, int32_t *batch_of, int32_t *n_batches, cudaStream_t s,
+                              int64_t *launches) {
+    const int64_t n = in.n_nets;
+    *n_batches = 0;
+    if (n == 0) return cudaSuccess;
+    char *buf = nullptr;
+    // key1 | key2 | key_a | key_b (4 x 8n) | idx_a | idx_b | flags | incl (4 x 4n) | sub0 heads (2 x 8n) | cmax
+    const size_t b8 = 8 * (size_t)n, b4 = 4 * (size_t)n;
+    size_t tmp_sort = 0, tmp_max = 0, tmp_sum = 0;
+    OCK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                        (int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, 64, s));
+    OCK(cub::DeviceScan::InclusiveScan(nullptr, tmp_max, (int64_t *)nullptr, (int64_t *)nullptr, MaxI64(), (int)n,
+                                       s));
+    OCK(cub::DeviceScan::InclusiveSum(nullptr, tmp_sum, (int32_t *)nullptr, (int32_t *)nullptr, (int)n, s));
+    const size_t tmp = std::max(tmp_sort, std::max(tmp_max, tmp_sum));
+    const size_t total = 6 * b8 + 4 * b4 + 256 + tmp;
+    OCK(dmalloc(&buf, total));
+    uint64_t *key1 = (uint64_t *)buf, *key2 = key1 + n, *ka = key2 + n, *kb = ka + n;
+    int64_t *heads = (int64_t *)(kb + n), *sub0 = heads + n;
+    int32_t *idx_a = (int32_t *)(sub0 + n), *idx_b = idx_a + n, *flag = idx_b + n, *incl = flag + n;
+    int32_t *cmax = (int32_t *)(incl + n);
+    void *tmpp = (char *)cmax + 256;
+    cudaError_t e = cudaSuccess;
+    do {
+        const int T = 256;
+        if ((e = cudaMemsetAsync(cmax, 0, 4, s))) break;
+        k_crit_max<<<nblk(n, T), T, 0, s>>>(in.crit, n, in.th, cmax);
+        k_order_keys<<<nblk(n, T), T, 0, s>>>(in, cmax, key1, key2, idx_a);
+        size_t tb = tmp;
+        // pass 1: key1 (stable over the identity order = ties by net index)
+        if ((e = cub::DeviceRadixSort::SortPairs(tmpp, tb, key1, ka, idx_a, idx_b, (int)n, 0, 64, s))) break;
+        k_gather_key<<<nblk(n, T), T, 0, s>>>(key2, idx_b, n, key1);
+        // pass 2: key2 (class, band, criticality descending), stable over pass 1's order
+        tb = tmp;
+        if ((e = cub::DeviceRadixSort::SortPairs(tmpp, tb, key1, kb, idx_b, idx_a, (int)n, 0, 50, s))) break;
+        k_subset_heads<<<nblk(n, T), T, 0, s>>>(kb, n, heads);
+        tb = tmp;
+        if ((e = cub::DeviceScan::InclusiveScan(tmpp, tb, heads, sub0, MaxI64(), (int)n, s))) break;
+        k_batch_flags<<<nblk(n, T), T, 0, s>>>(sub0, n, in.max_batch, flag);
+        tb = tmp;
+        if ((e = cub::DeviceScan::InclusiveSum(tmpp, tb, flag, incl, (int)n, s))) break;
+        k_batch_scatter<<<nblk(n, T), T, 0, s>>>(incl, idx_a, n, batch_of);
+        if ((e = cudaGetLastError())) break;
+        if ((e = cudaMemcpyAsync(n_batches, incl + n - 1, 4, cudaMemcpyDeviceToHost, s))) break;
+        e = cudaStreamSynchronize(s);
+        if (launches) *launches += 11;
+    } while (0);
+    dfree(buf);
+    return e;
+}
+
+}  // namespace gapla

@@ -73,7 +73,9 @@ class la_stats(ctypes.Structure):
 class la_profile(ctypes.Structure):
     _fields_ = [("assign_launches", c_i64), ("commit_launches", c_i64), ("elmore_launches", c_i64),
                 ("reconcile_calls", c_i64), ("assign_ms", c_f64), ("commit_ms", c_f64), ("elmore_ms", c_f64),
-                ("reconcile_ms", c_f64), ("eval_launches", c_i64), ("eval_ms", c_f64)]
+                ("reconcile_ms", c_f64), ("eval_launches", c_i64), ("eval_ms", c_f64),
+                ("pretime_launches", c_i64), ("order_calls", c_i64), ("pretime_ms", c_f64), ("order_ms", c_f64),
+                ("order_kernel_ms", c_f64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -97,7 +99,8 @@ def _load():
         "la_batch_extent": ([c_void_p, c_i32, P(c_i64), P(c_i64)], c_i32),
         "la_get_decisions": ([c_void_p, c_i32, P(ctypes.c_uint32), P(c_f64)], c_i32),
         "la_put_decisions": ([c_void_p, c_i32, P(ctypes.c_uint32), P(c_f64)], c_i32),
-        "la_paper_batches": ([P(la_net_desc), P(c_i32), c_f64, c_i32, c_i64, P(c_i32), P(c_i32)], c_i32),
+        "la_paper_batches": ([c_void_p, P(la_net_desc), P(c_i32), c_f64, c_i32, c_i64, P(c_i32), P(c_i32)], c_i32),
+        "la_pre_timing": ([c_void_p, c_f64, c_f64, c_f64, c_f64, P(c_f64), P(c_f64)], c_i32),
         "la_get_trace": ([c_void_p, P(c_i64)], c_i32),
         "la_eval_timing": ([c_void_p, P(c_f64), P(c_f64), P(c_f64)], c_i32),
         "la_get_solution": ([c_void_p, P(c_i64), P(c_i64), P(c_i64), P(c_i32), P(c_i64), P(c_i32), P(c_f64)], c_i32),
@@ -126,7 +129,8 @@ EXPORTS = ("la_init_grid", "la_load_nets", "la_assign_batch", "la_commit_demand"
            "la_get_solution", "la_get_demand", "la_get_batches", "la_reset", "la_get_stats", "la_sync", "la_destroy",
            "la_last_error", "la_shard_range", "la_set_profiling", "la_get_profile", "la_nccl_unique_id",
            "la_set_schedule", "la_set_tracing", "la_get_trace", "la_eval_overflow", "la_set_snapshot_batches",
-           "la_paper_batches", "la_batch_extent", "la_get_decisions", "la_put_decisions", "la_fp64_peak")
+           "la_paper_batches", "la_batch_extent", "la_get_decisions", "la_put_decisions", "la_fp64_peak",
+           "la_pre_timing")
 
 
 def _check(st):
@@ -230,16 +234,25 @@ def net_desc_of(d, keep) -> la_net_desc:
     return n
 
 
-def la_paper_batches(d, criticality, alpha: float = 0.7, th: int = 3, max_batch: int = 1 << 20):
-    """Alg. 1 lines 3-10 (include/la.h): batch id per net (input order) and the batch count."""
+def la_paper_batches(ctx, d, criticality, alpha: float = 0.7, th: int = 3, max_batch: int = 1 << 20):
+    """Alg. 1 lines 3-10 on the GPU (include/la.h): batch id per net (input order) and the batch count."""
     keep = []
     desc = net_desc_of(d, keep)
     crit = np.ascontiguousarray(criticality, np.int32)
     out = np.zeros(d.n_nets, np.int32)
     nb = c_i32(0)
-    _check(_lib.la_paper_batches(ctypes.byref(desc), crit.ctypes.data_as(P(c_i32)), float(alpha), int(th),
+    _check(_lib.la_paper_batches(ctx, ctypes.byref(desc), crit.ctypes.data_as(P(c_i32)), float(alpha), int(th),
                                  int(max_batch), out.ctypes.data_as(P(c_i32)), ctypes.byref(nb)))
     return out, int(nb.value)
+
+
+def la_pre_timing(ctx, n_pins: int, n_nets: int, r_h=float("nan"), r_v=float("nan"), c_h=float("nan"),
+                  c_v=float("nan")):
+    """Pre-assignment pi-model timing on the loaded 2D trees (include/la.h): (sink_delay, net_cap)."""
+    delay = np.zeros(n_pins, np.float64)
+    cap = np.zeros(n_nets, np.float64)
+    _check(_lib.la_pre_timing(ctx, float(r_h), float(r_v), float(c_h), float(c_v), _p(delay, c_f64), _p(cap, c_f64)))
+    return delay, cap
 
 
 def la_get_decisions(ctx, batch: int):

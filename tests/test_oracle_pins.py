@@ -416,17 +416,6 @@ def test_paper_batches_by_hand():
     assert nb2 == 5 and list(b2) == [0, 0, 1, 1, 2, 3, 4, 4]
 
 
-def test_paper_batches_library_equals_oracle():
-    """The library's host Alg. 1 (la_paper_batches, no GPU needed) == the plain oracle."""
-    from paper_2507_13375_b200 import la
-    d = synth.make_config(1)
-    for seed, mb in ((1, 50), (2, 1000)):
-        crit = synth.criticality(d, seed)
-        got, nb = la.la_paper_batches(d, crit, 0.7, 3, mb)
-        ref, nbr = oracle.paper_batches(d.pin_ptr, d.pin_slack, d.seg_ptr, d.seg_xy, d.wns, crit, 0.7, 3, mb)
-        assert nb == nbr and np.array_equal(got, ref)
-
-
 # ------------------------------------------------------------------ O3 look-ahead (PAPER l.442-453)
 def _tree_ids(d, net=0):
     """(x, y) -> oracle node id."""

@@ -37,10 +37,6 @@ def test_pre_timing_hand_fixtures(name):
     assert cap[0] == pytest.approx(fx["net_cap"], rel=1e-15)
 
 
-def _dir_rc(d, r_h, r_v, c_h, c_v):
-    return (r_h, r_v), (c_h, c_v)
-
-
 def unit_graph_elmore(d, net, rd, cd):
     """Elmore on the route's unit-edge graph: each unit edge (a, b) of direction t is a pi
     section r_t, c_t (c_t / 2 at each end); cell cap = its sinks' caps + the halves of its
@@ -119,3 +115,134 @@ def test_pre_timing_net_cap_closed_form_and_default_rc():
         assert math.isclose(cap[net], sinks + ch * wh + cv * wv, rel_tol=1e-12), net
     drv = d.pin_ptr[:-1]
     assert np.all(delay[drv] == 0.0) and np.all(delay >= 0.0)
+
+
+# ------------------------------------------------------------------ GPU parity (la_pre_timing)
+@pytest.fixture(scope="module")
+def la():
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2507_13375_b200 import la as mod
+    return mod
+
+
+def _gpu_pre(la, d, *rc_vals):
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    out = la.la_pre_timing(A.ctx, int(d.pin_ptr[-1]), d.n_nets, *rc_vals)
+    A.close()
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["fixtures", "cfg1", "cfg2", "cfg4_sample", "explicit_rc"])
+def test_pre_timing_gpu_parity(la, case):
+    """k_pre_timing == oracle.pre_timing element by element within 1e-9 relative (the north
+    star's fp64 tolerance; the two sum the same terms in different orders).  cfg4_sample holds
+    64-256-pin nets (the windowed big-net path) next to the chunked small nets."""
+    rcv = ()
+    if case == "fixtures":
+        g = golden("pre_timing_fixtures.json")
+        d = synth.empty_design(8, 8, 4)
+        d = synth.with_nets(d, [dict(pins=[tuple(p) for p in g[k]["pins"]], segs=[tuple(s) for s in g[k]["segs"]])
+                                for k in ("L", "T", "driver_cell")])
+        rcv = (g["rc"]["r_h"], g["rc"]["r_v"], g["rc"]["c_h"], g["rc"]["c_v"])
+    elif case == "cfg1":
+        d = synth.make_config(1)
+    elif case == "cfg2":
+        d = synth.make_config(2)
+    elif case == "cfg4_sample":
+        d = synth.generate(n_nets=40_000, X=512, Y=512, L=13, seed=104, hf_frac=0.01, rdrv_mode=1, name="pre_hf")
+    else:
+        d = synth.make_config(2, n_nets=20_000)
+        rcv = (0.0123, 0.0456, 0.31, 0.27)
+    got_d, got_c = _gpu_pre(la, d, *rcv)
+    ref_d, ref_c = oracle.pre_timing(d, *rcv)
+    np.testing.assert_allclose(got_d, ref_d, rtol=1e-9, atol=0.0)
+    np.testing.assert_allclose(got_c, ref_c, rtol=1e-9, atol=0.0)
+    assert np.all(got_d[d.pin_ptr[:-1]] == 0.0)
+    if case == "fixtures":
+        assert got_d.tolist() == pytest.approx(sum((g[k]["delay"] for k in ("L", "T", "driver_cell")), []), rel=1e-15)
+
+
+@pytest.mark.gpu
+def test_pre_timing_gpu_full_cfg3_sampled(la):
+    """Config 3 at full size (1M nets) through the bench's launch: 2,000 nets sampled across
+    the forest compared with the oracle run on exactly those nets."""
+    d = synth.make_config(3)
+    got_d, got_c = _gpu_pre(la, d)
+    rng = np.random.default_rng(3)
+    nets = np.sort(rng.choice(d.n_nets, 2000, replace=False))
+    from helpers import single_net
+    for j in nets:
+        e = single_net(d, int(j))
+        rd, rcap = oracle.pre_timing(e)
+        a, b = int(d.pin_ptr[j]), int(d.pin_ptr[j + 1])
+        np.testing.assert_allclose(got_d[a:b], rd, rtol=1e-9, atol=0.0)
+        assert math.isclose(got_c[j], rcap[0], rel_tol=1e-9)
+
+
+# ------------------------------------------------------------------ GPU Alg. 1 (la_paper_batches)
+def _gpu_batches(la, d, crit, alpha=0.7, th=3, mb=1 << 20):
+    A = la.LayerAssigner(d, device=0)
+    try:
+        return la.la_paper_batches(A.ctx, d, crit, alpha, th, mb)
+    finally:
+        A.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["cfg1_50", "cfg2_1000", "cfg2_ties", "wns_pos", "all_critical", "th0_cap1"])
+def test_paper_batches_gpu_equals_oracle(la, case):
+    """Alg. 1 lines 3-10 on the GPU == oracle.paper_batches, batch ids bit-exact (integer work),
+    including ties of slack / criticality / wirelength (index order decides), WNS >= 0 (no
+    semi-critical class), every net critical, and a size cap of one net per batch."""
+    d = synth.make_config(2 if "cfg2" in case or case in ("wns_pos", "all_critical", "th0_cap1") else 1)
+    crit = synth.criticality(d, 1)
+    alpha, th, mb = 0.7, 3, 50
+    if case == "cfg2_1000":
+        mb = 1000
+    elif case == "cfg2_ties":
+        d.pin_slack = np.round(d.pin_slack / 50.0) * 50.0       # many equal net slacks
+        crit = (crit // 2) * 2
+        mb = 333
+    elif case == "wns_pos":
+        d.wns = 10.0
+        mb = 777
+    elif case == "all_critical":
+        crit = crit + 4
+        mb = 5000
+    elif case == "th0_cap1":
+        d = synth.make_config(1)
+        crit = synth.criticality(d, 2)
+        th, mb = 0, 1
+    got, nb = _gpu_batches(la, d, crit, alpha, th, mb)
+    ref, nbr = oracle.paper_batches(d.pin_ptr, d.pin_slack, d.seg_ptr, d.seg_xy, d.wns, crit, alpha, th, mb)
+    assert nb == nbr
+    if not np.array_equal(got, ref):
+        bad = np.flatnonzero(got != ref)
+        raise AssertionError(f"{bad.size} nets differ, first {bad[:5].tolist()}: {got[bad[:5]]} vs {ref[bad[:5]]}")
+
+
+@pytest.mark.gpu
+def test_paper_batches_gpu_argument_errors(la):
+    """la_paper_batches validates its arguments (include/la.h): alpha > 0, th >= 0,
+    max_batch >= 1, non-negative criticality."""
+    d = synth.make_config(1)
+    crit = np.zeros(d.n_nets, np.int32)
+    A = la.LayerAssigner(d, device=0)
+    try:
+        for kw in (dict(alpha=0.0), dict(mb=0), dict(th=-1)):
+            args = dict(alpha=0.7, th=3, mb=100)
+            args.update(kw)
+            with pytest.raises(la.LaError) as ei:
+                la.la_paper_batches(A.ctx, d, crit, args["alpha"], args["th"], args["mb"])
+            assert ei.value.status == la.LA_EINVAL
+        bad = crit.copy()
+        bad[3] = -1
+        with pytest.raises(la.LaError, match="criticality"):
+            la.la_paper_batches(A.ctx, d, bad)
+        b, nb = la.la_paper_batches(A.ctx, d, crit, max_batch=10**9)
+        assert nb >= 1 and b.min() == 0 and b.max() == nb - 1
+    finally:
+        A.close()
