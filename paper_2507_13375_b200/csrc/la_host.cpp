@@ -1900,34 +1900,39 @@ la_status la_paper_batches(la_ctx *ctx, const la_net_desc *n, const int32_t *cri
     return LA_OK;
 }
 
-// Chunks of the tree passes (la_order.cu): consecutive forest positions packed into runs of at
+// Chunks of the tree passes (la_tree.cu): consecutive forest positions packed into runs of at
 // most CHUNK_NODES nodes / CHUNK_SINKS sinks / 32 nets; a net beyond that is a chunk of its own.
-static la_status build_chunks(la_ctx *ctx) {
-    if (ctx->d_chunks) return LA_OK;
-    const int64_t N = ctx->n_nets;
+// pos: the positions to cover, ascending (nullptr: all); a chunk never spans a gap.
+static la_status build_chunks(la_ctx *ctx, const std::vector<int32_t> *pos, int4 **d_out, int64_t *n_out) {
+    if (*d_out) return LA_OK;
+    const int64_t M = pos ? (int64_t)pos->size() : ctx->n_nets;
+    auto P = [&](int64_t i) -> int64_t { return pos ? (int64_t)(*pos)[i] : i; };
     std::vector<int4> ch;
-    ch.reserve((size_t)(N / 6 + 16));
-    int64_t p = 0;
-    while (p < N) {
-        const int64_t q0 = ctx->h_net_sink0[p];
+    ch.reserve((size_t)(M / 6 + 16));
+    int64_t i = 0;
+    while (i < M) {
+        const int64_t p0 = P(i);
+        const int64_t n0 = ctx->h_net_node0[p0], q0 = ctx->h_net_sink0[p0];
         int64_t nodes = 0, sinks = 0, k = 0;
-        while (p + k < N && k < 32) {
-            const int64_t a = ctx->h_net_node0[p + k + 1] - ctx->h_net_node0[p + k];
-            const int64_t b = ctx->h_net_sink0[p + k + 1] - ctx->h_net_sink0[p + k];
+        while (i + k < M && k < 32 && P(i + k) == p0 + k) {
+            const int64_t p = p0 + k;
+            const int64_t a = ctx->h_net_node0[p + 1] - ctx->h_net_node0[p];
+            const int64_t b = ctx->h_net_sink0[p + 1] - ctx->h_net_sink0[p];
             if (nodes + a > CHUNK_NODES || sinks + b > CHUNK_SINKS) break;
             nodes += a;
             sinks += b;
             k++;
         }
-        if (k == 0) {   // one net beyond a chunk
+        if (k == 0) {   // one bigger net
             k = 1;
-            sinks = ctx->h_net_sink0[p + 1] - q0;
+            ch.push_back(make_int4((int)p0, (int)n0, (int)q0, (int)(1u << 31)));
+        } else {
+            ch.push_back(make_int4((int)p0, (int)n0, (int)q0, (int)(k | (sinks << 6) | (nodes << 13))));
         }
-        ch.push_back(make_int4((int)p, (int)k, (int)q0, (int)std::min<int64_t>(sinks, INT32_MAX)));
-        p += k;
+        i += k;
     }
-    ctx->n_chunks = (int64_t)ch.size();
-    TRY(dev_upload(ctx, &ctx->d_chunks, ch.data(), ch.size()));
+    *n_out = (int64_t)ch.size();
+    TRY(dev_upload(ctx, d_out, ch.data(), std::max<size_t>(ch.size(), 1)));
     return LA_OK;
 }
 
@@ -1938,7 +1943,7 @@ la_status la_pre_timing(la_ctx *ctx, double r_h, double r_v, double c_h, double 
         !(std::isnan(c_v) || c_v >= 0))
         return set_err(LA_EINVAL, "negative unit R / C");
     CK(cudaSetDevice(ctx->device));
-    TRY(build_chunks(ctx));
+    TRY(build_chunks(ctx, nullptr, &ctx->d_chunks, &ctx->n_chunks));
     // per-direction averages over the routable layers (R44): plain mean, ascending l
     PreRC P{};
     const double give_r[2] = {r_h, r_v}, give_c[2] = {c_h, c_v};
@@ -2001,9 +2006,12 @@ la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, doubl
         CK(cudaMemsetAsync(ctx->S.net_cap, 0, sizeof(double) * ctx->n_nets, ctx->stream));
         CK(cudaMemsetAsync(ctx->S.net_rc, 0, sizeof(double) * ctx->n_nets, ctx->stream));
     }
+    static const bool v1 = getenv("GAPLA_ELMORE_V1") && atoi(getenv("GAPLA_ELMORE_V1")) != 0;   // A/B: round-1 kernel
     int pe = prof_begin(ctx, K_ELMORE);
-    if (shard) CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_own, ctx->d_own_pos, ctx->stream));
-    else CK(launch_elmore(ctx->G, ctx->F, ctx->S, 0, ctx->n_nets, nullptr, ctx->stream));
+    const int64_t ne = shard ? ctx->n_own : ctx->n_nets;
+    const int32_t *lst = shard ? ctx->d_own_pos : nullptr;
+    if (v1) CK(launch_elmore_v1(ctx->G, ctx->F, ctx->S, 0, ne, lst, ctx->stream));
+    else CK(launch_elmore(ctx->F, ctx->S, ctx->d_tab, 0, ne, lst, ctx->stream));
     prof_end(ctx, pe);
     ctx->stats.launches += 1;
     if (ctx->nccl) {

@@ -171,13 +171,17 @@ cudaError_t launch_commit(const DevGrid &G, const DevForest &F, const DevScratch
 cudaError_t launch_pack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);
 cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64_t node_end, cudaStream_t s);
 // k_elmore over the nets [net_beg, net_end) of `list` (forest positions), or over the positions
-// [net_beg, net_end) themselves when list is null.
-cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
-                          int64_t net_end, const int32_t *list, cudaStream_t s);
+// [net_beg, net_end) themselves when list is null: la_tree.cu (launch_elmore), the round-1 kernel
+// in la_kernels.cu (launch_elmore_v1, A/B only).
+cudaError_t launch_elmore(const DevForest &F, const DevScratch &S, const TechTab *tab, int64_t net_beg, int64_t net_end,
+                          const int32_t *list, cudaStream_t s);
+cudaError_t launch_elmore_v1(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
+                             int64_t net_end, const int32_t *list, cudaStream_t s);
 
-// Chunked tree passes (la_order.cu): a chunk is a run of consecutive forest positions
-// {first position, count, first sink, sink count} run by one warp — whole nets with at most
-// CHUNK_NODES nodes and CHUNK_SINKS sinks together (lane = node), or one bigger net alone.
+// Chunked tree passes (la_tree.cu): a chunk is a run of consecutive forest positions
+// run by one warp — whole nets with at most CHUNK_NODES nodes and CHUNK_SINKS sinks together
+// (lane = node), or one bigger net.  Record {first position, first node, first sink,
+// nets | sinks << 6 | nodes << 13}, or {position, first node, first sink, 1 << 31} for a bigger net.
 constexpr int CHUNK_NODES = 32;
 constexpr int CHUNK_SINKS = 64;
 // Pre-assignment pi-model parasitics per direction (0 = H, 1 = V): unit R (kOhm), unit C (fF).

@@ -113,10 +113,11 @@ __global__ void k_unpack_dec(DevScratch S, int64_t node_beg, int64_t node_end) {
 }
 
 // ------------------------------------------------------------------ K6 + K7 --
-// Canonical fast Elmore form (DESIGN §3 O9), one thread per net.
+// Canonical fast Elmore form (DESIGN §3 O9), one thread per net: the round-1 kernel, kept for
+// A/B runs (GAPLA_ELMORE_V1=1); la_eval_timing runs the chunked k_elmore of la_tree.cu.
 constexpr int ELMORE_THREADS = 128;
 
-__global__ void __launch_bounds__(ELMORE_THREADS) k_elmore(DevGrid G, DevForest F, DevScratch S, int64_t net_beg,
+__global__ void __launch_bounds__(ELMORE_THREADS) k_elmore_v1(DevGrid G, DevForest F, DevScratch S, int64_t net_beg,
                                                           int64_t net_end, const int32_t *list) {
     __shared__ TechTab T;
     __shared__ double Tks[MAXL][ELMORE_THREADS];   // T(n, k) of the current node, one column per thread
@@ -346,11 +347,11 @@ cudaError_t fp64_peak(double *ops_per_s) {
     return e;
 }
 
-cudaError_t launch_elmore(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
-                          int64_t net_end, const int32_t *list, cudaStream_t s) {
+cudaError_t launch_elmore_v1(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
+                             int64_t net_end, const int32_t *list, cudaStream_t s) {
     int64_t n = net_end - net_beg;
     if (n <= 0) return cudaSuccess;
-    k_elmore<<<nblk(n, ELMORE_THREADS), ELMORE_THREADS, 0, s>>>(G, F, S, net_beg, net_end, list);
+    k_elmore_v1<<<nblk(n, ELMORE_THREADS), ELMORE_THREADS, 0, s>>>(G, F, S, net_beg, net_end, list);
     return cudaGetLastError();
 }
 

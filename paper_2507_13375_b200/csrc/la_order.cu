@@ -1,10 +1,6 @@
-// The step before the hot path, on the GPU:
+// The step before the hot path, on the GPU (the pre-assignment pi-model
+// timing that goes with it is k_pre_timing in la_tree.cu):
 //
-//   k_pre_timing      pre-assignment timing on the 2D LA trees with the pi model and the
-//                     per-direction average unit R / C (PAPER §III-B l.283-286; Alg. 1 inputs
-//                     r_avg, c_avg l.240-241; reading R44): sink wire delays and net load caps,
-//                     the parasitics the STA of Alg. 1 line 1 consumes (the STA itself is out of
-//                     scope).
 //   k_order_keys ..   Alg. 1 lines 3-10 (PAPER §III-A l.213-262; readings R31, R33, R42, R43):
 //   k_batch_ids       Divide, PartitionAndSort(N_c), PartitionAndSort(N_s), Sort(N_n),
 //                     GetBatches, Concat; two stable CUB radix passes (a library sort
@@ -22,164 +18,6 @@ namespace gapla {
 namespace {
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
-
-// ------------------------------------------------------------ pre-timing ----
-// A warp per CHUNK of consecutive forest positions (DESIGN §5 "Chunked tree passes"): either
-// several whole nets with at most 32 nodes and 64 sinks together — lane = node, every node and
-// sink field loaded once with coalesced loads, the recursion run in height steps out of shared
-// memory — or one bigger net, walked in windows of 32 nodes with its per-node values in global
-// scratch (bottom-up forward, top-down backward).
-constexpr int PT_WARPS = 8;
-
-__device__ __forceinline__ int dtype_of(int edir) { return edir <= 1 ? 0 : 1; }   // E / W = H
-
-__device__ void pre_small(const DevForest &F, const PreRC &P, int64_t pb, int np, int64_t n0, int nn, int64_t q0,
-                          int nq, double *sCd, double *sD, double *sR, double *sC, double *sQ, double *sink_delay,
-                          double *net_cap) {
-    const int lane = threadIdx.x & 31;
-    const bool act = lane < nn;
-    int4 kid = make_int4(-1, -1, -1, -1);
-    int nk = 0, h = 0, s0 = 0, ns = 0;
-    double R = 0.0, C = 0.0;
-    int e = 0;
-    int64_t nid = 0;
-    if (lane < np) {
-        e = (int)(F.net_node0[pb + lane + 1] - n0) - 1;   // local id of net lane's root (last node)
-        nid = F.net_id[pb + lane];
-    }
-    for (int k = lane; k < nq; k += 32) sQ[k] = F.p_cap[q0 + k];
-    const unsigned roots = __reduce_or_sync(FULL_MASK, lane < np ? 1u << e : 0u);
-    const bool root = (roots >> lane) & 1u;
-    if (act) {
-        const int64_t n = n0 + lane;
-        kid = reinterpret_cast<const int4 *>(F.kid)[n];
-        nk = F.nkid[n];
-        h = F.height[n];
-        s0 = (int)(F.sink0[n] - q0);
-        ns = F.nsink[n];
-        if (!root) {
-            const int t = dtype_of(F.edir[n]);
-            const double len = (double)F.len[n];
-            R = P.rd[t] * len;
-            C = P.cd[t] * len;
-        }
-    }
-    sR[lane] = R;
-    sC[lane] = C;
-    const int hmax = __reduce_max_sync(FULL_MASK, act ? h : 0);
-    const int kl[4] = {kid.x - (int)n0, kid.y - (int)n0, kid.z - (int)n0, kid.w - (int)n0};
-    __syncwarp();
-    // bottom-up: Cdn(n) = sum of its sink caps + sum over sons s of (C_s + Cdn(s))
-    for (int hh = 0; hh <= hmax; ++hh) {
-        if (act && h == hh) {
-            double c0 = 0.0;
-            for (int k = 0; k < ns; ++k) c0 = c0 + sQ[s0 + k];
-            double K = 0.0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i < nk) K = K + (sC[kl[i]] + sCd[kl[i]]);
-            sCd[lane] = c0 + K;
-        }
-        __syncwarp();
-    }
-    // top-down: D(s) = D(n) + R_s (C_s / 2 + Cdn(s)); D(root) = 0
-    if (root) sD[lane] = 0.0;
-    __syncwarp();
-    for (int hh = hmax; hh >= 0; --hh) {
-        if (act && h == hh) {
-            const double D = sD[lane];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i < nk) sD[kl[i]] = D + sR[kl[i]] * (0.5 * sC[kl[i]] + sCd[kl[i]]);
-            for (int k = 0; k < ns; ++k) sQ[s0 + k] = D;   // the sink caps are no longer needed
-        }
-        __syncwarp();
-    }
-    for (int k = lane; k < nq; k += 32) sink_delay[F.p_orig[q0 + k]] = sQ[k];
-    if (lane < np) net_cap[nid] = sCd[e];
-    __syncwarp();
-}
-
-__device__ void pre_big(const DevForest &F, const PreRC &P, int64_t n0, int nn, int64_t nid, double *Cd,
-                        double *Dg, double *sink_delay, double *net_cap) {
-    const int lane = threadIdx.x & 31;
-    auto RC = [&](int64_t s, double &R, double &C) {
-        const int t = dtype_of(F.edir[s]);
-        const double len = (double)F.len[s];
-        R = P.rd[t] * len;
-        C = P.cd[t] * len;
-    };
-    for (int wb = 0; wb < nn; wb += 32) {   // bottom-up, windows forward (children before parents)
-        const bool act = wb + lane < nn;
-        const int64_t n = n0 + wb + lane;
-        const int h = act ? F.height[n] : 0;
-        const int hlo = __reduce_min_sync(FULL_MASK, act ? h : 0x7fffffff);
-        const int hhi = __reduce_max_sync(FULL_MASK, act ? h : 0);
-        for (int hh = hlo; hh <= hhi; ++hh) {
-            if (act && h == hh) {
-                double c0 = 0.0;
-                const int64_t q = F.sink0[n];
-                for (int k = 0; k < F.nsink[n]; ++k) c0 = c0 + F.p_cap[q + k];
-                double K = 0.0;
-                for (int i = 0; i < F.nkid[n]; ++i) {
-                    const int64_t s = F.kid[n * 4 + i];
-                    double R, C;
-                    RC(s, R, C);
-                    K = K + (C + Cd[s]);
-                }
-                Cd[n] = c0 + K;
-            }
-            __syncwarp();
-        }
-    }
-    const int64_t rt = n0 + nn - 1;
-    if (lane == 0) {
-        Dg[rt] = 0.0;
-        net_cap[nid] = Cd[rt];
-    }
-    __syncwarp();
-    for (int wb = ((nn - 1) / 32) * 32; wb >= 0; wb -= 32) {   // top-down, windows backward
-        const bool act = wb + lane < nn;
-        const int64_t n = n0 + wb + lane;
-        const int h = act ? F.height[n] : 0;
-        const int hlo = __reduce_min_sync(FULL_MASK, act ? h : 0x7fffffff);
-        const int hhi = __reduce_max_sync(FULL_MASK, act ? h : 0);
-        for (int hh = hhi; hh >= hlo; --hh) {
-            if (act && h == hh) {
-                const double D = Dg[n];
-                for (int i = 0; i < F.nkid[n]; ++i) {
-                    const int64_t s = F.kid[n * 4 + i];
-                    double R, C;
-                    RC(s, R, C);
-                    Dg[s] = D + R * (0.5 * C + Cd[s]);
-                }
-                const int64_t q = F.sink0[n];
-                for (int k = 0; k < F.nsink[n]; ++k) sink_delay[F.p_orig[q + k]] = D;
-            }
-            __syncwarp();
-        }
-    }
-}
-
-__global__ void __launch_bounds__(PT_WARPS * 32) k_pre_timing(DevForest F, const int4 *__restrict__ chunks,
-                                                             int64_t n_chunks, PreRC P, double *Cd, double *Dg,
-                                                             double *sink_delay, double *net_cap) {
-    __shared__ double sCd[PT_WARPS][32], sD[PT_WARPS][32], sR[PT_WARPS][32], sC[PT_WARPS][32];
-    __shared__ double sQ[PT_WARPS][CHUNK_SINKS];
-    const int w = threadIdx.x >> 5;
-    const int64_t nw = (int64_t)gridDim.x * PT_WARPS;
-    for (int64_t ci = (int64_t)blockIdx.x * PT_WARPS + w; ci < n_chunks; ci += nw) {
-        const int4 ch = chunks[ci];
-        const int64_t pb = ch.x, q0 = ch.z;
-        const int np = ch.y, nq = ch.w;
-        const int64_t n0 = F.net_node0[pb];
-        const int64_t nn = F.net_node0[pb + np] - n0;
-        if (nn <= CHUNK_NODES && nq <= CHUNK_SINKS)
-            pre_small(F, P, pb, np, n0, (int)nn, q0, nq, sCd[w], sD[w], sR[w], sC[w], sQ[w], sink_delay, net_cap);
-        else
-            pre_big(F, P, n0, (int)nn, F.net_id[pb], Cd, Dg, sink_delay, net_cap);
-    }
-}
 
 // ---------------------------------------------------------- Alg. 1 l.3-10 --
 // Per net: net slack (minimum over its sinks, l.217), 2D wirelength (sum of its segments'
@@ -276,20 +114,6 @@ struct MaxI64 {
 #define OCK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
 
 }  // namespace
-
-cudaError_t launch_pre_timing(const DevForest &F, const int4 *chunks, int64_t n_chunks, const PreRC &P, double *Cd,
-                              double *Dg, double *sink_delay, double *net_cap, cudaStream_t s) {
-    if (n_chunks == 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    OCK(cudaGetDevice(&dev));
-    OCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int per_sm = 1;
-    OCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pre_timing, PT_WARPS * 32, 0));
-    const int64_t want = (n_chunks + PT_WARPS - 1) / PT_WARPS;
-    const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1));
-    k_pre_timing<<<grid, PT_WARPS * 32, 0, s>>>(F, chunks, n_chunks, P, Cd, Dg, sink_delay, net_cap);
-    return cudaGetLastError();
-}
 
 cudaError_t gpu_paper_batches(const OrderIn &in, int32_t *batch_of, int32_t *n_batches, cudaStream_t s,
                               int64_t *launches) {
