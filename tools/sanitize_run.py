@@ -118,6 +118,25 @@ def sc_group_paths():
             del os.environ[k]
 
 
+def sc_next2():
+    """NEXT #2 on the GPU: k_pre_timing (chunks of small nets and a windowed bigger net) and the
+    Alg. 1 kernels, against the oracle; plus k_elmore's local / global node-value paths (bignets)."""
+    d = synth.generate(n_nets=3000, X=96, Y=96, L=10, seed=9, hf_frac=0.01, rdrv_mode=1, name="san_next2")
+    A = la.LayerAssigner(d, device=0)
+    A.load()
+    got_d, got_c = la.la_pre_timing(A.ctx, int(d.pin_ptr[-1]), d.n_nets)
+    crit = synth.criticality(d, 1)
+    b, nb = la.la_paper_batches(A.ctx, d, crit, 0.7, 3, 97)
+    A.close()
+    ref_d, ref_c = oracle.pre_timing(d)
+    if not (np.allclose(got_d, ref_d, rtol=1e-9, atol=0) and np.allclose(got_c, ref_c, rtol=1e-9, atol=0)):
+        raise SystemExit("pre_timing differs from the oracle")
+    rb, rnb = oracle.paper_batches(d.pin_ptr, d.pin_slack, d.seg_ptr, d.seg_xy, d.wns, crit, 0.7, 3, 97)
+    if nb != rnb or not np.array_equal(b, rb):
+        raise SystemExit("paper_batches differs from the oracle")
+    print(f"next2: ok ({d.n_nets} nets, {nb} Alg. 1 batches)", flush=True)
+
+
 SCENARIOS = {k[3:]: v for k, v in globals().items() if k.startswith("sc_")}
 
 if __name__ == "__main__":
