@@ -2011,7 +2011,7 @@ la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, doubl
     const int64_t ne = shard ? ctx->n_own : ctx->n_nets;
     const int32_t *lst = shard ? ctx->d_own_pos : nullptr;
     if (v1) CK(launch_elmore_v1(ctx->G, ctx->F, ctx->S, 0, ne, lst, ctx->stream));
-    else CK(launch_elmore(ctx->F, ctx->S, ctx->d_tab, 0, ne, lst, ctx->stream));
+    else CK(launch_elmore(ctx->F, ctx->S, ctx->d_tab, ctx->L, 0, ne, lst, ctx->stream));
     prof_end(ctx, pe);
     ctx->stats.launches += 1;
     if (ctx->nccl) {

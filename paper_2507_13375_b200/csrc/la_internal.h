@@ -173,8 +173,8 @@ cudaError_t launch_unpack_decisions(const DevScratch &S, int64_t node_beg, int64
 // k_elmore over the nets [net_beg, net_end) of `list` (forest positions), or over the positions
 // [net_beg, net_end) themselves when list is null: la_tree.cu (launch_elmore), the round-1 kernel
 // in la_kernels.cu (launch_elmore_v1, A/B only).
-cudaError_t launch_elmore(const DevForest &F, const DevScratch &S, const TechTab *tab, int64_t net_beg, int64_t net_end,
-                          const int32_t *list, cudaStream_t s);
+cudaError_t launch_elmore(const DevForest &F, const DevScratch &S, const TechTab *tab, int L, int64_t net_beg,
+                          int64_t net_end, const int32_t *list, cudaStream_t s);
 cudaError_t launch_elmore_v1(const DevGrid &G, const DevForest &F, const DevScratch &S, int64_t net_beg,
                              int64_t net_end, const int32_t *list, cudaStream_t s);
 

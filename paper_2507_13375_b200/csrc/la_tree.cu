@@ -64,7 +64,14 @@ __device__ __forceinline__ Chunk decode(const DevForest &F, int4 c) {
 // once its parent has read it) live in shared memory, [node][thread], for nets of at most
 // ELM_LOCAL nodes, in global scratch beyond.  Measured alternatives (profiles/r02_elm_*): a warp
 // per chunk of nets with lane = node in height steps ran 4x slower (2.5 active lanes per
-// instruction in the via-stack loops).
+// instruction in the via-stack loops).  Round 2, session 4 (config 5, one box, 10 steps): the
+// via stacks sum each branch set once per change point (via_stack): 4.61 -> 4.18 ms, 1.34G warp
+// instructions; a CTA per block of consecutive nets with every field staged into shared memory
+// by coalesced loads (row-major 7.5-10 ms: bank conflicts; transposed [node-in-net][net] columns
+// 7.6-8.9 ms for 64/128-thread CTAs and 192-1024-node capacities): DRAM 7.9 -> 4.8 GB, but 2.5x
+// the instructions, 10-13 active lanes and barrier stalls between the phases; the next node's
+// fields loaded before the current node's arithmetic: 4.35 ms (107 registers; config 4 2.94 ->
+// 2.64 ms); register caps of 80 / 64 (6 / 8 CTAs per SM): 4.97 / 8.57 ms (spills).
 #ifndef ELM_LOCAL
 #define ELM_LOCAL 6
 #endif
@@ -103,6 +110,39 @@ __device__ __forceinline__ void elm_up(const Vals &V, const TechTab &T, const De
     }
     V.Cd[V.at(n)] = C0 + K;
     V.Rc[V.at(n)] = F0u + R;
+}
+
+// The via stack of one node (K7): T(k+1) = T(k) + vr[k] C>=(k+1) going up from the entry layer
+// to t, T(k-1) = T(k) + vr[k-1] C<=(k-1) going down to b.  C>=(j) sums the branches (sinks in
+// input order, then sons in child order) with layer >= j in that canonical order; the set only
+// changes where j passes a branch's layer, so one sum serves every level up to the smallest
+// branch layer >= j (down: the largest <= j) — the same terms in the same order, hence the same
+// double, bit for bit, with one sum per distinct branch layer instead of one per level.
+// each(f) calls f(layer, C) for every branch in canonical order; TK(k) is T at layer k.
+template <class Each, class TKf>
+__device__ __forceinline__ void via_stack(const TechTab &T, int ln, int b, int t, Each each, TKf TK) {
+    for (int j = ln + 1; j <= t;) {
+        double acc = 0.0;
+        int lim = t;
+        each([&](int l, double c) {
+            if (l >= j) {
+                acc = acc + c;
+                lim = min(lim, l);
+            }
+        });
+        for (; j <= lim; ++j) TK(j) = TK(j - 1) + T.vr[j - 1] * acc;
+    }
+    for (int j = ln - 1; j >= b;) {
+        double acc = 0.0;
+        int lim = b;
+        each([&](int l, double c) {
+            if (l <= j) {
+                acc = acc + c;
+                lim = max(lim, l);
+            }
+        });
+        for (; j >= lim; --j) TK(j) = TK(j + 1) + T.vr[j] * acc;
+    }
 }
 
 // Top-down (K7): T through the via stack [b, t] of node n (entry layer ln), then the pi wires of
@@ -144,25 +184,19 @@ __device__ __forceinline__ void elm_down(const Vals &V, const TechTab &T, const 
             pc[u] = F.p_cap[qa + u];
         }
     }
-    auto branch_sum = [&](int j, bool up) {
-        double acc = 0.0;
+    auto each = [&](auto f) {
         if (few) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (u < ns && (up ? pl[u] >= j : pl[u] <= j)) acc = acc + pc[u];
+                if (u < ns) f(pl[u], pc[u]);
         } else {
-            for (int64_t q = qa; q < qa + ns; ++q) {
-                const int pq = F.p_layer[q];
-                if (up ? pq >= j : pq <= j) acc = acc + F.p_cap[q];
-            }
+            for (int64_t q = qa; q < qa + ns; ++q) f((int)F.p_layer[q], F.p_cap[q]);
         }
 #pragma unroll
         for (int i = 0; i < MAXKIDS; ++i)
-            if (i < nk && (up ? lsk[i] >= j : lsk[i] <= j)) acc = acc + cbk[i];
-        return acc;
+            if (i < nk) f(lsk[i], cbk[i]);
     };
-    for (int k = ln; k < t; ++k) TK(k + 1) = TK(k) + T.vr[k] * branch_sum(k + 1, true);
-    for (int k = ln; k > b; --k) TK(k - 1) = TK(k) + T.vr[k - 1] * branch_sum(k - 1, false);
+    via_stack(T, ln, b, t, each, [&](int k) -> double & { return TK(k); });
     if (few) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -180,7 +214,7 @@ __global__ void __launch_bounds__(ELM_T, ELM_MINB) k_elmore(DevForest F, DevScra
                                                  int64_t net_beg, int64_t net_end, const int32_t *__restrict__ list) {
     __shared__ TechTab T;
     __shared__ double sv[2][ELM_LOCAL][ELM_T];   // Cdown; rc, then T(in)
-    __shared__ double Tks[MAXL][ELM_T];           // T(n, k) of the current node, a column per thread
+    extern __shared__ double Tks[];               // [L][ELM_T]: T(n, k) of the current node, a column per thread
     stage_tab(T, tab);
     __syncthreads();
     const int64_t idx = net_beg + blockIdx.x * (int64_t)ELM_T + threadIdx.x;
@@ -202,7 +236,7 @@ __global__ void __launch_bounds__(ELM_T, ELM_MINB) k_elmore(DevForest F, DevScra
     for (int64_t n = n1 - 1; n >= n0; --n) {
         const int4 k4 = reinterpret_cast<const int4 *>(F.kid)[n];
         const int kid[4] = {k4.x, k4.y, k4.z, k4.w};
-        elm_down(V, T, F, lay, S.sink_delay, &Tks[0][threadIdx.x], n, lay[n], S.sb[n], S.st[n], n == n1 - 1,
+        elm_down(V, T, F, lay, S.sink_delay, &Tks[threadIdx.x], n, lay[n], S.sb[n], S.st[n], n == n1 - 1,
                  F.sink0[n], F.nsink[n], F.nkid[n], kid);
     }
 }
@@ -405,11 +439,12 @@ cudaError_t tree_grid(K kernel, int64_t n_chunks, unsigned *grid) {
 
 }  // namespace
 
-cudaError_t launch_elmore(const DevForest &F, const DevScratch &S, const TechTab *tab, int64_t net_beg, int64_t net_end,
-                          const int32_t *list, cudaStream_t s) {
+cudaError_t launch_elmore(const DevForest &F, const DevScratch &S, const TechTab *tab, int L, int64_t net_beg,
+                          int64_t net_end, const int32_t *list, cudaStream_t s) {
     const int64_t n = net_end - net_beg;
     if (n <= 0) return cudaSuccess;
-    k_elmore<<<(unsigned)((n + ELM_T - 1) / ELM_T), ELM_T, 0, s>>>(F, S, tab, net_beg, net_end, list);
+    const size_t sm = sizeof(double) * (size_t)L * ELM_T;
+    k_elmore<<<(unsigned)((n + ELM_T - 1) / ELM_T), ELM_T, sm, s>>>(F, S, tab, net_beg, net_end, list);
     return cudaGetLastError();
 }
 
