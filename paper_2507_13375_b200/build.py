@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 SO = os.path.join(LIBDIR, "libgapla.so")
-SOURCES = ["la_host.cpp", "la_kernels.cu", "la_assign.cu", "la_batch.cu", "la_order.cu", "la_tree.cu"]
+SOURCES = ["la_host.cpp", "la_kernels.cu", "la_assign.cu", "la_batch.cu", "la_order.cu", "la_tree.cu", "la_solution.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

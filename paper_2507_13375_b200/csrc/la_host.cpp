@@ -109,9 +109,6 @@ struct la_ctx {
 
     // forest (host copies needed for outputs)
     int64_t n_nets = 0, n_pins = 0, n_nodes = 0, n_sinks = 0;
-    hvec<uint32_t> h_xy;
-    hvec<int32_t> h_len;
-    hvec<uint8_t> h_edir;
     std::vector<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
     int32_t LD = 0;                           // layer slots per direction
@@ -128,9 +125,12 @@ struct la_ctx {
     // la_get_solution: decisions copied to the host and the per-net counts, kept between the count
     // query and the fill call until the next assignment or reset
     bool sol_valid = false;
-    std::vector<uint8_t> sol_lay, sol_sb, sol_st;
-    std::vector<double> sol_froot;
-    std::vector<int64_t> sol_nw, sol_nv, sol_pos_of;
+    int64_t *d_sol_w = nullptr;               // [4][N+1] wire / via counts and offsets (la_solution.cu)
+    double *d_sol_cost = nullptr;             // [N] f[root] in input order
+    unsigned long long *d_sol_vc = nullptr;   // via cuts
+    void *d_sol_temp = nullptr;               // CUB scan scratch
+    size_t sol_temp_bytes = 0;
+    int64_t sol_nw_total = 0, sol_nv_total = 0;
     int32_t *d_own_pos = nullptr;             // world > 1: this rank's nets (forest positions), every batch
     int64_t n_own = 0;
     int32_t put_batch = -1;                   // host transport: batch whose reconciled decisions arrived
@@ -799,10 +799,20 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     }
     ctx->n_wire_api = ctx->wire_off[L];
     ctx->n_via_api = (int64_t)(L - 1) * g->X * g->Y;
-    for (int64_t i = 0; i < ctx->n_wire_api; i++)
-        if (g->wire_cap[i] < 0) { delete ctx; return set_err(LA_EINVAL, "negative wire capacity"); }
-    for (int64_t i = 0; i < ctx->n_via_api; i++)
-        if (g->via_cap[i] < 0) { delete ctx; return set_err(LA_EINVAL, "negative via capacity"); }
+    {   // capacities >= 0, checked on the host threads (one pass over each array)
+        const unsigned nthr = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        auto any_neg = [&](const int32_t *a, int64_t n) {
+            std::atomic<bool> bad{false};
+            par_chunks(n, n < (1 << 20) ? 1u : nthr, [&](unsigned, int64_t lo, int64_t hi) {
+                int32_t m = 0;
+                for (int64_t i = lo; i < hi; i++) m |= a[i];   // sign bit of any element
+                if (m < 0) bad = true;
+            });
+            return bad.load();
+        };
+        if (any_neg(g->wire_cap, ctx->n_wire_api)) { delete ctx; return set_err(LA_EINVAL, "negative wire capacity"); }
+        if (any_neg(g->via_cap, ctx->n_via_api)) { delete ctx; return set_err(LA_EINVAL, "negative via capacity"); }
+    }
 
     // technology tables (O4): VR[a][b] ascending sums; Eq. (3) marginals with host libm
     std::memset(&ctx->tab, 0, sizeof(TechTab));
@@ -862,15 +872,31 @@ la_status la_init_grid(const la_grid_desc *g, la_ctx **out) {
     if ((st = up(&ctx->d_wH, (const int32_t *)nullptr, (size_t)(g->X - 1) * g->Y * ctx->LH)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_wV, (const int32_t *)nullptr, (size_t)g->X * (g->Y - 1) * ctx->LV)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_via, (const int32_t *)nullptr, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
-    if ((st = up(&ctx->d_wcap, g->wire_cap, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
-    if ((st = up(&ctx->d_vcap, g->via_cap, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+    // capacities (and initial demand) through the pinned pipeline (copy_many), not pageable copies
+    if ((st = up(&ctx->d_wcap, (const int32_t *)nullptr, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
+    if ((st = up(&ctx->d_vcap, (const int32_t *)nullptr, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_wire_off, ctx->wire_off.data(), (size_t)L + 1)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_Mpos, Mpos.data(), (size_t)nd)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_Mzero, Mzero.data(), (size_t)nd)) != LA_OK) return fail(st);
     if ((st = up(&ctx->d_tab, &ctx->tab, 1)) != LA_OK) return fail(st);
     int32_t *d_wdem0 = nullptr, *d_vdem0 = nullptr;
-    if (g->wire_dem0 && (st = up(&d_wdem0, g->wire_dem0, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
-    if (g->via_dem0 && (st = up(&d_vdem0, g->via_dem0, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+    if (g->wire_dem0 && (st = up(&d_wdem0, (const int32_t *)nullptr, (size_t)ctx->n_wire_api)) != LA_OK) return fail(st);
+    if (g->via_dem0 && (st = up(&d_vdem0, (const int32_t *)nullptr, (size_t)ctx->n_via_api)) != LA_OK) return fail(st);
+    {
+        std::vector<Xfer> xs{{ctx->d_wcap, g->wire_cap, sizeof(int32_t) * (size_t)ctx->n_wire_api},
+                             {ctx->d_vcap, g->via_cap, sizeof(int32_t) * (size_t)ctx->n_via_api}};
+        if (d_wdem0) xs.push_back({d_wdem0, g->wire_dem0, sizeof(int32_t) * (size_t)ctx->n_wire_api});
+        if (d_vdem0) xs.push_back({d_vdem0, g->via_dem0, sizeof(int32_t) * (size_t)ctx->n_via_api});
+        e = cudaStreamSynchronize(ctx->stream);   // the small table uploads above are on ctx->stream
+        if (e == cudaSuccess) e = copy_many(xs, g->device, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            if (d_wdem0) dfree(d_wdem0);
+            if (d_vdem0) dfree(d_vdem0);
+            delete ctx;
+            return cuda_fail(nullptr, e, "grid upload");
+        }
+        for (const Xfer &x : xs) ctx->stats.h2d_bytes += (int64_t)x.bytes;
+    }
 
     DevGrid &G = ctx->G;
     G.X = g->X; G.Y = g->Y; G.L = L; G.LH = ctx->LH; G.LV = ctx->LV;
@@ -1041,6 +1067,66 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             return set_err(LA_EINVAL, "net " + std::to_string(net) + ": more than 65534 LA-tree nodes or sinks");
 
     phase("tree build");
+    std::vector<int64_t> cnode(nchunks + 1, 0), csink(nchunks + 1, 0);
+    for (int64_t c = 0; c < nchunks; c++) {
+        cnode[c + 1] = cnode[c] + (int64_t)chunks[c].acc.xy.size();
+        csink[c + 1] = csink[c] + (int64_t)chunks[c].acc.p_layer.size();
+    }
+    // ---- upload the trees as built (input-order chunks) on a background thread while the host
+    // orders and batches the nets: the copies depend on the build only (k_permute_forest lays the
+    // forest out batch-major once the order is known).  The thread owns its allocations until the
+    // join below; every return path between here and the join joins it first (UpJoin).
+    ForestSrc src{};
+    std::vector<void *> raw;                                // input-order device copies, freed below
+    cudaError_t up_err = cudaSuccess;
+    int64_t up_bytes = 0;
+    std::thread up_thr([&]() {
+        std::vector<Xfer> xfers;
+        auto raw_up = [&](auto member, const std::vector<int64_t> &base, int per, auto **dst) -> cudaError_t {
+            using T = typename std::remove_reference<decltype(chunks[0].acc.*member)>::type::value_type;
+            T *d = nullptr;
+            cudaError_t e = dmalloc(&d, sizeof(T) * std::max<int64_t>(base[nchunks] * per, 1));
+            if (e != cudaSuccess) return e;
+            raw.push_back(d);
+            for (int64_t c = 0; c < nchunks; c++) {
+                const auto &v = chunks[c].acc.*member;
+                if (v.empty()) continue;
+                xfers.push_back({d + base[c] * per, v.data(), sizeof(T) * v.size()});
+                up_bytes += (int64_t)(sizeof(T) * v.size());
+            }
+            *dst = d;
+            return cudaSuccess;
+        };
+        cudaError_t e = cudaSetDevice(ctx->device);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::xy, cnode, 1, &src.xy);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::kid, cnode, 4, &src.kid);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::len, cnode, 1, &src.len);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::sink0, cnode, 1, &src.sink0);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::edir, cnode, 1, &src.edir);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::nkid, cnode, 1, &src.nkid);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::nl, cnode, 1, &src.nl);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::nh, cnode, 1, &src.nh);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::nsink, cnode, 1, &src.nsink);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::height, cnode, 1, &src.height);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::wd, cnode, 1, &src.wd);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::ur, cnode, 1, &src.ur);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::p_layer, csink, 1, &src.p_layer);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::p_cap, csink, 1, &src.p_cap);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::p_w, csink, 1, &src.p_w);
+        if (e == cudaSuccess) e = raw_up(&BuiltNet::p_orig, csink, 1, &src.p_orig);
+        if (e == cudaSuccess) e = copy_many(xfers, ctx->device, cudaMemcpyHostToDevice);
+        up_err = e;
+    });
+    struct UpJoin {
+        std::thread &t;
+        std::vector<void *> &raw;
+        ~UpJoin() {
+            if (t.joinable()) {   // an early return: wait for the copies, then free their buffers
+                t.join();
+                for (void *p : raw) dfree(p);
+            }
+        }
+    } up_join{up_thr, raw};
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
     std::vector<int64_t> by_rank(N);
     // key range of order_key: a small range (priorities, wirelengths) is ordered by a parallel
@@ -1278,11 +1364,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (NN >= ((int64_t)1 << 31) || NS >= ((int64_t)1 << 31)) return set_err(LA_EINVAL, "forest too large");
     // ---- upload the trees as built (chunk by chunk, input order); k_permute_forest lays them out
     // batch-major on the GPU (rebasing child ids and sink offsets) -- no host staging pass
-    std::vector<int64_t> cnode(nchunks + 1, 0), csink(nchunks + 1, 0);
-    for (int64_t c = 0; c < nchunks; c++) {
-        cnode[c + 1] = cnode[c] + (int64_t)chunks[c].acc.xy.size();
-        csink[c + 1] = csink[c] + (int64_t)chunks[c].acc.p_layer.size();
-    }
     if (cnode[nchunks] != NN || csink[nchunks] != NS) return set_err(LA_EINVAL, "internal: forest size mismatch");
     hvec<int64_t> src_node0(N), src_sink0(N);
     hvec<uint8_t> pdrv(N);
@@ -1302,34 +1383,10 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     for (auto &ch : chunks) { wl += ch.acc.wl; wsw += ch.acc.wsw; maxh = std::max(maxh, ch.max_height); }
     phase("forest source offsets");
 
-    ForestSrc src{};
-    std::vector<void *> raw;                                // input-order device copies, freed below
-    std::vector<Xfer> xfers;                                // their uploads (pipelined, below)
-    auto raw_up = [&](auto member, const std::vector<int64_t> &base, int per, auto **dst) -> cudaError_t {
-        using T = typename std::remove_reference<decltype(chunks[0].acc.*member)>::type::value_type;
-        T *d = nullptr;
-        cudaError_t e = dmalloc(&d, sizeof(T) * std::max<int64_t>(base[nchunks] * per, 1));
-        if (e != cudaSuccess) return e;
-        raw.push_back(d);
-        for (int64_t c = 0; c < nchunks; c++) {
-            const auto &v = chunks[c].acc.*member;
-            if (v.empty()) continue;
-            xfers.push_back({d + base[c] * per, v.data(), sizeof(T) * v.size()});
-            ctx->stats.h2d_bytes += (int64_t)(sizeof(T) * v.size());
-        }
-        *dst = d;
-        return cudaSuccess;
-    };
-    CK(raw_up(&BuiltNet::xy, cnode, 1, &src.xy)); CK(raw_up(&BuiltNet::kid, cnode, 4, &src.kid));
-    CK(raw_up(&BuiltNet::len, cnode, 1, &src.len)); CK(raw_up(&BuiltNet::sink0, cnode, 1, &src.sink0));
-    CK(raw_up(&BuiltNet::edir, cnode, 1, &src.edir)); CK(raw_up(&BuiltNet::nkid, cnode, 1, &src.nkid));
-    CK(raw_up(&BuiltNet::nl, cnode, 1, &src.nl)); CK(raw_up(&BuiltNet::nh, cnode, 1, &src.nh));
-    CK(raw_up(&BuiltNet::nsink, cnode, 1, &src.nsink)); CK(raw_up(&BuiltNet::height, cnode, 1, &src.height));
-    CK(raw_up(&BuiltNet::wd, cnode, 1, &src.wd)); CK(raw_up(&BuiltNet::ur, cnode, 1, &src.ur));
-    CK(raw_up(&BuiltNet::p_layer, csink, 1, &src.p_layer)); CK(raw_up(&BuiltNet::p_cap, csink, 1, &src.p_cap));
-    CK(raw_up(&BuiltNet::p_w, csink, 1, &src.p_w)); CK(raw_up(&BuiltNet::p_orig, csink, 1, &src.p_orig));
-    CK(cudaStreamSynchronize(ctx->stream));                 // the allocations above precede the copies
-    CK(copy_many(xfers, ctx->device, cudaMemcpyHostToDevice));
+    // the as-built arrays were uploaded by the background thread started after the build
+    up_thr.join();
+    CK(up_err);
+    ctx->stats.h2d_bytes += up_bytes;
     int64_t *d_srcn = nullptr, *d_srcs = nullptr, *d_dsts = nullptr;
     CK(dmalloc(&d_srcn, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcn);
     CK(dmalloc(&d_srcs, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcs);
@@ -1364,16 +1421,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv; F.height = d_height;
     CK(launch_permute_forest(F, src, ctx->stream));
     ctx->stats.launches += N > 0 ? 1 : 0;
-    // the host keeps x/y, length and direction per node (batch-major) for la_get_solution
-    hvec<uint32_t> xy(NN);
-    hvec<int32_t> len(NN);
-    hvec<uint8_t> edir(NN);
-    if (NN) {
-        CK(cudaMemcpyAsync(xy.data(), d_xy, sizeof(uint32_t) * NN, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(len.data(), d_len, sizeof(int32_t) * NN, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(edir.data(), d_edir, NN, cudaMemcpyDeviceToHost, ctx->stream));
-    }
-    ctx->stats.d2h_bytes += 9 * NN;
     CK(cudaStreamSynchronize(ctx->stream));
     for (void *q : raw) dfree(q);
     DevScratch &S = ctx->S;
@@ -1488,9 +1535,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("  (slots)");
     CK(cudaStreamSynchronize(ctx->stream));
     phase("  (sync)");
-    ctx->h_xy.swap(xy);
-    ctx->h_len.swap(len);
-    ctx->h_edir.swap(edir);
     ctx->h_net_node0.swap(node0);
     ctx->h_net_id.swap(net_id);
     phase("grid/tickets/slots");
@@ -2028,13 +2072,14 @@ la_status la_eval_timing(la_ctx *ctx, double *sink_delay, double *net_cap, doubl
         }
         prof_end(ctx, pr);
     }
-    if (sink_delay && ctx->n_pins)
-        CK(cudaMemcpyAsync(sink_delay, ctx->S.sink_delay, sizeof(double) * ctx->n_pins, cudaMemcpyDeviceToHost, ctx->stream));
-    if (net_cap && ctx->n_nets)
-        CK(cudaMemcpyAsync(net_cap, ctx->S.net_cap, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
-    if (net_rc && ctx->n_nets)
-        CK(cudaMemcpyAsync(net_rc, ctx->S.net_rc, sizeof(double) * ctx->n_nets, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    {   // outputs to the caller's (pageable) buffers through the pinned pipeline
+        std::vector<Xfer> xs;
+        if (sink_delay && ctx->n_pins) xs.push_back({sink_delay, ctx->S.sink_delay, sizeof(double) * (size_t)ctx->n_pins});
+        if (net_cap && ctx->n_nets) xs.push_back({net_cap, ctx->S.net_cap, sizeof(double) * (size_t)ctx->n_nets});
+        if (net_rc && ctx->n_nets) xs.push_back({net_rc, ctx->S.net_rc, sizeof(double) * (size_t)ctx->n_nets});
+        CK(copy_many(xs, ctx->device, cudaMemcpyDeviceToHost));
+    }
     ctx->stats.d2h_bytes += (sink_delay ? 8 * ctx->n_pins : 0) + (net_cap ? 8 * ctx->n_nets : 0) +
                             (net_rc ? 8 * ctx->n_nets : 0);
     return LA_OK;
@@ -2045,89 +2090,65 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     TRY(require_done(ctx));
     const int64_t N = ctx->n_nets, NN = ctx->n_nodes;
     const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-    std::vector<uint8_t> &lay = ctx->sol_lay, &sb = ctx->sol_sb, &st = ctx->sol_st;
-    std::vector<double> &froot = ctx->sol_froot;
-    std::vector<int64_t> &nw = ctx->sol_nw, &nv = ctx->sol_nv, &pos_of = ctx->sol_pos_of;
+    const bool verbose = getenv("GAPLA_VERBOSE") != nullptr;   // phase times to stderr
+    auto tph = std::chrono::steady_clock::now();
+    auto phase = [&](const char *what) {
+        if (!verbose) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[gapla solution] %-24s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tph).count());
+        tph = t;
+    };
+    // counts, offsets, costs and the rows on the GPU (la_solution.cu); the caller's buffers are
+    // filled through the pinned pipeline
+    if (!ctx->d_sol_w) {
+        TRY(dev_alloc(ctx, &ctx->d_sol_w, 4 * (N + 1)));   // wcnt, vcnt, wptr, vptr
+        TRY(dev_alloc(ctx, &ctx->d_sol_cost, std::max<int64_t>(N, 1)));
+        TRY(dev_alloc(ctx, &ctx->d_sol_vc, 1));
+        CK(sol_count(ctx->F, ctx->S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                     &ctx->sol_temp_bytes, ctx->stream));
+        TRY(dev_alloc(ctx, &ctx->d_sol_temp, std::max<size_t>(ctx->sol_temp_bytes, 16)));
+    }
+    int64_t *wcnt = ctx->d_sol_w, *vcnt = wcnt + (N + 1), *wptr = vcnt + (N + 1), *vptr = wptr + (N + 1);
     if (!ctx->sol_valid) {
-    lay.resize(NN); sb.resize(NN); st.resize(NN);
-    froot.resize(N);
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(copy_many({{lay.data(), ctx->S.lay, (size_t)NN}, {sb.data(), ctx->S.sb, (size_t)NN}, {st.data(), ctx->S.st, (size_t)NN},
-                  {froot.data(), ctx->S.froot, sizeof(double) * N}}, ctx->device, cudaMemcpyDeviceToHost));
-    ctx->stats.d2h_bytes += 3 * NN + 8 * N;
-    // per input net: counts (threads over positions)
-    nw.assign(N + 1, 0);
-    nv.assign(N + 1, 0);
-    pos_of.resize(N);
-    std::vector<int64_t> vc_part(nthr + 1, 0);
-    {
-        std::vector<std::thread> th;
-        for (unsigned t = 0; t < nthr; t++)
-            th.emplace_back([&, t] {
-                int64_t vc = 0;
-                for (int64_t p = N * t / nthr; p < N * (t + 1) / nthr; p++) {
-                    const int64_t net = ctx->h_net_id[p];
-                    pos_of[net] = p;
-                    const int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
-                    nw[net + 1] = (b - a) - 1;
-                    int64_t v = 0;
-                    for (int64_t k = a; k < b; k++) {
-                        if (st[k] > sb[k]) v++;
-                        vc += st[k] - sb[k];
-                    }
-                    nv[net + 1] = v;
-                }
-                vc_part[t] = vc;
-            });
-        for (auto &x : th) x.join();
+        CK(sol_count(ctx->F, ctx->S, wcnt, vcnt, wptr, vptr, ctx->d_sol_cost, ctx->d_sol_vc, ctx->d_sol_temp,
+                     &ctx->sol_temp_bytes, ctx->stream));
+        ctx->stats.launches += 3;
+        int64_t tot[2] = {0, 0};
+        unsigned long long vc = 0;
+        CK(cudaMemcpyAsync(&tot[0], wptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&tot[1], vptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&vc, ctx->d_sol_vc, sizeof(vc), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->stats.d2h_bytes += 24;
+        ctx->sol_nw_total = tot[0];
+        ctx->sol_nv_total = tot[1];
+        ctx->stats.via_cuts = (int64_t)vc;
+        ctx->sol_valid = true;
+        phase("counts (GPU)");
     }
-    int64_t vcuts = 0;
-    for (unsigned t = 0; t < nthr; t++) vcuts += vc_part[t];
-    ctx->stats.via_cuts = vcuts;
-    for (int64_t i = 0; i < N; i++) { nw[i + 1] += nw[i]; nv[i + 1] += nv[i]; }
-    ctx->sol_valid = true;
-    }
-    if (n_wires) *n_wires = nw[N];
-    if (n_vias) *n_vias = nv[N];
-    if (wire_ptr) std::memcpy(wire_ptr, nw.data(), sizeof(int64_t) * (N + 1));
-    if (via_ptr) std::memcpy(via_ptr, nv.data(), sizeof(int64_t) * (N + 1));
-    if (net_cost)
-        par_for(N, nthr, [&](int64_t i) { net_cost[i] = froot[pos_of[i]]; });
+    const int64_t NWt = ctx->sol_nw_total, NVt = ctx->sol_nv_total;
+    if (n_wires) *n_wires = NWt;
+    if (n_vias) *n_vias = NVt;
+    std::vector<Xfer> xs;
+    int32_t *d_rows = nullptr;
     if (wires || vias) {
-        std::vector<std::thread> th;
-        for (unsigned t = 0; t < nthr; t++)
-            th.emplace_back([&, t] {
-                std::vector<std::array<int32_t, 5>> W;
-                std::vector<std::array<int32_t, 4>> V;
-                for (int64_t net = N * t / nthr; net < N * (t + 1) / nthr; net++) {
-                    const int64_t p = pos_of[net];
-                    const int64_t a = ctx->h_net_node0[p], b = ctx->h_net_node0[p + 1];
-                    W.clear();
-                    V.clear();
-                    for (int64_t k = a; k < b; k++) {
-                        const int x = ctx->h_xy[k] & 0xffff, y = ctx->h_xy[k] >> 16;
-                        if (ctx->h_edir[k] != NO_DIR) {
-                            const int ln = ctx->h_len[k];
-                            int qx = x, qy = y;   // parent GCell
-                            switch (ctx->h_edir[k]) {
-                                case DIR_E: qx = x - ln; break;
-                                case DIR_W: qx = x + ln; break;
-                                case DIR_N: qy = y - ln; break;
-                                default: qy = y + ln; break;
-                            }
-                            W.push_back({std::min(x, qx), std::min(y, qy), std::max(x, qx), std::max(y, qy),
-                                         (int32_t)lay[k]});
-                        }
-                        if (st[k] > sb[k]) V.push_back({x, y, (int32_t)sb[k], (int32_t)st[k]});
-                    }
-                    std::sort(W.begin(), W.end());
-                    std::sort(V.begin(), V.end());
-                    if (wires) std::memcpy(wires + 5 * nw[net], W.data(), 20 * W.size());
-                    if (vias) std::memcpy(vias + 4 * nv[net], V.data(), 16 * V.size());
-                }
-            });
-        for (auto &x : th) x.join();
+        CK(dmalloc(&d_rows, sizeof(int32_t) * (size_t)std::max<int64_t>(5 * NWt + 4 * NVt, 1)));
+        cudaError_t e = sol_fill(ctx->F, ctx->S, wptr, vptr, d_rows, d_rows + 5 * NWt, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) { dfree(d_rows); return cuda_fail(ctx, e, "la_get_solution: fill"); }
+        ctx->stats.launches += 1;
+        if (wires && NWt) xs.push_back({wires, d_rows, sizeof(int32_t) * 5 * (size_t)NWt});
+        if (vias && NVt) xs.push_back({vias, d_rows + 5 * NWt, sizeof(int32_t) * 4 * (size_t)NVt});
+        phase("rows (GPU)");
     }
+    if (wire_ptr) xs.push_back({wire_ptr, wptr, sizeof(int64_t) * (size_t)(N + 1)});
+    if (via_ptr) xs.push_back({via_ptr, vptr, sizeof(int64_t) * (size_t)(N + 1)});
+    if (net_cost && N) xs.push_back({net_cost, ctx->d_sol_cost, sizeof(double) * (size_t)N});
+    cudaError_t e = copy_many(xs, ctx->device, cudaMemcpyDeviceToHost);
+    if (d_rows) dfree(d_rows);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_solution: copies");
+    for (const Xfer &x : xs) ctx->stats.d2h_bytes += (int64_t)x.bytes;
+    phase("to host");
     return LA_OK;
 }
 

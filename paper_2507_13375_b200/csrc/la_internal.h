@@ -202,6 +202,16 @@ struct OrderIn {
 cudaError_t gpu_paper_batches(const OrderIn &in, int32_t *batch_of, int32_t *n_batches, cudaStream_t s,
                               int64_t *launches);
 
+// la_get_solution on the GPU (la_solution.cu): sol_count fills wcnt / vcnt [N+1] (input net order),
+// their exclusive sums wptr / vptr [N+1], cost [N] = f[root] and *vcuts; temp == nullptr queries
+// the CUB scratch size.  sol_fill writes each net's wires (5 x int32) and via stacks (4 x int32)
+// at its offsets, ascending.
+cudaError_t sol_count(const DevForest &F, const DevScratch &S, int64_t *wcnt, int64_t *vcnt, int64_t *wptr,
+                      int64_t *vptr, double *cost, unsigned long long *vcuts, void *temp, size_t *temp_bytes,
+                      cudaStream_t s);
+cudaError_t sol_fill(const DevForest &F, const DevScratch &S, const int64_t *wptr, const int64_t *vptr, int32_t *wires,
+                     int32_t *vias, cudaStream_t s);
+
 // Evaluator (la_kernels.cu): histogram of (layer, c == 0, clamp(d - c)) over one packed
 // plane with `slots` layers per element group (slot -> layer via layer_of), exact
 // legacy sum of max(0, d - c) per layer, and the out-of-domain count.
