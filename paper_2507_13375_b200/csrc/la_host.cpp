@@ -128,9 +128,10 @@ struct la_ctx {
     int64_t *d_sol_w = nullptr;               // [4][N+1] wire / via counts and offsets (la_solution.cu)
     double *d_sol_cost = nullptr;             // [N] f[root] in input order
     unsigned long long *d_sol_vc = nullptr;   // via cuts
-    void *d_sol_temp = nullptr;               // CUB scan scratch
+    char *d_sol_temp = nullptr;               // CUB scan scratch
     size_t sol_temp_bytes = 0;
     int64_t sol_nw_total = 0, sol_nv_total = 0;
+    int32_t *d_sol_rows = nullptr;            // wires (5 x int32) then via stacks (4 x int32), in dev_allocs
     int32_t *d_own_pos = nullptr;             // world > 1: this rank's nets (forest positions), every batch
     int64_t n_own = 0;
     int32_t put_batch = -1;                   // host transport: batch whose reconciled decisions arrived
@@ -416,22 +417,33 @@ bool ok_nonneg(const double *a, int n) {
 // driver GCell; children ordered E, W, N, S; sinks keep input order.
 struct BuiltNet {
     // per node, final order (height ascending, then preorder)
-    std::vector<uint32_t> xy;
-    std::vector<int32_t> kid;      // 4 per node, local final ids, -1
-    std::vector<int32_t> len;
-    std::vector<uint8_t> edir, nkid, nl, nh;
-    std::vector<int32_t> sink0;    // local sink offset
-    std::vector<uint16_t> nsink;
-    std::vector<double> wd, ur;
-    std::vector<uint16_t> height;
+    hvec<uint32_t> xy;
+    hvec<int32_t> kid;      // 4 per node, local final ids, -1
+    hvec<int32_t> len;
+    hvec<uint8_t> edir, nkid, nl, nh;
+    hvec<int32_t> sink0;    // local sink offset
+    hvec<uint16_t> nsink;
+    hvec<double> wd, ur;
+    hvec<uint16_t> height;
     // sinks grouped by node in final node order
-    std::vector<uint8_t> p_layer;
-    std::vector<double> p_cap, p_w;
-    std::vector<int64_t> p_orig;
-    std::vector<uint64_t> fp;      // footprint elements
+    hvec<uint8_t> p_layer;
+    hvec<double> p_cap, p_w;
+    hvec<int64_t> p_orig;
+    hvec<uint64_t> fp;      // footprint elements
     int64_t wl = 0;                // unit edges (summed over the nets appended)
     int64_t wsw = 0;               // sum over tree edges of len x #legal layers of the edge direction
 };
+
+// Section timers of Builder::build for the CPU harness (tools/hostbench); no-ops in the library.
+#ifdef GAPLA_BUILD_PROF
+inline uint64_t bprof_now() { return __builtin_ia32_rdtsc(); }
+thread_local uint64_t bprof_acc[16], bprof_t;
+#define BPROF(k) do { const uint64_t t_ = bprof_now(); bprof_acc[k] += t_ - bprof_t; bprof_t = t_; } while (0)
+#define BPROF_START() (bprof_t = bprof_now())
+#else
+#define BPROF(k) do {} while (0)
+#define BPROF_START() do {} while (0)
+#endif
 
 struct Builder {
     const la_ctx *ctx;
@@ -443,7 +455,6 @@ struct Builder {
     std::vector<uint8_t> mask;     // neighbour bits per vertex (1 << dir)
     std::vector<int32_t> vnode;    // vertex -> preorder node id, -1
     std::vector<int32_t> stack, bfs;
-    std::vector<uint64_t> pcells;
     // preorder tree
     std::vector<int32_t> px, py, ppar, plen, pedir, pheight, pnl, pnh;
     std::vector<std::array<int32_t, 4>> pkids;     // children per preorder node (E, W, N, S order)
@@ -453,7 +464,8 @@ struct Builder {
     std::vector<double> w, ur, pwq;                 // pwq: Eq. (4) weight per pin of the net
     std::vector<int32_t> order, finalid, pre, vof, hcnt;
     int last_height = 0;                            // height of the last built net's root
-    std::vector<uint8_t> seen;
+    std::vector<uint8_t> seen, isn;                 // isn: vertex is a tree node
+    std::vector<int32_t> nbr, pin_v;                 // [4 per vertex] neighbour; vertex of each pin
 
     // GCell -> vertex index: open-addressing hash over vs (built once per net)
     std::vector<uint64_t> hkey;
@@ -506,6 +518,7 @@ struct Builder {
                 return buf;
             }
         }
+        BPROF_START();
         ek.clear();
         for (int64_t s = s0; s < s1; s++) {
             const int32_t *q = nd->seg_xy + 4 * s;
@@ -526,6 +539,7 @@ struct Builder {
                 for (int y = std::min(y1, y2); y < std::max(y1, y2); y++) ek.push_back(((uint64_t)y * X + x1) * 2 + 1);
             }
         }
+        BPROF(0);   // pin checks + unit edges
         std::sort(ek.begin(), ek.end());
         ek.erase(std::unique(ek.begin(), ek.end()), ek.end());
         const uint64_t g_drv = (uint64_t)nd->pin_y[p0] * X + nd->pin_x[p0];
@@ -538,43 +552,52 @@ struct Builder {
         if (ek.empty()) vs.push_back(g_drv);
         std::sort(vs.begin(), vs.end());
         vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+        BPROF(1);   // sort / unique edges and vertices
         hbuild();
+        pin_v.resize(p1 - p0);
         for (int64_t p = p0; p < p1; p++) {
-            if (vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]) < 0) {
+            const int64_t v = vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]);
+            if (v < 0) {
                 std::snprintf(buf, sizeof buf, "net %lld: pin %lld GCell not on the route", (long long)net, (long long)p);
                 return buf;
             }
+            pin_v[p - p0] = (int32_t)v;
         }
         const size_t nv = vs.size();
         if (nv != ek.size() + 1) {
             std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
             return buf;
         }
+        BPROF(2);   // hash build + pin lookups
         mask.assign(nv, 0);
+        nbr.resize(4 * nv);                          // neighbour vertex per direction (where mask has it)
         for (uint64_t k : ek) {                      // both endpoints of every unit edge
             const uint64_t g = k >> 1;
+            const int32_t a = (int32_t)vfind(g);
             if (k & 1) {
-                mask[vfind(g)] |= 1 << DIR_N;
-                mask[vfind(g + X)] |= 1 << DIR_S;
+                const int32_t b = (int32_t)vfind(g + X);
+                mask[a] |= 1 << DIR_N; nbr[4 * a + DIR_N] = b;
+                mask[b] |= 1 << DIR_S; nbr[4 * b + DIR_S] = a;
             } else {
-                mask[vfind(g)] |= 1 << DIR_E;
-                mask[vfind(g + 1)] |= 1 << DIR_W;
+                const int32_t b = (int32_t)vfind(g + 1);
+                mask[a] |= 1 << DIR_E; nbr[4 * a + DIR_E] = b;
+                mask[b] |= 1 << DIR_W; nbr[4 * b + DIR_W] = a;
             }
         }
+        BPROF(3);   // neighbour masks
         // connectivity from the driver
         {
             seen.assign(nv, 0);
             bfs.clear();
-            int64_t r0 = vfind(g_drv);
-            bfs.push_back((int32_t)r0);
+            const int32_t r0 = pin_v[0];               // the driver's GCell
+            bfs.push_back(r0);
             seen[r0] = 1;
             for (size_t h = 0; h < bfs.size(); h++) {
-                uint64_t g = vs[bfs[h]];
-                int x = (int)(g % X), y = (int)(g / X);
+                const int32_t v = bfs[h];
                 for (int d = 0; d < 4; d++) {
-                    if (!(mask[bfs[h]] >> d & 1)) continue;
-                    int64_t j = vfind((uint64_t)(y + DY[d]) * X + (x + DX[d]));
-                    if (!seen[j]) { seen[j] = 1; bfs.push_back((int32_t)j); }
+                    if (!(mask[v] >> d & 1)) continue;
+                    const int32_t j = nbr[4 * v + d];
+                    if (!seen[j]) { seen[j] = 1; bfs.push_back(j); }
                 }
             }
             if (bfs.size() != nv) {
@@ -582,15 +605,16 @@ struct Builder {
                 return buf;
             }
         }
-        pcells.clear();
-        for (int64_t p = p0; p < p1; p++) pcells.push_back((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]);
-        std::sort(pcells.begin(), pcells.end());
-        auto is_node = [&](size_t vi) {
-            if (std::binary_search(pcells.begin(), pcells.end(), vs[vi])) return true;
-            uint8_t m = mask[vi];
-            if (__builtin_popcount(m) != 2) return true;
-            return !(m == ((1 << DIR_E) | (1 << DIR_W)) || m == ((1 << DIR_N) | (1 << DIR_S)));
-        };
+        BPROF(4);   // BFS connectivity
+        // tree nodes (O1): pin GCells, GCells of degree != 2 and bends
+        isn.assign(nv, 0);
+        for (int64_t p = p0; p < p1; p++) isn[pin_v[p - p0]] = 1;
+        for (size_t vi = 0; vi < nv; vi++) {
+            const uint8_t m = mask[vi];
+            if (__builtin_popcount(m) != 2 || !(m == ((1 << DIR_E) | (1 << DIR_W)) || m == ((1 << DIR_N) | (1 << DIR_S))))
+                isn[vi] = 1;
+        }
+        BPROF(5);   // pin cells
         // preorder DFS from the root, children E, W, N, S
         px.clear(); py.clear(); ppar.clear(); plen.clear(); pedir.clear(); pkids.clear(); pnk.clear();
         vnode.assign(nv, -1);
@@ -602,7 +626,7 @@ struct Builder {
         };
         pre.clear();
         {
-            int64_t rv = vfind(g_drv);
+            const int32_t rv = pin_v[0];
             add((int)(g_drv % X), (int)(g_drv / X), -1, 0, -1, rv);
             stack.assign(1, 0);
             vof.assign(1, (int32_t)rv);
@@ -616,10 +640,10 @@ struct Builder {
                     if (ppar[n] >= 0 && d == OPP[pedir[n]]) continue;
                     if (!(mask[vof[n]] >> d & 1)) continue;
                     int cx = px[n] + DX[d], cy = py[n] + DY[d], ln = 1;
-                    int64_t vi = vfind((uint64_t)cy * X + cx);
-                    while (!is_node(vi)) {
+                    int32_t vi = nbr[4 * vof[n] + d];
+                    while (!isn[vi]) {                 // straight through: the run continues in d
                         cx += DX[d]; cy += DY[d]; ln++;
-                        vi = vfind((uint64_t)cy * X + cx);
+                        vi = nbr[4 * vi + d];
                     }
                     int32_t k = add(cx, cy, n, ln, d, vi);
                     vof.push_back((int32_t)vi);
@@ -629,6 +653,7 @@ struct Builder {
                 for (int i = nk - 1; i >= 0; i--) stack.push_back(kids[i]);
             }
         }
+        BPROF(6);   // preorder DFS (run walks)
         const size_t nn = px.size();
         // pins: nl/nh over all pins (driver included); sinks in input order
         pnl.assign(nn, 255);
@@ -637,7 +662,7 @@ struct Builder {
         pin_node.resize(p1 - p0);
         pwq.resize(p1 - p0);
         for (int64_t p = p0; p < p1; p++) {
-            int32_t n = vnode[vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p])];
+            int32_t n = vnode[pin_v[p - p0]];
             pin_node[p - p0] = n;
             pnl[n] = std::min<int32_t>(pnl[n], nd->pin_layer[p]);
             pnh[n] = std::max<int32_t>(pnh[n], nd->pin_layer[p]);
@@ -651,6 +676,7 @@ struct Builder {
         sink_list.resize(sink_beg[nn]);
         for (size_t n = 0; n < nn; n++) sink_cnt[n] = sink_beg[n];     // fill cursors
         for (int64_t p = p0 + 1; p < p1; p++) sink_list[sink_cnt[pin_node[p - p0]]++] = p;   // input order per node
+        BPROF(7);   // pins -> nodes, Eq. (4) weights, sink lists
         // heights; subtree max sink weight (Eq. 5, reading R3); 0 without sinks (R39)
         pheight.assign(nn, 0);
         w.assign(nn, 0.0);
@@ -667,6 +693,7 @@ struct Builder {
         ur.assign(nn, 0.0);
         for (int32_t n : pre)
             ur[n] = (ppar[n] < 0) ? (nd->r_drv ? nd->r_drv[net] : 0.0) : ur[ppar[n]] + ctx->r_avg * plen[n];
+        BPROF(8);   // heights, w, ur
         // final order: height ascending, then preorder
         // (counting sort by height, stable in preorder; the root has the largest height)
         hcnt.assign((size_t)pheight[pre[0]] + 2, 0);
@@ -676,16 +703,20 @@ struct Builder {
         for (int32_t n : pre) order[hcnt[pheight[n]]++] = n;
         finalid.assign(nn, -1);
         for (size_t i = 0; i < nn; i++) finalid[order[i]] = (int32_t)i;
+        BPROF(9);   // final order
         // appended to the chunk's arrays (node ids and sink offsets stay net-local)
-        const size_t b0 = out.xy.size(), q0 = out.p_layer.size();
-        out.xy.resize(b0 + nn); out.kid.resize((b0 + nn) * 4, -1); out.len.resize(b0 + nn); out.edir.resize(b0 + nn);
+        // (default-initialising vectors: one resize per array per net, every element written below)
+        const size_t b0 = out.xy.size(), q0 = out.p_layer.size(), nq = (size_t)sink_beg[nn];
+        out.xy.resize(b0 + nn); out.kid.resize((b0 + nn) * 4); out.len.resize(b0 + nn); out.edir.resize(b0 + nn);
         out.nkid.resize(b0 + nn); out.nl.resize(b0 + nn); out.nh.resize(b0 + nn); out.sink0.resize(b0 + nn);
         out.nsink.resize(b0 + nn); out.wd.resize(b0 + nn); out.ur.resize(b0 + nn); out.height.resize(b0 + nn);
+        out.p_layer.resize(q0 + nq); out.p_cap.resize(q0 + nq); out.p_w.resize(q0 + nq); out.p_orig.resize(q0 + nq);
+        size_t qo = q0;
         for (size_t j = 0; j < nn; j++) {
             const size_t i = b0 + j;
             int32_t n = order[j];
             out.xy[i] = (uint32_t)px[n] | ((uint32_t)py[n] << 16);
-            for (int k = 0; k < pnk[n]; k++) out.kid[i * 4 + k] = finalid[pkids[n][k]];
+            for (int k = 0; k < 4; k++) out.kid[i * 4 + k] = k < pnk[n] ? finalid[pkids[n][k]] : -1;
             out.len[i] = plen[n];
             out.edir[i] = ppar[n] < 0 ? NO_DIR : (uint8_t)pedir[n];
             out.nkid[i] = pnk[n];
@@ -694,24 +725,28 @@ struct Builder {
             out.wd[i] = ctx->W_D * w[n];
             out.ur[i] = ur[n];
             out.height[i] = (uint16_t)std::min(pheight[n], 65535);
-            out.sink0[i] = (int32_t)(out.p_layer.size() - q0);
+            out.sink0[i] = (int32_t)(qo - q0);
             out.nsink[i] = (uint16_t)(sink_beg[n + 1] - sink_beg[n]);
-            for (int32_t qi = sink_beg[n]; qi < sink_beg[n + 1]; qi++) {
+            for (int32_t qi = sink_beg[n]; qi < sink_beg[n + 1]; qi++, qo++) {
                 const int64_t q = sink_list[qi];
-                out.p_layer.push_back(nd->pin_layer[q]);
-                out.p_cap.push_back(nd->pin_cap[q]);
+                out.p_layer[qo] = nd->pin_layer[q];
+                out.p_cap[qo] = nd->pin_cap[q];
                 // pin-via delay weight: w^d_{n->par} for a non-root node (Alg. 3 l.6), W_D * w_q at the root (R13)
-                out.p_w.push_back(ppar[n] < 0 ? ctx->W_D * pwq[q - p0] : ctx->W_D * w[n]);
-                out.p_orig.push_back(q);
+                out.p_w[qo] = ppar[n] < 0 ? ctx->W_D * pwq[q - p0] : ctx->W_D * w[n];
+                out.p_orig[qo] = q;
             }
         }
+        BPROF(10);  // output arrays
         // footprint = unit edges U node GCells (disjoint element spaces)
-        for (uint64_t k : ek) out.fp.push_back(k);
+        const size_t f0 = out.fp.size();
+        out.fp.resize(f0 + ek.size() + nn);
+        std::memcpy(out.fp.data() + f0, ek.data(), sizeof(uint64_t) * ek.size());
         const uint64_t gbase = (uint64_t)2 * X * Y;
-        for (size_t n = 0; n < nn; n++) out.fp.push_back(gbase + (uint64_t)py[n] * X + px[n]);
+        for (size_t n = 0; n < nn; n++) out.fp[f0 + ek.size() + n] = gbase + (uint64_t)py[n] * X + px[n];
         out.wl += (int64_t)ek.size();
         for (size_t n = 0; n < nn; n++)
             if (ppar[n] >= 0) out.wsw += (int64_t)plen[n] * nlegal[(pedir[n] == DIR_E || pedir[n] == DIR_W) ? 0 : 1];
+        BPROF(11);  // footprint
         last_height = pheight[pre[0]];
         return "";
     }
@@ -726,6 +761,31 @@ struct Chunk {
     int64_t err_net = -1;
     int max_height = 0;
 };
+
+// Reserve a chunk's arrays once from upper bounds (nodes <= pins + 2 segments: every tree node is
+// a pin GCell or an endpoint of a segment; unit edges <= the summed segment lengths; sinks = pins
+// - nets), so they never regrow: no reallocation copies, and pages are touched (faulted) once --
+// reserved but untouched virtual memory costs nothing, and default_init_alloc backs buffers of
+// 32 MB and more with transparent huge pages.
+void reserve_chunk(Chunk &ch, const la_net_desc *nd) {
+    const int64_t P = nd->pin_ptr[ch.end] - nd->pin_ptr[ch.beg];
+    const int64_t s0 = nd->seg_ptr[ch.beg], s1 = nd->seg_ptr[ch.end];
+    int64_t len = 0;
+    for (int64_t s = s0; s < s1; s++) {
+        const int32_t *q = nd->seg_xy + 4 * s;
+        len += std::abs((int64_t)q[2] - q[0]) + std::abs((int64_t)q[3] - q[1]);
+    }
+    const int64_t nodes = P + 2 * (s1 - s0) + 1, sinks = std::max<int64_t>(0, P - (ch.end - ch.beg));
+    BuiltNet &a = ch.acc;
+    a.xy.reserve(nodes); a.kid.reserve(4 * nodes); a.len.reserve(nodes); a.edir.reserve(nodes);
+    a.nkid.reserve(nodes); a.nl.reserve(nodes); a.nh.reserve(nodes); a.sink0.reserve(nodes);
+    a.nsink.reserve(nodes); a.wd.reserve(nodes); a.ur.reserve(nodes); a.height.reserve(nodes);
+    a.p_layer.reserve(sinks); a.p_cap.reserve(sinks); a.p_w.reserve(sinks); a.p_orig.reserve(sinks);
+    a.fp.reserve(len + nodes);
+    ch.node_off.reserve(ch.end - ch.beg + 1);
+    ch.sink_off.reserve(ch.end - ch.beg + 1);
+    ch.fp_off.reserve(ch.end - ch.beg + 1);
+}
 
 }  // namespace
 
@@ -987,6 +1047,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             int64_t c = next.fetch_add(1);
             if (c >= nchunks) break;
             Chunk &ch = chunks[c];
+            reserve_chunk(ch, n);
             ch.node_off.assign(1, 0);
             ch.sink_off.assign(1, 0);
             ch.fp_off.assign(1, 0);
@@ -1425,6 +1486,8 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     for (void *q : raw) dfree(q);
     DevScratch &S = ctx->S;
     TRY(dev_alloc(ctx, &S.froot, N));
+    // la_get_solution's rows: N trees have NN - N edges (wires) and at most NN via stacks
+    TRY(dev_alloc(ctx, &ctx->d_sol_rows, std::max<int64_t>(5 * (NN - N) + 4 * NN, 1)));
     TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
     TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
     TRY(dev_alloc(ctx, &S.sink_delay, std::max<int64_t>(ctx->n_pins, 1)));
@@ -2130,12 +2193,11 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     if (n_wires) *n_wires = NWt;
     if (n_vias) *n_vias = NVt;
     std::vector<Xfer> xs;
-    int32_t *d_rows = nullptr;
+    int32_t *d_rows = ctx->d_sol_rows;   // allocated at load: 5 (nodes - nets) + 4 nodes int32 >= the rows
     if (wires || vias) {
-        CK(dmalloc(&d_rows, sizeof(int32_t) * (size_t)std::max<int64_t>(5 * NWt + 4 * NVt, 1)));
         cudaError_t e = sol_fill(ctx->F, ctx->S, wptr, vptr, d_rows, d_rows + 5 * NWt, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-        if (e != cudaSuccess) { dfree(d_rows); return cuda_fail(ctx, e, "la_get_solution: fill"); }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_solution: fill");
         ctx->stats.launches += 1;
         if (wires && NWt) xs.push_back({wires, d_rows, sizeof(int32_t) * 5 * (size_t)NWt});
         if (vias && NVt) xs.push_back({vias, d_rows + 5 * NWt, sizeof(int32_t) * 4 * (size_t)NVt});
@@ -2145,7 +2207,6 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     if (via_ptr) xs.push_back({via_ptr, vptr, sizeof(int64_t) * (size_t)(N + 1)});
     if (net_cost && N) xs.push_back({net_cost, ctx->d_sol_cost, sizeof(double) * (size_t)N});
     cudaError_t e = copy_many(xs, ctx->device, cudaMemcpyDeviceToHost);
-    if (d_rows) dfree(d_rows);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "la_get_solution: copies");
     for (const Xfer &x : xs) ctx->stats.d2h_bytes += (int64_t)x.bytes;
     phase("to host");
