@@ -454,7 +454,7 @@ struct Builder {
     std::vector<uint64_t> vs;      // vertex gcells
     std::vector<uint8_t> mask;     // neighbour bits per vertex (1 << dir)
     std::vector<int32_t> vnode;    // vertex -> preorder node id, -1
-    std::vector<int32_t> stack, bfs;
+    std::vector<int32_t> stack;
     // preorder tree
     std::vector<int32_t> px, py, ppar, plen, pedir, pheight, pnl, pnh;
     std::vector<std::array<int32_t, 4>> pkids;     // children per preorder node (E, W, N, S order)
@@ -472,19 +472,25 @@ struct Builder {
     std::vector<int32_t> hval;
     uint64_t hmask = 0;
     int hshift = 0;
-    void hbuild() {
+    void hinit(size_t maxn) {                     // empty table for up to maxn GCells
         int bits = 4;
-        while (((size_t)1 << bits) < 2 * vs.size()) bits++;
+        while (((size_t)1 << bits) < 2 * maxn) bits++;
         hkey.assign((size_t)1 << bits, ~0ull);
         hval.resize((size_t)1 << bits);
         hmask = ((uint64_t)1 << bits) - 1;
         hshift = 64 - bits;
-        for (size_t i = 0; i < vs.size(); i++) {
-            uint64_t h = (vs[i] * 0x9E3779B97F4A7C15ull) >> hshift;
-            while (hkey[h] != ~0ull) h = (h + 1) & hmask;
-            hkey[h] = vs[i];
-            hval[h] = (int32_t)i;
+        vs.clear();
+    }
+    int32_t hinsert(uint64_t g) {                 // vertex of GCell g, added if new
+        uint64_t h = (g * 0x9E3779B97F4A7C15ull) >> hshift;
+        while (hkey[h] != ~0ull) {
+            if (hkey[h] == g) return hval[h];
+            h = (h + 1) & hmask;
         }
+        hkey[h] = g;
+        hval[h] = (int32_t)vs.size();
+        vs.push_back(g);
+        return hval[h];
     }
     int64_t vfind(uint64_t g) const {
         uint64_t h = (g * 0x9E3779B97F4A7C15ull) >> hshift;
@@ -543,17 +549,28 @@ struct Builder {
         std::sort(ek.begin(), ek.end());
         ek.erase(std::unique(ek.begin(), ek.end()), ek.end());
         const uint64_t g_drv = (uint64_t)nd->pin_y[p0] * X + nd->pin_x[p0];
-        vs.clear();
-        for (uint64_t k : ek) {
-            uint64_t g = k >> 1;
-            vs.push_back(g);
-            vs.push_back((k & 1) ? g + X : g + 1);
+        // vertices: the edges' endpoints, deduplicated on insertion into the GCell -> vertex hash
+        // (numbered in first-seen order: the numbering is internal), with each vertex's
+        // neighbour bits and neighbour vertex per direction filled in the same pass
+        const size_t vmax = 2 * ek.size() + 1;
+        hinit(vmax);
+        mask.assign(vmax, 0);
+        nbr.resize(4 * vmax);                        // neighbour vertex per direction (where mask has it)
+        for (uint64_t k : ek) {                      // both endpoints of every unit edge
+            const uint64_t g = k >> 1;
+            const int32_t a = hinsert(g);
+            if (k & 1) {
+                const int32_t b = hinsert(g + X);
+                mask[a] |= 1 << DIR_N; nbr[4 * a + DIR_N] = b;
+                mask[b] |= 1 << DIR_S; nbr[4 * b + DIR_S] = a;
+            } else {
+                const int32_t b = hinsert(g + 1);
+                mask[a] |= 1 << DIR_E; nbr[4 * a + DIR_E] = b;
+                mask[b] |= 1 << DIR_W; nbr[4 * b + DIR_W] = a;
+            }
         }
-        if (ek.empty()) vs.push_back(g_drv);
-        std::sort(vs.begin(), vs.end());
-        vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
-        BPROF(1);   // sort / unique edges and vertices
-        hbuild();
+        if (ek.empty()) hinsert(g_drv);
+        BPROF(1);   // sort / unique edges, vertices and neighbours
         pin_v.resize(p1 - p0);
         for (int64_t p = p0; p < p1; p++) {
             const int64_t v = vfind((uint64_t)nd->pin_y[p] * X + nd->pin_x[p]);
@@ -568,44 +585,9 @@ struct Builder {
             std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
             return buf;
         }
-        BPROF(2);   // hash build + pin lookups
-        mask.assign(nv, 0);
-        nbr.resize(4 * nv);                          // neighbour vertex per direction (where mask has it)
-        for (uint64_t k : ek) {                      // both endpoints of every unit edge
-            const uint64_t g = k >> 1;
-            const int32_t a = (int32_t)vfind(g);
-            if (k & 1) {
-                const int32_t b = (int32_t)vfind(g + X);
-                mask[a] |= 1 << DIR_N; nbr[4 * a + DIR_N] = b;
-                mask[b] |= 1 << DIR_S; nbr[4 * b + DIR_S] = a;
-            } else {
-                const int32_t b = (int32_t)vfind(g + 1);
-                mask[a] |= 1 << DIR_E; nbr[4 * a + DIR_E] = b;
-                mask[b] |= 1 << DIR_W; nbr[4 * b + DIR_W] = a;
-            }
-        }
+        BPROF(2);   // pin lookups
         BPROF(3);   // neighbour masks
-        // connectivity from the driver
-        {
-            seen.assign(nv, 0);
-            bfs.clear();
-            const int32_t r0 = pin_v[0];               // the driver's GCell
-            bfs.push_back(r0);
-            seen[r0] = 1;
-            for (size_t h = 0; h < bfs.size(); h++) {
-                const int32_t v = bfs[h];
-                for (int d = 0; d < 4; d++) {
-                    if (!(mask[v] >> d & 1)) continue;
-                    const int32_t j = nbr[4 * v + d];
-                    if (!seen[j]) { seen[j] = 1; bfs.push_back(j); }
-                }
-            }
-            if (bfs.size() != nv) {
-                std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
-                return buf;
-            }
-        }
-        BPROF(4);   // BFS connectivity
+        BPROF(4);   // (connectivity: checked by the DFS below)
         // tree nodes (O1): pin GCells, GCells of degree != 2 and bends
         isn.assign(nv, 0);
         for (int64_t p = p0; p < p1; p++) isn[pin_v[p - p0]] = 1;
@@ -625,8 +607,13 @@ struct Builder {
             return (int32_t)px.size() - 1;
         };
         pre.clear();
+        // every vertex is walked exactly once from the driver iff the route is a tree (nv = edges + 1
+        // was checked): a vertex met twice closes a cycle, fewer than nv walked leaves a component out
+        seen.assign(nv, 0);
+        size_t walked = 1;
         {
             const int32_t rv = pin_v[0];
+            seen[rv] = 1;
             add((int)(g_drv % X), (int)(g_drv / X), -1, 0, -1, rv);
             stack.assign(1, 0);
             vof.assign(1, (int32_t)rv);
@@ -641,7 +628,15 @@ struct Builder {
                     if (!(mask[vof[n]] >> d & 1)) continue;
                     int cx = px[n] + DX[d], cy = py[n] + DY[d], ln = 1;
                     int32_t vi = nbr[4 * vof[n] + d];
-                    while (!isn[vi]) {                 // straight through: the run continues in d
+                    for (;;) {                         // straight through non-nodes: the run continues in d
+                        if (seen[vi]) {
+                            std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)",
+                                          (long long)net);
+                            return buf;
+                        }
+                        seen[vi] = 1;
+                        walked++;
+                        if (isn[vi]) break;
                         cx += DX[d]; cy += DY[d]; ln++;
                         vi = nbr[4 * vi + d];
                     }
@@ -652,6 +647,10 @@ struct Builder {
                 }
                 for (int i = nk - 1; i >= 0; i--) stack.push_back(kids[i]);
             }
+        }
+        if (walked != nv) {
+            std::snprintf(buf, sizeof buf, "net %lld: route is not a tree (cycle or disconnected)", (long long)net);
+            return buf;
         }
         BPROF(6);   // preorder DFS (run walks)
         const size_t nn = px.size();
