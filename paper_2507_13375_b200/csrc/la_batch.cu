@@ -127,7 +127,7 @@ cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int ele
     DevBuf kin, kout, tmp, outdeg, indeg, off, cursor, succ, batch, fa, fb, cnt;
     BCK(kin.alloc(8 * n_keys));
     BCK(kout.alloc(8 * n_keys));
-    BCK(cudaMemcpyAsync(kin.p, h_keys, 8 * n_keys, cudaMemcpyHostToDevice, s));
+    BCK(pinned_copy(kin.p, h_keys, 8 * n_keys, cudaMemcpyHostToDevice));   // pinned pipeline (the allocation synced)
     // K1: sort (element, rank) pairs
     size_t tmp_bytes = 0;
     int end_bit = 32 + elem_bits;

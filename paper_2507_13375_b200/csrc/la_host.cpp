@@ -109,7 +109,7 @@ struct la_ctx {
 
     // forest (host copies needed for outputs)
     int64_t n_nets = 0, n_pins = 0, n_nodes = 0, n_sinks = 0;
-    std::vector<int64_t> h_net_node0, h_net_id;
+    hvec<int64_t> h_net_node0, h_net_id;
     std::vector<int64_t> batch_net0;          // [n_batches+1] first net (batch-major) of each batch
     int32_t LD = 0;                           // layer slots per direction
     int32_t NS = NS_DEFAULT, NP = NP_DEFAULT; // small-path capacities of k_assign
@@ -146,7 +146,7 @@ struct la_ctx {
     // 16-byte load per net instead of a chain of dependent loads in k_assign
     int4 *d_big_pos = nullptr, *d_small_pos = nullptr;               // batch order
     int4 *d_flow_big_pos = nullptr, *d_flow_small_pos = nullptr;     // dataflow priority order
-    std::vector<int64_t> h_net_sink0;                                // [n_nets+1] first sink per position
+    hvec<int64_t> h_net_sink0;                                       // [n_nets+1] first sink per position
     int32_t n_big_ctas = 0;
     std::vector<int32_t> snap_batch;          // la_set_snapshot_batches (input order); empty: conflict-free
     bool hybrid = true;                       // batch-mode launches: all CTAs take big nets first
@@ -366,6 +366,19 @@ cudaError_t copy_many(const std::vector<Xfer> &xs, int device, cudaMemcpyKind ki
     for (auto &t : th) t.join();
     return (cudaError_t)err.load();
 }
+
+}  // namespace
+
+namespace gapla {
+cudaError_t pinned_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    return copy_many({{dst, src, bytes}}, dev, kind);
+}
+}  // namespace gapla
+
+namespace {
 
 // Run f(t, begin, end) on nthr threads over contiguous blocks [n*t/nthr, n*(t+1)/nthr).
 template <class F>
@@ -1072,10 +1085,10 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (ch.err_net >= 0) return set_err(LA_EINVAL, ch.err);
 
     // per-net index: chunk and local position; flat per-net node and sink counts
-    std::vector<int32_t> chunk_of(N);
+    hvec<int32_t> chunk_of(N);                // (default-initialised: every element is written)
     for (int64_t c = 0; c < nchunks; c++)
         for (int64_t i = chunks[c].beg; i < chunks[c].end; i++) chunk_of[i] = (int32_t)c;
-    std::vector<int32_t> nn_of(N), ns_of(N);
+    hvec<int32_t> nn_of(N), ns_of(N);
     par_for(N, nthr, [&](int64_t net) {
         const Chunk &ch = chunks[chunk_of[net]];
         const int64_t i = net - ch.beg;
@@ -1188,7 +1201,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         }
     } up_join{up_thr, raw};
     // ---- priority order (order_key, index) and footprint keys (element << 32 | rank)
-    std::vector<int64_t> by_rank(N);
+    hvec<int64_t> by_rank(N);
     // key range of order_key: a small range (priorities, wirelengths) is ordered by a parallel
     // counting sort, stable in input order -- the same (key, index) order as the comparison sort
     int64_t kmin = 0, kmax = -1;
@@ -1242,7 +1255,8 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     } else {
         for (int64_t i = 0; i < N; i++) by_rank[i] = i;
     }
-    std::vector<int64_t> fp_pos(N + 1, 0);
+    hvec<int64_t> fp_pos(N + 1);
+    fp_pos[0] = 0;
     par_for(N, nthr, [&](int64_t r) {
         const int64_t net = by_rank[r];
         const Chunk &ch = chunks[chunk_of[net]];
@@ -1306,7 +1320,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
 
     phase("GPU batching");
     // ---- batch-major net order: by batch, then node count descending, then rank
-    std::vector<int64_t> pos_net(N);   // final position -> input net
+    hvec<int64_t> pos_net(N);          // final position -> input net
     {
         std::vector<int64_t> cnt(nb + 1, 0);
         for (int64_t i = 0; i < N; i++) cnt[ctx->batch_of_net[i] + 1]++;
@@ -1360,7 +1374,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     small_pos.reserve(N);
     ctx->batch_big0.assign(1, 0);
     ctx->batch_small0.assign(1, 0);
-    std::vector<uint8_t> big_at(N);
+    hvec<uint8_t> big_at(N);
     par_for(N, nthr, [&](int64_t p) {
         const int64_t net = pos_net[p];
         big_at[p] = is_big(net, ctx->batch_of_net[net]) ? 1 : 0;
@@ -1406,7 +1420,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     }
     phase("DAG to positions");
     // offsets in final order
-    std::vector<int64_t> node0(N + 1, 0), sink0g(N + 1, 0);
+    hvec<int64_t> node0(N + 1), sink0g(N + 1);
+    node0[0] = 0;
+    sink0g[0] = 0;
     int64_t max_nodes = 0;
     par_for(N, nthr, [&](int64_t p) {
         node0[p + 1] = nn_of[pos_net[p]];
@@ -1427,7 +1443,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     if (cnode[nchunks] != NN || csink[nchunks] != NS) return set_err(LA_EINVAL, "internal: forest size mismatch");
     hvec<int64_t> src_node0(N), src_sink0(N);
     hvec<uint8_t> pdrv(N);
-    std::vector<int64_t> net_id(N);
+    hvec<int64_t> net_id(N);
     par_for(N, nthr, [&](int64_t p) {
         const int64_t net = pos_net[p];
         const int32_t c = chunk_of[net];

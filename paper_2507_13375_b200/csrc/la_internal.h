@@ -202,6 +202,10 @@ struct OrderIn {
 cudaError_t gpu_paper_batches(const OrderIn &in, int32_t *batch_of, int32_t *n_batches, cudaStream_t s,
                               int64_t *launches);
 
+// A large copy between pageable host memory and the device through the pinned pipeline of
+// la_host.cpp (copy_many): returns once the bytes have landed.
+cudaError_t pinned_copy(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind);
+
 // la_get_solution on the GPU (la_solution.cu): sol_count fills wcnt / vcnt [N+1] (input net order),
 // their exclusive sums wptr / vptr [N+1], cost [N] = f[root] and *vcuts; temp == nullptr queries
 // the CUB scratch size.  sol_fill writes each net's wires (5 x int32) and via stacks (4 x int32)
