@@ -1522,8 +1522,9 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         CK(cudaMemsetAsync(ctx->d_ticket, 0, sizeof(unsigned long long) * 2 * (nb + 1), ctx->stream));
         ctx->h_big_pos = big_pos;
         ctx->h_small_pos = small_pos;
-        ctx->h_net_node0.assign(node0.begin(), node0.end());
-        ctx->h_net_sink0.assign(sink0g.begin(), sink0g.end());
+        ctx->h_net_node0.swap(node0);      // node0 / sink0g are read through the ctx from here on
+        ctx->h_net_sink0.swap(sink0g);
+        const hvec<int64_t> &nd0 = ctx->h_net_node0, &sk0 = ctx->h_net_sink0;
         phase("  (ticket alloc)");
         const std::vector<int4> ib = pack_nets(ctx, big_pos), is = pack_nets(ctx, small_pos);
         phase("  (pack_nets)");
@@ -1541,29 +1542,44 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             ctx->h_jobs.clear();
             ctx->batch_job0.assign(1, 0);
             const int WA = ctx->warp_arena;
-            for (int32_t b = 0; b < nb && ctx->group_path; b++) {
-                const int64_t m0 = ctx->batch_small0[b], m1 = ctx->batch_small0[b + 1];
-                int64_t s0 = 0, s1 = 0;
-                la_shard_range(m1 - m0, ctx->world, ctx->rank, &s0, &s1);
-                int4 cur{0, 0, 0, 0};
-                int used = 0;
-                for (int64_t idx = m0 + s0; idx < m0 + s1; idx++) {
-                    const int32_t p = small_pos[idx];
-                    const int bytes = (int)assign_group_net_bytes((int)(node0[p + 1] - node0[p]),
-                                                                  (int)(sink0g[p + 1] - sink0g[p]), ctx->L, ctx->LD);
-                    if (cur.y == 4 || (cur.y > 0 && used + bytes > WA)) {
-                        ctx->h_jobs.push_back(cur);
-                        cur = int4{0, 0, 0, 0};
-                        used = 0;
+            // batches are packed independently (host threads over batches), then concatenated in order
+            std::vector<std::vector<int4>> bj(ctx->group_path ? nb : 0);
+            std::atomic<int32_t> nxb{0};
+            auto packer = [&]() {
+                for (int32_t b; (b = nxb.fetch_add(1)) < (int32_t)bj.size();) {
+                    std::vector<int4> &out = bj[b];
+                    const int64_t m0 = ctx->batch_small0[b], m1 = ctx->batch_small0[b + 1];
+                    int64_t s0 = 0, s1 = 0;
+                    la_shard_range(m1 - m0, ctx->world, ctx->rank, &s0, &s1);
+                    int4 cur{0, 0, 0, 0};
+                    int used = 0;
+                    for (int64_t idx = m0 + s0; idx < m0 + s1; idx++) {
+                        const int32_t p = small_pos[idx];
+                        const int bytes = (int)assign_group_net_bytes((int)(nd0[p + 1] - nd0[p]), (int)(sk0[p + 1] - sk0[p]),
+                                                                      ctx->L, ctx->LD);
+                        if (cur.y == 4 || (cur.y > 0 && used + bytes > WA)) {
+                            out.push_back(cur);
+                            cur = int4{0, 0, 0, 0};
+                            used = 0;
+                        }
+                        if (cur.y == 0) cur.x = (int32_t)idx;
+                        else if (cur.y == 1) cur.z = used;
+                        else if (cur.y == 2) cur.z |= used << 16;
+                        else cur.w = used;
+                        cur.y++;
+                        used += bytes;
                     }
-                    if (cur.y == 0) cur.x = (int32_t)idx;
-                    else if (cur.y == 1) cur.z = used;
-                    else if (cur.y == 2) cur.z |= used << 16;
-                    else cur.w = used;
-                    cur.y++;
-                    used += bytes;
+                    if (cur.y) out.push_back(cur);
                 }
-                if (cur.y) ctx->h_jobs.push_back(cur);
+            };
+            {
+                std::vector<std::thread> th;
+                for (unsigned i = 1; i < nthr && bj.size() > 1; i++) th.emplace_back(packer);
+                packer();
+                for (auto &t : th) t.join();
+            }
+            for (auto &v : bj) {
+                ctx->h_jobs.insert(ctx->h_jobs.end(), v.begin(), v.end());
                 ctx->batch_job0.push_back((int64_t)ctx->h_jobs.size());
             }
             if (ctx->group_path) TRY(dev_upload(ctx, &ctx->d_jobs, ctx->h_jobs.data(), ctx->h_jobs.size()));
@@ -1613,7 +1629,6 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("  (slots)");
     CK(cudaStreamSynchronize(ctx->stream));
     phase("  (sync)");
-    ctx->h_net_node0.swap(node0);
     ctx->h_net_id.swap(net_id);
     phase("grid/tickets/slots");
     auto t3 = std::chrono::steady_clock::now();
@@ -1876,12 +1891,13 @@ la_status la_commit_demand(la_ctx *ctx, int32_t batch) {
 // Packed k_assign records of the nets at forest positions `pos` (+ one dummy: never empty).
 static std::vector<int4> pack_nets(const la_ctx *ctx, const std::vector<int32_t> &pos) {
     std::vector<int4> v(pos.size() + 1, int4{0, 0, 0, 0});
-    for (size_t i = 0; i < pos.size(); i++) {
+    const unsigned nthr = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    par_for((int64_t)pos.size(), nthr, [&](int64_t i) {
         const int64_t p = pos[i];
         const int64_t n0 = ctx->h_net_node0[p], nn = ctx->h_net_node0[p + 1] - n0;
         const int64_t q0 = ctx->h_net_sink0[p], ns = ctx->h_net_sink0[p + 1] - q0;
         v[i] = int4{(int)p, (int)n0, (int)(nn | (ns << 16)), (int)q0};
-    }
+    });
     return v;
 }
 
