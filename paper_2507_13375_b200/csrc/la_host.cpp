@@ -389,6 +389,26 @@ void par_chunks(int64_t n, unsigned nthr, F f) {
     for (auto &x : th) x.join();
 }
 
+// In-place inclusive prefix sum of a[0, n) on nthr threads: each block sums its range, then adds
+// the sum of the blocks before it (integer: exact, the serial loop's result).
+template <class T>
+void par_prefix(T *a, int64_t n, unsigned nthr) {
+    if (n < ((int64_t)1 << 20) || nthr <= 1) {
+        for (int64_t i = 1; i < n; i++) a[i] += a[i - 1];
+        return;
+    }
+    std::vector<T> part(nthr, 0), off(nthr, 0);
+    par_chunks(n, nthr, [&](unsigned t, int64_t lo, int64_t hi) {
+        T s = 0;
+        for (int64_t i = lo; i < hi; i++) { s += a[i]; a[i] = s; }
+        part[t] = s;
+    });
+    for (unsigned t = 1; t < nthr; t++) off[t] = off[t - 1] + part[t - 1];
+    par_chunks(n, nthr, [&](unsigned t, int64_t lo, int64_t hi) {
+        if (t) for (int64_t i = lo; i < hi; i++) a[i] += off[t];
+    });
+}
+
 // Sort v by cmp on nthr threads: sorted blocks, then pairwise merges in parallel.
 template <class T, class C>
 void par_sort(std::vector<T> &v, C cmp, unsigned nthr) {
@@ -1263,7 +1283,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         const int64_t i = net - ch.beg;
         fp_pos[r + 1] = ch.fp_off[i + 1] - ch.fp_off[i];
     });
-    for (int64_t r = 0; r < N; r++) fp_pos[r + 1] += fp_pos[r];
+    par_prefix(fp_pos.data() + 1, N, nthr);
     const int64_t n_fp = fp_pos[N];
     phase("  footprint offsets");
     hvec<uint64_t> keys(n_fp);
@@ -1424,14 +1444,20 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     node0[0] = 0;
     sink0g[0] = 0;
     int64_t max_nodes = 0;
-    par_for(N, nthr, [&](int64_t p) {
-        node0[p + 1] = nn_of[pos_net[p]];
-        sink0g[p + 1] = ns_of[pos_net[p]];
-    });
-    for (int64_t p = 0; p < N; p++) {
-        max_nodes = std::max(max_nodes, node0[p + 1]);
-        node0[p + 1] += node0[p];
-        sink0g[p + 1] += sink0g[p];
+    {
+        std::vector<int64_t> mx(nthr, 0);
+        par_chunks(N, nthr, [&](unsigned t, int64_t lo, int64_t hi) {
+            int64_t m = 0;
+            for (int64_t p = lo; p < hi; p++) {
+                node0[p + 1] = nn_of[pos_net[p]];
+                sink0g[p + 1] = ns_of[pos_net[p]];
+                m = std::max<int64_t>(m, node0[p + 1]);
+            }
+            mx[t] = m;
+        });
+        for (int64_t m : mx) max_nodes = std::max(max_nodes, m);
+        par_prefix(node0.data() + 1, N, nthr);
+        par_prefix(sink0g.data() + 1, N, nthr);
     }
     const int64_t NN = node0[N], NS = sink0g[N];
     ctx->n_nodes = NN;
