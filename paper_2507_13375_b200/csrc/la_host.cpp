@@ -192,7 +192,9 @@ struct la_ctx {
         return e;
     }
 
+    std::thread free_thr;                     // releases la_load_nets' host staging in the background
     ~la_ctx() {
+        if (free_thr.joinable()) free_thr.join();
         if (stream) cudaStreamSynchronize(stream);   // frees are ordered on the legacy stream
         cudaDeviceSynchronize();
         for (void *p : dev_allocs) dfree(p);
@@ -1493,15 +1495,13 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     CK(dmalloc(&d_srcn, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcn);
     CK(dmalloc(&d_srcs, sizeof(int64_t) * std::max<int64_t>(N, 1))); raw.push_back(d_srcs);
     CK(dmalloc(&d_dsts, sizeof(int64_t) * (N + 1))); raw.push_back(d_dsts);
-    if (N) {
-        CK(cudaMemcpyAsync(d_srcn, src_node0.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(d_srcs, src_sink0.data(), sizeof(int64_t) * N, cudaMemcpyHostToDevice, ctx->stream));
-    }
-    CK(cudaMemcpyAsync(d_dsts, sink0g.data(), sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice, ctx->stream));
+    CK(copy_many({{d_srcn, src_node0.data(), sizeof(int64_t) * (size_t)N},
+                  {d_srcs, src_sink0.data(), sizeof(int64_t) * (size_t)N},
+                  {d_dsts, sink0g.data(), sizeof(int64_t) * (size_t)(N + 1)}}, ctx->device, cudaMemcpyHostToDevice));
     ctx->stats.h2d_bytes += 8 * (3 * N + 1);
     src.src_node0 = d_srcn; src.src_sink0 = d_srcs; src.dst_sink0 = d_dsts;
-    chunks.clear();
-    chunks.shrink_to_fit();
+    // the as-built host arrays (GBs) are released on a background thread, joined by ~la_ctx
+    ctx->free_thr = std::thread([c = std::move(chunks)]() mutable { c.clear(); c.shrink_to_fit(); });
     phase("forest upload (as built)");
 
     DevForest &F = ctx->F;
@@ -1516,8 +1516,12 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     TRY(dev_alloc(ctx, &d_height, NN));
     TRY(dev_alloc(ctx, &d_ur, NN)); TRY(dev_alloc(ctx, &d_pl, NS));
     TRY(dev_alloc(ctx, &d_pc, NS)); TRY(dev_alloc(ctx, &d_pw, NS));
-    TRY(dev_alloc(ctx, &d_po, NS)); TRY(dev_upload(ctx, &d_node0, node0.data(), N + 1));
-    TRY(dev_upload(ctx, &d_netid, net_id.data(), N)); TRY(dev_upload(ctx, &d_pdrv, pdrv.data(), N));
+    TRY(dev_alloc(ctx, &d_po, NS)); TRY(dev_alloc(ctx, &d_node0, N + 1));
+    TRY(dev_alloc(ctx, &d_netid, N)); TRY(dev_alloc(ctx, &d_pdrv, N));
+    CK(copy_many({{d_node0, node0.data(), sizeof(int64_t) * (size_t)(N + 1)},
+                  {d_netid, net_id.data(), sizeof(int64_t) * (size_t)N}, {d_pdrv, pdrv.data(), (size_t)N}},
+                 ctx->device, cudaMemcpyHostToDevice));
+    ctx->stats.h2d_bytes += 8 * (2 * N + 1) + N;
     F.xy = d_xy; F.kid = d_kid; F.len = d_len; F.edir = d_edir; F.nkid = d_nkid; F.nl = d_nl; F.nh = d_nh;
     F.sink0 = d_sink0; F.nsink = d_nsink; F.wd = d_wd; F.ur = d_ur; F.p_layer = d_pl; F.p_cap = d_pc; F.p_w = d_pw;
     F.p_orig = d_po; F.net_node0 = d_node0; F.net_id = d_netid; F.net_pdrv = d_pdrv; F.height = d_height;
