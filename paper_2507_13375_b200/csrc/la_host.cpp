@@ -1531,7 +1531,15 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     for (void *q : raw) dfree(q);
     DevScratch &S = ctx->S;
     TRY(dev_alloc(ctx, &S.froot, N));
-    // la_get_solution's rows: N trees have NN - N edges (wires) and at most NN via stacks
+    // la_get_solution's buffers (allocated here, with the rest of the context's device memory):
+    // counts / offsets, costs, the CUB scan scratch, and the rows -- N trees have NN - N edges
+    // (wires) and at most NN via stacks
+    TRY(dev_alloc(ctx, &ctx->d_sol_w, 4 * (N + 1)));   // wcnt, vcnt, wptr, vptr
+    TRY(dev_alloc(ctx, &ctx->d_sol_cost, std::max<int64_t>(N, 1)));
+    TRY(dev_alloc(ctx, &ctx->d_sol_vc, 1));
+    CK(sol_count(F, S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &ctx->sol_temp_bytes,
+                 ctx->stream));
+    TRY(dev_alloc(ctx, &ctx->d_sol_temp, std::max<size_t>(ctx->sol_temp_bytes, 16)));
     TRY(dev_alloc(ctx, &ctx->d_sol_rows, std::max<int64_t>(5 * (NN - N) + 4 * NN, 1)));
     TRY(dev_alloc(ctx, &S.lay, NN)); TRY(dev_alloc(ctx, &S.sb, NN)); TRY(dev_alloc(ctx, &S.st, NN));
     TRY(dev_alloc(ctx, &S.Cd, NN)); TRY(dev_alloc(ctx, &S.rcv, NN)); TRY(dev_alloc(ctx, &S.Tin, NN));
@@ -2224,14 +2232,7 @@ la_status la_get_solution(la_ctx *ctx, int64_t *n_wires, int64_t *n_vias, int64_
     };
     // counts, offsets, costs and the rows on the GPU (la_solution.cu); the caller's buffers are
     // filled through the pinned pipeline
-    if (!ctx->d_sol_w) {
-        TRY(dev_alloc(ctx, &ctx->d_sol_w, 4 * (N + 1)));   // wcnt, vcnt, wptr, vptr
-        TRY(dev_alloc(ctx, &ctx->d_sol_cost, std::max<int64_t>(N, 1)));
-        TRY(dev_alloc(ctx, &ctx->d_sol_vc, 1));
-        CK(sol_count(ctx->F, ctx->S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                     &ctx->sol_temp_bytes, ctx->stream));
-        TRY(dev_alloc(ctx, &ctx->d_sol_temp, std::max<size_t>(ctx->sol_temp_bytes, 16)));
-    }
+    if (!ctx->d_sol_w) return set_err(LA_ESTATE, "internal: solution buffers missing");   // allocated at load
     int64_t *wcnt = ctx->d_sol_w, *vcnt = wcnt + (N + 1), *wptr = vcnt + (N + 1), *vptr = wptr + (N + 1);
     if (!ctx->sol_valid) {
         CK(sol_count(ctx->F, ctx->S, wcnt, vcnt, wptr, vptr, ctx->d_sol_cost, ctx->d_sol_vc, ctx->d_sol_temp,
