@@ -75,7 +75,10 @@ __device__ __forceinline__ Chunk decode(const DevForest &F, int4 c) {
 #ifndef ELM_LOCAL
 #define ELM_LOCAL 6
 #endif
-constexpr int ELM_T = 128;
+#ifndef ELM_T_DEF
+#define ELM_T_DEF 128
+#endif
+constexpr int ELM_T = ELM_T_DEF;   // threads per k_elmore CTA
 #ifndef ELM_MINB
 #define ELM_MINB 1      // k_elmore CTAs per SM the register budget must allow
 #endif
