@@ -71,7 +71,9 @@ __device__ __forceinline__ Chunk decode(const DevForest &F, int4 c) {
 // 7.6-8.9 ms for 64/128-thread CTAs and 192-1024-node capacities): DRAM 7.9 -> 4.8 GB, but 2.5x
 // the instructions, 10-13 active lanes and barrier stalls between the phases; the next node's
 // fields loaded before the current node's arithmetic: 4.35 ms (107 registers; config 4 2.94 ->
-// 2.64 ms); register caps of 80 / 64 (6 / 8 CTAs per SM): 4.97 / 8.57 ms (spills).
+// 2.64 ms); register caps of 80 / 64 (6 / 8 CTAs per SM): 4.97 / 8.57 ms (spills); CTAs of 64 / 32
+// threads (ELM_T_DEF; more resident warps at 93 registers): 4.18 / 4.41 ms vs 4.17 at 128, and 64
+// threads at 80 registers 4.41 ms.
 #ifndef ELM_LOCAL
 #define ELM_LOCAL 6
 #endif
