@@ -232,6 +232,12 @@ def test_call_order_errors(la):
 @pytest.mark.parametrize("net,msg", [
     (dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2)]),
      "not a tree"),
+    # a cycle plus a separate run: vertices = edges + 1, so the DFS itself must find the cycle
+    # (driver on the square) or the unreached component (driver on the separate run)
+    (dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)],
+          segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2), (4, 4, 5, 4)]), "not a tree"),
+    (dict(pins=[(4, 4, 0, 1, 0), (5, 4, 0, 1, 0), (2, 2, 0, 1, 0)],
+          segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2), (4, 4, 5, 4)]), "not a tree"),
     (dict(pins=[(0, 0, 0, 1, 0), (3, 3, 0, 1, 0)], segs=[(0, 0, 2, 0)]), "not on the route"),
     (dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 2)]), "axis-aligned"),
     (dict(pins=[(0, 0, 0, 1, 0), (2, 0, 9, 1, 0)], segs=[(0, 0, 2, 0)]), "layer"),

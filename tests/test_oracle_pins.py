@@ -109,8 +109,13 @@ def test_route_errors():
     d = synth.empty_design(8, 8, 4)
     bad = [dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2)]),
            dict(pins=[(0, 0, 0, 1, 0), (3, 3, 0, 1, 0)], segs=[(0, 0, 2, 0)]),
-           dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 2)])]
-    msgs = ["not a tree", "not on the route", "axis-aligned"]
+           dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)], segs=[(0, 0, 2, 2)]),
+           # a cycle plus a separate run (vertices = edges + 1): driver on the cycle / on the run
+           dict(pins=[(0, 0, 0, 1, 0), (2, 2, 0, 1, 0)],
+                segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2), (4, 4, 5, 4)]),
+           dict(pins=[(4, 4, 0, 1, 0), (5, 4, 0, 1, 0), (2, 2, 0, 1, 0)],
+                segs=[(0, 0, 2, 0), (2, 0, 2, 2), (0, 0, 0, 2), (0, 2, 2, 2), (4, 4, 5, 4)])]
+    msgs = ["not a tree", "not on the route", "axis-aligned", "not a tree", "not a tree"]
     for n, m in zip(bad, msgs):
         e = synth.with_nets(synth.empty_design(8, 8, 4), [n])
         with pytest.raises(oracle.OracleError, match=m):
