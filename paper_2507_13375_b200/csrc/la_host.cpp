@@ -1401,25 +1401,54 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         const int64_t net = pos_net[p];
         big_at[p] = is_big(net, ctx->batch_of_net[net]) ? 1 : 0;
     });
-    for (int32_t b = 0; b < nb; b++) {
-        for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++) {
-            if (big_at[p]) {
-                const int64_t net = pos_net[p];
-                big_pos.push_back((int32_t)p);
-                max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
-                max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
-            } else {
-                small_pos.push_back((int32_t)p);
+    {   // per batch (host threads over batches): counts, then the lists filled at their offsets
+        std::vector<int64_t> nbig(nb, 0);
+        std::vector<int64_t> mxn(nthr, 0), mxs(nthr, 0);
+        auto over_batches = [&](auto body) {
+            std::atomic<int32_t> nx{0};
+            auto w = [&](unsigned t) { for (int32_t b; (b = nx.fetch_add(1)) < nb;) body(t, b); };
+            std::vector<std::thread> th;
+            for (unsigned i = 1; i < nthr && nb > 1; i++) th.emplace_back(w, i);
+            w(0);
+            for (auto &x : th) x.join();
+        };
+        over_batches([&](unsigned t, int32_t b) {
+            int64_t c = 0;
+            for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++)
+                if (big_at[p]) {
+                    const int64_t net = pos_net[p];
+                    c++;
+                    mxn[t] = std::max(mxn[t], nnodes_of(net));
+                    mxs[t] = std::max(mxs[t], nsinks_of(net));
+                }
+            nbig[b] = c;
+        });
+        for (int32_t b = 0; b < nb; b++) {
+            ctx->batch_big0.push_back(ctx->batch_big0.back() + nbig[b]);
+            ctx->batch_small0.push_back(ctx->batch_small0.back() + (ctx->batch_net0[b + 1] - ctx->batch_net0[b]) - nbig[b]);
+        }
+        big_pos.resize(ctx->batch_big0.back());
+        small_pos.resize(ctx->batch_small0.back());
+        over_batches([&](unsigned, int32_t b) {
+            int64_t ib = ctx->batch_big0[b], is = ctx->batch_small0[b];
+            for (int64_t p = ctx->batch_net0[b]; p < ctx->batch_net0[b + 1]; p++) {
+                if (big_at[p]) big_pos[ib++] = (int32_t)p;
+                else small_pos[is++] = (int32_t)p;
             }
+        });
+        // the dataflow kernel's (k_assign) big nets: input order
+        par_chunks(N, nthr, [&](unsigned t, int64_t lo, int64_t hi) {
+            for (int64_t net = lo; net < hi; net++)
+                if (is_big_flow(net)) {
+                    mxn[t] = std::max(mxn[t], nnodes_of(net));
+                    mxs[t] = std::max(mxs[t], nsinks_of(net));
+                }
+        });
+        for (unsigned t = 0; t < nthr; t++) {
+            max_big_nodes = std::max(max_big_nodes, mxn[t]);
+            max_big_sinks = std::max(max_big_sinks, mxs[t]);
         }
-        ctx->batch_big0.push_back((int64_t)big_pos.size());
-        ctx->batch_small0.push_back((int64_t)small_pos.size());
     }
-    for (int64_t net = 0; net < N; net++)   // the dataflow kernel's (k_assign) big nets: input order, sequential
-        if (is_big_flow(net)) {
-            max_big_nodes = std::max(max_big_nodes, nnodes_of(net));
-            max_big_sinks = std::max(max_big_sinks, nsinks_of(net));
-        }
     phase("role lists");
     // dataflow DAG in forest order (snapshot batches: none -- every net has 0 predecessors)
     if (snapshot) {
