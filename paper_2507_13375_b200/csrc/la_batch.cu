@@ -118,16 +118,33 @@ void DagDev::release() {
     n = n_edges = 0;
 }
 
-cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int elem_bits, int64_t n_nets,
-                                 std::vector<int32_t> &batch_of_rank, int32_t &n_batches, cudaStream_t s,
-                                 int64_t *launches, DagDev *dag) {
+// Footprint keys (element << 32 | rank) of every input net's as-built footprint elements, in place.
+__global__ void k_fp_keys(const uint64_t *__restrict__ fp, const int64_t *__restrict__ start,
+                          const int32_t *__restrict__ rank, int64_t n, uint64_t *keys) {
+    const int64_t net = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (net >= n) return;
+    const uint64_t r = (uint32_t)rank[net];
+    for (int64_t j = start[net]; j < start[net + 1]; ++j) keys[j] = (fp[j] << 32) | r;
+}
+
+cudaError_t launch_fp_keys(const uint64_t *fp, const int64_t *start, const int32_t *rank, int64_t n, uint64_t *keys,
+                           cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_fp_keys<<<nblk(n, 256), 256, 0, s>>>(fp, start, rank, n, keys);
+    return cudaGetLastError();
+}
+
+cudaError_t gpu_conflict_batches(const uint64_t *h_keys, const uint64_t *d_keys, int64_t n_keys, int elem_bits,
+                                 int64_t n_nets, std::vector<int32_t> &batch_of_rank, int32_t &n_batches,
+                                 cudaStream_t s, int64_t *launches, DagDev *dag) {
     batch_of_rank.assign(n_nets, 0);
     n_batches = n_nets > 0 ? 1 : 0;
     if (n_nets == 0) return cudaSuccess;
     DevBuf kin, kout, tmp, outdeg, indeg, off, cursor, succ, batch, fa, fb, cnt;
     BCK(kin.alloc(8 * n_keys));
     BCK(kout.alloc(8 * n_keys));
-    BCK(pinned_copy(kin.p, h_keys, 8 * n_keys, cudaMemcpyHostToDevice));   // pinned pipeline (the allocation synced)
+    if (d_keys) BCK(cudaMemcpyAsync(kin.p, d_keys, 8 * n_keys, cudaMemcpyDeviceToDevice, s));
+    else BCK(pinned_copy(kin.p, h_keys, 8 * n_keys, cudaMemcpyHostToDevice));   // pinned pipeline (the allocation synced)
     // K1: sort (element, rank) pairs
     size_t tmp_bytes = 0;
     int end_bit = 32 + elem_bits;

@@ -1162,11 +1162,13 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             return set_err(LA_EINVAL, "net " + std::to_string(net) + ": more than 65534 LA-tree nodes or sinks");
 
     phase("tree build");
-    std::vector<int64_t> cnode(nchunks + 1, 0), csink(nchunks + 1, 0);
+    std::vector<int64_t> cnode(nchunks + 1, 0), csink(nchunks + 1, 0), cfp(nchunks + 1, 0);
     for (int64_t c = 0; c < nchunks; c++) {
         cnode[c + 1] = cnode[c] + (int64_t)chunks[c].acc.xy.size();
         csink[c + 1] = csink[c] + (int64_t)chunks[c].acc.p_layer.size();
+        cfp[c + 1] = cfp[c] + (int64_t)chunks[c].acc.fp.size();
     }
+    uint64_t *d_fp_raw = nullptr;   // the footprints as built (input order), for the GPU keys
     // ---- upload the trees as built (input-order chunks) on a background thread while the host
     // orders and batches the nets: the copies depend on the build only (k_permute_forest lays the
     // forest out batch-major once the order is known).  The thread owns its allocations until the
@@ -1209,6 +1211,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
         if (e == cudaSuccess) e = raw_up(&BuiltNet::p_cap, csink, 1, &src.p_cap);
         if (e == cudaSuccess) e = raw_up(&BuiltNet::p_w, csink, 1, &src.p_w);
         if (e == cudaSuccess) e = raw_up(&BuiltNet::p_orig, csink, 1, &src.p_orig);
+        if (e == cudaSuccess && ctx->snap_batch.empty()) e = raw_up(&BuiltNet::fp, cfp, 1, &d_fp_raw);
         if (e == cudaSuccess) e = copy_many(xfers, ctx->device, cudaMemcpyHostToDevice);
         up_err = e;
     });
@@ -1277,39 +1280,18 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     } else {
         for (int64_t i = 0; i < N; i++) by_rank[i] = i;
     }
-    hvec<int64_t> fp_pos(N + 1);
-    fp_pos[0] = 0;
-    par_for(N, nthr, [&](int64_t r) {
-        const int64_t net = by_rank[r];
+    // footprint keys (element << 32 | rank) are formed on the GPU from the as-built footprints
+    // (k_fp_keys, one thread per input net, in place: the radix sort makes the order irrelevant)
+    hvec<int64_t> fp_start(N + 1);
+    fp_start[0] = 0;
+    par_for(N, nthr, [&](int64_t net) {
         const Chunk &ch = chunks[chunk_of[net]];
         const int64_t i = net - ch.beg;
-        fp_pos[r + 1] = ch.fp_off[i + 1] - ch.fp_off[i];
+        fp_start[net + 1] = ch.fp_off[i + 1] - ch.fp_off[i];
     });
-    par_prefix(fp_pos.data() + 1, N, nthr);
-    const int64_t n_fp = fp_pos[N];
+    par_prefix(fp_start.data() + 1, N, nthr);
+    const int64_t n_fp = fp_start[N];
     phase("  footprint offsets");
-    hvec<uint64_t> keys(n_fp);
-    {
-        std::atomic<int64_t> nx{0};
-        auto fill = [&]() {
-            const int64_t step = 4096;
-            for (;;) {
-                int64_t a = nx.fetch_add(step);
-                if (a >= N) break;
-                for (int64_t r = a; r < std::min(N, a + step); r++) {
-                    int64_t net = by_rank[r];
-                    const Chunk &ch = chunks[chunk_of[net]];
-                    int64_t i = net - ch.beg;
-                    int64_t o = fp_pos[r];
-                    for (int64_t k = ch.fp_off[i]; k < ch.fp_off[i + 1]; k++) keys[o++] = (ch.acc.fp[k] << 32) | (uint64_t)r;
-                }
-            }
-        };
-        std::vector<std::thread> th;
-        for (unsigned i = 1; i < nthr; i++) th.emplace_back(fill);
-        fill();
-        for (auto &t : th) t.join();
-    }
     int elem_bits = 1;
     while (((uint64_t)1 << elem_bits) < (uint64_t)3 * ctx->X * ctx->Y) elem_bits++;
     auto t1 = std::chrono::steady_clock::now();
@@ -1331,11 +1313,30 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
             nb = std::max(nb, b + 1);
         }
     } else {
-        cudaError_t e = gpu_conflict_batches(keys.data(), n_fp, elem_bits, N, batch_of_rank, nb, ctx->stream,
-                                             &ctx->stats.launches, &dag);
+        up_thr.join();   // the footprints must have landed
+        CK(up_err);
+        hvec<int32_t> rank_of(N);
+        par_for(N, nthr, [&](int64_t r) { rank_of[by_rank[r]] = (int32_t)r; });
+        uint64_t *d_keys = nullptr;
+        int64_t *d_fps = nullptr;
+        int32_t *d_rank = nullptr;
+        cudaError_t e = dmalloc(&d_keys, sizeof(uint64_t) * (size_t)std::max<int64_t>(n_fp, 1));
+        if (e == cudaSuccess) e = dmalloc(&d_fps, sizeof(int64_t) * (size_t)(N + 1));
+        if (e == cudaSuccess) e = dmalloc(&d_rank, sizeof(int32_t) * (size_t)std::max<int64_t>(N, 1));
+        if (e == cudaSuccess) e = pinned_copy(d_fps, fp_start.data(), sizeof(int64_t) * (size_t)(N + 1), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = pinned_copy(d_rank, rank_of.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = launch_fp_keys(d_fp_raw, d_fps, d_rank, N, d_keys, ctx->stream);
+        ctx->stats.h2d_bytes += 8 * (N + 1) + 4 * N;
+        ctx->stats.launches += 1;
+        if (e == cudaSuccess)
+            e = gpu_conflict_batches(nullptr, d_keys, n_fp, elem_bits, N, batch_of_rank, nb, ctx->stream,
+                                     &ctx->stats.launches, &dag);
+        cudaStreamSynchronize(ctx->stream);
+        dfree(d_keys);
+        dfree(d_fps);
+        dfree(d_rank);
         if (e != cudaSuccess) { dag.release(); return cuda_fail(ctx, e, "conflict-free batching"); }
     }
-    hvec<uint64_t>().swap(keys);
     auto t2 = std::chrono::steady_clock::now();
     ctx->batch_of_net.assign(N, 0);
     par_for(N, nthr, [&](int64_t r) { ctx->batch_of_net[by_rank[r]] = batch_of_rank[r]; });
@@ -1517,7 +1518,7 @@ la_status la_load_nets(la_ctx *ctx, const la_net_desc *n, int32_t *n_batches) {
     phase("forest source offsets");
 
     // the as-built arrays were uploaded by the background thread started after the build
-    up_thr.join();
+    if (up_thr.joinable()) up_thr.join();
     CK(up_err);
     ctx->stats.h2d_bytes += up_bytes;
     int64_t *d_srcn = nullptr, *d_srcs = nullptr, *d_dsts = nullptr;

@@ -245,9 +245,13 @@ struct DagDev {
     DagDev &operator=(const DagDev &) = delete;
     ~DagDev() { release(); }
 };
-cudaError_t gpu_conflict_batches(const uint64_t *h_keys, int64_t n_keys, int elem_bits, int64_t n_nets,
-                                 std::vector<int32_t> &batch_of_rank, int32_t &n_batches, cudaStream_t s,
-                                 int64_t *launches, DagDev *dag);
+// keys: host (h_keys) or device (d_keys, not owned) array of n_keys.
+cudaError_t gpu_conflict_batches(const uint64_t *h_keys, const uint64_t *d_keys, int64_t n_keys, int elem_bits,
+                                 int64_t n_nets, std::vector<int32_t> &batch_of_rank, int32_t &n_batches,
+                                 cudaStream_t s, int64_t *launches, DagDev *dag);
+// k_fp_keys: keys[j] = fp[j] << 32 | rank[net] for j in [start[net], start[net + 1]), nets [0, n).
+cudaError_t launch_fp_keys(const uint64_t *fp, const int64_t *start, const int32_t *rank, int64_t n, uint64_t *keys,
+                           cudaStream_t s);
 // pos_of_rank / rank_of_pos: host arrays [n].  Outputs (device, caller frees
 // with cudaFree): off_p [n+1], succ_p [n_edges], indeg_p [n], all in positions.
 cudaError_t gpu_dag_to_positions(DagDev &dag, const int64_t *h_rank_of_pos, int64_t **off_p, int32_t **succ_p,
